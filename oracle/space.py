@@ -1,0 +1,182 @@
+"""CPU enumeration of the v0 schedule space -- TEST INFRASTRUCTURE ONLY.
+
+Independent Python mirror of the schedule space that ``libtp`` enumerates in
+C++ (paper_2008_03602_b200/csrc/space.cpp).  The two share no code; both are
+written from the declarative knob table in DESIGN.md section "Schedule space
+v0".  ``north_star`` requires "schedule selection and indexing must be
+bit-exact against a CPU enumeration of the same search space"; this module is
+that CPU enumeration (SURVEY.md 8(c) check P-S).
+
+Paper basis: the knobs a conv2d autotuner searches are "loop tiles and
+ordering, caching, and loop unrolling ... CUDA threading";
+the first batch is random when no training data exists; selection
+keeps the fastest profiled configuration.  Readings C13
+(tie -> lowest index), C16 (trials = distinct candidates, >= |space| means
+exhaustive) and C17 (SplitMix64 + partial Fisher-Yates) are DESIGN.md's.
+"""
+from __future__ import annotations
+
+import itertools
+import math
+
+KIND_IGEMM_TC = 0
+KIND_DIRECT = 1
+DTYPE_BF16 = 0
+DTYPE_FP32 = 1
+SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
+
+TC_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("bk", (16, 32, 64, 128)),
+            ("stages", (2, 3, 4, 6)), ("threads", (128, 256)), ("split_k", (1, 2, 4, 8)))
+DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
+                ("tile_p", (1, 2, 4, 8)), ("smem_stage", (0, 1)))
+
+
+def _np2(v: int) -> int:
+    p = 1
+    while p < v:
+        p *= 2
+    return p
+
+
+def _cdiv(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def out_pq(d: dict) -> tuple[int, int]:
+    P = (d["h"] + 2 * d["pad_h"] - d.get("dil_h", 1) * (d["r"] - 1) - 1) // d["stride_h"] + 1
+    Q = (d["w"] + 2 * d["pad_w"] - d.get("dil_w", 1) * (d["s"] - 1) - 1) // d["stride_w"] + 1
+    return P, Q
+
+
+def layer_kind(d: dict) -> int:
+    """One kind per layer: tensor cores for bf16 dense layers whose
+    channel counts meet the TMA/vector alignment, CUDA cores otherwise."""
+    if (d["dtype"] == DTYPE_BF16 and d.get("groups", 1) == 1 and d["c"] % 8 == 0
+            and d["k"] % 8 == 0 and d.get("dil_h", 1) == 1 and d.get("dil_w", 1) == 1):
+        return KIND_IGEMM_TC
+    return KIND_DIRECT
+
+
+def direct_lanes(d: dict, threads: int, tile_q: int, vec_k: int, tile_p: int) -> tuple[int, int]:
+    """(lanes_k, lanes_q): threads are split into lanes along K (power of two,
+    capped so every output row of the CTA gets at least one thread) and Q."""
+    kv = _cdiv(d["k"], vec_k)
+    lanes_k = min(_np2(kv), threads // tile_p)
+    lanes_q = threads // (lanes_k * tile_p)
+    return lanes_k, lanes_q
+
+
+def direct_smem_bytes(d: dict, threads: int, tile_q: int, vec_k: int, tile_p: int) -> int:
+    lanes_k, lanes_q = direct_lanes(d, threads, tile_q, vec_k, tile_p)
+    qt, kt = lanes_q * tile_q, lanes_k * vec_k
+    rows_in = (tile_p - 1) * d["stride_h"] + d["r"]
+    cols_in = (qt - 1) * d["stride_w"] + d["s"]
+    if d.get("groups", 1) == 1:
+        cc = min(d["c"], 16)
+        return 4 * (rows_in * cols_in * cc + d["r"] * d["s"] * cc * kt)
+    return 4 * (rows_in * cols_in * kt + d["r"] * d["s"] * kt)
+
+
+def _valid_tc(d: dict, bm, bn, bk, stages, threads, split_k) -> bool:
+    P, Q = out_pq(d)
+    M = d["n"] * P * Q
+    if stages * (bm + bn) * bk * 2 + 1024 > SMEM_LIMIT:
+        return False
+    if bn > max(32, _np2(d["k"])) or bm > max(64, _np2(M)) or bk > max(16, _np2(d["c"])):
+        return False
+    return split_k <= d["r"] * d["s"] * _cdiv(d["c"], bk)
+
+
+def _valid_direct(d: dict, threads, tile_q, vec_k, tile_p, smem_stage) -> bool:
+    P, Q = out_pq(d)
+    if tile_q > Q or tile_p > P or vec_k > d["k"]:
+        return False
+    if d.get("groups", 1) != 1 and d["c"] % vec_k != 0:
+        return False
+    if smem_stage and direct_smem_bytes(d, threads, tile_q, vec_k, tile_p) > SMEM_LIMIT:
+        return False
+    return True
+
+
+def enumerate_space(d: dict) -> list[dict]:
+    """Valid schedules in lexicographic knob order (outermost knob first);
+    ``space_index`` is the rank among the valid tuples."""
+    kind = layer_kind(d)
+    knobs, valid = (TC_KNOBS, _valid_tc) if kind == KIND_IGEMM_TC else (DIRECT_KNOBS, _valid_direct)
+    names = [k for k, _ in knobs]
+    out = []
+    for combo in itertools.product(*[v for _, v in knobs]):
+        if valid(d, *combo):
+            s = dict(zip(names, combo))
+            s["kind"] = kind
+            s["space_index"] = len(out)
+            s.update(geometry(d, s))
+            out.append(s)
+    return out
+
+
+def geometry(d: dict, s: dict) -> dict:
+    """Frozen launch geometry of a schedule (grid, threads per CTA)."""
+    P, Q = out_pq(d)
+    if s.get("kind", layer_kind(d)) == KIND_IGEMM_TC:
+        M = d["n"] * P * Q
+        g = (_cdiv(M, s["bm"]), _cdiv(d["k"], s["bn"]), s["split_k"])
+    else:
+        lanes_k, lanes_q = direct_lanes(d, s["threads"], s["tile_q"], s["vec_k"], s["tile_p"])
+        g = (_cdiv(Q, lanes_q * s["tile_q"]) * _cdiv(P, s["tile_p"]),
+             _cdiv(d["k"], lanes_k * s["vec_k"]), d["n"])
+    return {"grid_x": g[0], "grid_y": g[1], "grid_z": g[2], "threads_per_cta": s["threads"],
+            "ctas": g[0] * g[1] * g[2]}
+
+
+def waves(ctas: int, sm_granted: int, ctas_per_sm: int) -> int:
+    """Waves = ceil(CTAs / (SM_granted * CTAs_per_SM))."""
+    return _cdiv(ctas, sm_granted * max(1, ctas_per_sm))
+
+
+MASK64 = (1 << 64) - 1
+
+
+def splitmix64(state: int):
+    """Generator of SplitMix64 outputs from ``state`` (C17)."""
+    while True:
+        state = (state + 0x9E3779B97F4A7C15) & MASK64
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+        yield z ^ (z >> 31)
+
+
+def sample(n_space: int, trials: int, seed: int) -> list[int]:
+    """trials >= |space| -> all of it in order; else partial Fisher-Yates over
+    0..n-1 driven by SplitMix64(seed), j = i + next() mod (n - i)."""
+    if trials >= n_space:
+        return list(range(n_space))
+    a = list(range(n_space))
+    rng = splitmix64(seed & MASK64)
+    for i in range(trials):
+        j = i + next(rng) % (n_space - i)
+        a[i], a[j] = a[j], a[i]
+    return a[:trials]
+
+
+def argmin(records: list[dict]) -> int:
+    """Index into ``records`` of the best OK record: min median_us, ties to the
+    lowest space_index (C13). Returns -1 if none is OK."""
+    best = -1
+    for i, r in enumerate(records):
+        if r["status"] != 0:
+            continue
+        if best < 0:
+            best = i
+            continue
+        b = records[best]
+        if r["median_us"] < b["median_us"] or (r["median_us"] == b["median_us"]
+                                               and r["space_index"] < b["space_index"]):
+            best = i
+    return best
+
+
+def requested_sms(fraction: float, total_sms: int = 148) -> int:
+    """requested = floor(total * p) (C14; SPEC's floor rule); 1.0 -> whole device."""
+    return max(1, int(math.floor(total_sms * fraction + 1e-9)))

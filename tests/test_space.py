@@ -1,0 +1,118 @@
+"""Pins for the CPU schedule-space enumeration (oracle/space.py), and
+bit-exact agreement of libtp's host-only space functions with it (P-S)."""
+import numpy as np
+import pytest
+
+from oracle import space as sp
+from paper_2008_03602_b200 import workloads as wl
+
+
+def test_splitmix64_reference_vector():
+    # Published SplitMix64 outputs for seed 0 (Vigna's reference implementation).
+    g = sp.splitmix64(0)
+    assert next(g) == 0xE220A8397B1DCDAF
+    assert next(g) == 0x6E789E6AA1B965F4
+    assert next(g) == 0x06C45D188009454F
+
+
+def test_sample_properties():
+    for n, t, seed in [(100, 10, 1), (920, 1000, 7), (5, 5, 3), (384, 383, 42), (1, 1, 0)]:
+        s = sp.sample(n, t, seed)
+        assert len(s) == min(n, t)
+        assert len(set(s)) == len(s)
+        assert all(0 <= i < n for i in s)
+        assert s == sp.sample(n, t, seed)
+    assert sp.sample(10, 20, 0) == list(range(10))
+    assert sp.sample(1000, 10, 1) != sp.sample(1000, 10, 2)
+
+
+def test_argmin_tie_break():
+    recs = [dict(status=0, median_us=5.0, space_index=9), dict(status=4, median_us=1.0, space_index=1),
+            dict(status=0, median_us=5.0, space_index=3), dict(status=0, median_us=6.0, space_index=0)]
+    assert sp.argmin(recs) == 2
+    assert sp.argmin([dict(status=5, median_us=1.0, space_index=0)]) == -1
+
+
+def test_space_counts_and_order():
+    # Totals cross-checked against SURVEY.md 8(a) a2's independent count of the same
+    # predicate (R50 14,432; VGG-19 6,672).
+    assert sum(len(sp.enumerate_space(d)) for d in wl.catalog("resnet50")) == 14432
+    assert sum(len(sp.enumerate_space(d)) for d in wl.catalog("vgg19_b16")) == 6672
+    d = wl.catalog("resnet50")[2]
+    s = sp.enumerate_space(d)
+    keys = [(x["bm"], x["bn"], x["bk"], x["stages"], x["threads"], x["split_k"]) for x in s]
+    assert keys == sorted(keys)
+    assert [x["space_index"] for x in s] == list(range(len(s)))
+
+
+def test_kind_selection():
+    r50 = wl.catalog("resnet50")
+    assert sp.layer_kind(r50[0]) == sp.KIND_DIRECT          # C = 3 stem
+    assert all(sp.layer_kind(d) == sp.KIND_IGEMM_TC for d in r50[1:])
+    assert sp.layer_kind(wl.catalog("cfg1")[0]) == sp.KIND_DIRECT   # fp32
+    mb = wl.catalog("mobilenetv2")
+    assert all(sp.layer_kind(d) == sp.KIND_DIRECT for d in mb if d["groups"] > 1)
+
+
+def test_waves_example():
+    # R50 l1.b0.c2 with 128x64 tiles -> 25 CTAs.
+    d = wl.catalog("resnet50")[2]
+    g = sp.geometry(d, dict(kind=0, bm=128, bn=64, split_k=1, threads=128))
+    assert g["ctas"] == 25
+    assert [sp.waves(25, m, 1) for m in (16, 32, 72, 148)] == [2, 1, 1, 1]
+    assert [sp.waves(100, m, 1) for m in (16, 32, 72, 148)] == [7, 4, 2, 1]
+
+
+# ---------------- libtp host-only functions vs the mirror (bit-exact) ----------------
+def _lib_or_skip():
+    try:
+        from paper_2008_03602_b200 import tp
+        return tp
+    except Exception as e:  # pragma: no cover
+        pytest.fail(f"libtp.so failed to load: {e}")
+
+
+SHAPES = wl.catalog("cfg1") + wl.catalog("resnet50") + wl.catalog("vgg19_b16") + wl.catalog("mobilenetv2")
+
+
+@pytest.mark.parametrize("d", SHAPES, ids=[d["name"] for d in SHAPES])
+def test_libtp_space_matches_mirror(d):
+    tp = _lib_or_skip()
+    mirror = sp.enumerate_space(d)
+    assert tp.space_size(d) == len(mirror)
+    fields_tc = ("bm", "bn", "bk", "stages", "threads", "split_k")
+    fields_dir = ("threads", "tile_q", "vec_k", "tile_p", "smem_stage")
+    for m in mirror:
+        s = tp.space_get(d, m["space_index"])
+        assert s["kind"] == m["kind"]
+        for f in (fields_tc if m["kind"] == sp.KIND_IGEMM_TC else fields_dir):
+            assert s[f] == m[f], (f, m)
+        assert (s["grid_x"], s["grid_y"], s["grid_z"]) == (m["grid_x"], m["grid_y"], m["grid_z"])
+        assert s["space_index"] == m["space_index"]
+
+
+@pytest.mark.parametrize("trials,seed", [(10, 42), (100, 43), (1000, 44), (5000, 45), (1, 0)])
+def test_libtp_sampler_matches_mirror(trials, seed):
+    tp = _lib_or_skip()
+    for d in wl.catalog("resnet50")[:6]:
+        n = tp.space_size(d)
+        assert tp.space_sample(d, trials, seed) == sp.sample(n, trials, seed)
+
+
+def test_libtp_argmin_matches_mirror():
+    tp = _lib_or_skip()
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        n = int(rng.integers(1, 50))
+        recs = [dict(status=int(rng.choice([0, 0, 0, 5])), median_us=float(rng.choice([1.5, 2.0, 2.5, 3.0])),
+                     space_index=int(i)) for i in rng.permutation(n)]
+        assert tp.select_best(recs) == sp.argmin(recs)
+
+
+def test_libtp_output_shape():
+    tp = _lib_or_skip()
+    for d in SHAPES:
+        assert tp.output_shape(d) == sp.out_pq(d)
+    bad = dict(SHAPES[1], h=0)
+    with pytest.raises(tp.TPError):
+        tp.output_shape(bad)
