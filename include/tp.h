@@ -1,0 +1,215 @@
+/*
+ * tp.h -- C ABI of libtp: SM-share-aware conv2d autotuning on B200 (sm_100a).
+ *
+ * The three calls of the paper's problem statement (arXiv 2008.03602):
+ *   - run a conv2d operator with a schedule under a GPU% limit
+ *       PAPER.md P:175 (GPU% = number of SMs an application can use), P:378,
+ *       P:388 (conv2d "operator"), P:254 (2D convolution)          -> tp_conv2d_run
+ *   - tune an operator at a GPU% to its best configuration
+ *       P:257-267 (select -> build -> profile -> search), P:586 (fixed trials
+ *       per operator), P:841 (combine per-operator best results)     -> tp_tune / tp_tune_subset
+ *   - infer with a schedule tuned at p% under a q% limit
+ *       P:385-399 (tuned-at-p x inferred-at-q tables T1-T3),
+ *       P:560-566 (thread counts frozen at tuning time)             -> tp_cross_eval
+ * plus the spatial partitioner that gives each tuner a fixed SM share
+ *       P:175, P:378, P:832-834 (TSI scaling with distinct GPU%)    -> tp_partition_*
+ *
+ * Conventions (all functions):
+ *   - Every function returns tp_status; nothing throws or aborts across the ABI.
+ *     On failure a thread-local message is available from tp_last_error().
+ *   - Device pointers (x, w, bias, y, ws) are device memory of the *primary*
+ *     context of `device` (e.g. PyTorch allocations); the caller owns them.
+ *     Host arrays (records, check_*, out structs) are owned by the caller.
+ *   - libtp owns green contexts, their streams and events, TMA descriptors and
+ *     the kernel instantiation table; tp_shutdown() frees them.
+ *   - Host-only functions (tp_space_*, tp_output_shape, tp_select_best,
+ *     tp_status_str, tp_last_error) never touch the GPU and work without one.
+ *   - Threading: one tuner thread per partition; calls on *different*
+ *     partitions may run concurrently from different host threads (a green
+ *     context may be current to one thread at a time, cuda.h cuGreenCtxCreate).
+ *
+ * Layouts:
+ *   x : NHWC (in_layout = TP_LAYOUT_NHWC) or NCHW (TP_LAYOUT_NCHW; a transpose
+ *       pre-pass into the workspace runs inside the call and is timed with it)
+ *   w : KRSC = [K][R][S][C/groups], dtype = desc.dtype
+ *   bias : fp32 [K] (read iff epilogue bit0)
+ *   y : same layout as x, dtype = desc.out_dtype
+ */
+#ifndef TP_H_
+#define TP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TP_OK = 0,
+    TP_EINVAL = 1,            /* bad descriptor / argument (readings C3-C6)             */
+    TP_EINVALID_CONFIG = 2,   /* schedule not in the layer's space          */
+    TP_ECAPACITY = 3,         /* requested SM partition cannot be granted   */
+    TP_ECUDA = 4,             /* driver / launch error ("server_error")      */
+    TP_EMISMATCH = 5,         /* correctness gate failed        */
+    TP_EUNSUPPORTED = 6       /* valid conv, not on the GPU path (e.g. dilation > 1)     */
+} tp_status;
+
+enum { TP_LAYOUT_NHWC = 0, TP_LAYOUT_NCHW = 1 };
+enum { TP_DTYPE_BF16 = 0, TP_DTYPE_FP32 = 1 };
+enum { TP_EPI_BIAS = 1, TP_EPI_RELU = 2 };
+enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1 };
+
+/* One conv2d operator ("tuning task", P:947 [src]).  P/Q follow reading C3:
+ * P = floor((h + 2 pad_h - dil_h (r-1) - 1) / stride_h) + 1; P < 1 -> TP_EINVAL. */
+typedef struct {
+    int32_t n, c, h, w, k, r, s;
+    int32_t stride_h, stride_w, pad_h, pad_w, dil_h, dil_w, groups;
+    int32_t in_layout;   /* TP_LAYOUT_*                       */
+    int32_t dtype;       /* input/weight dtype, TP_DTYPE_*     */
+    int32_t out_dtype;   /* output dtype, TP_DTYPE_*           */
+    int32_t epilogue;    /* bit0 bias, bit1 relu (TP_EPI_*)    */
+} tp_conv_desc;
+
+/* One configuration of the operator's schedule space (P:256 knobs; DESIGN.md
+ * "Schedule space v0").  IGEMM_TC uses bm,bn,bk,stages,threads,split_k; DIRECT
+ * uses threads,tile_q,vec_k,tile_p,smem_stage.  grid_* is the frozen launch
+ * geometry (reading C15): filled by tp_space_get, reused by tp_cross_eval. */
+typedef struct {
+    int32_t kind;
+    int32_t bm, bn, bk, stages, threads, split_k;
+    int32_t tile_q, vec_k, tile_p, smem_stage;
+    int32_t reserved;
+    int64_t space_index;                       /* rank in the layer's valid space */
+    int32_t grid_x, grid_y, grid_z, sm_tuned;  /* frozen geometry; sm_tuned = SMs at tune time */
+} tp_schedule;
+
+/* One profiled configuration ("measures the execution time"; the
+ * thread/wave fields are the paper's thread-count mechanism). */
+typedef struct {
+    double median_us, min_us, mean_us, std_us;   /* per-launch latency over groups (C12) */
+    int32_t n_per_group, groups;
+    int32_t sm_requested, sm_granted, device, status;   /* status: tp_status of this candidate */
+    int64_t space_index;
+    int64_t ctas;
+    int32_t threads_per_cta, waves, ctas_per_sm, kind;
+    double max_abs_err, max_ref;                 /* correctness gate (a10)               */
+} tp_measurement;
+
+/* Timing protocol (reading C12). NULL -> defaults {3, 5, 10, 20.0, 1, 0}. */
+typedef struct {
+    int32_t warmup;           /* untimed launches before timing                      */
+    int32_t groups;           /* r: number of timed groups (median over groups)      */
+    int32_t n_min;            /* minimum launches per group                          */
+    double target_group_us;   /* n = max(n_min, ceil(target / t_est))                */
+    int32_t use_graph;        /* capture each group's n launches as one CUDA graph    */
+    int32_t flush_l2;         /* 1: write a > L2 buffer before every launch (cold L2) */
+} tp_timing;
+
+typedef struct tp_partition tp_partition;   /* opaque: green context + stream (or whole device) */
+
+/* ---- library lifetime -------------------------------------------------- */
+tp_status tp_init(int32_t device);          /* idempotent; primary context + driver entry points */
+void tp_shutdown(void);                     /* destroys cached partitions, events, buffers       */
+const char* tp_status_str(tp_status s);
+const char* tp_last_error(void);            /* thread-local message of the last failure          */
+int64_t tp_launch_count(void);              /* kernels launched by libtp so far (all threads)    */
+
+/* ---- partitions: "GPU%" as an SM share ------------
+ * tp_partition_get: cached per (device, fraction, flags) -- created once and
+ * reused, the long-lived-server analog of P:844-846.  fraction in (0, 1];
+ * 1.0 -> whole device (no green context, own non-blocking stream).
+ * requested = floor(sm_count * fraction) (reading C14); the granted count is
+ * what the driver returns (multiples of 8 unless flags has
+ * TP_PART_FINE_GRAINED = CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING).
+ * TP_ECAPACITY if the driver cannot grant at least `requested` SMs. */
+enum { TP_PART_FINE_GRAINED = 1 };
+tp_status tp_partition_get(int32_t device, double fraction, int32_t flags, tp_partition** part,
+                           int32_t* sm_requested, int32_t* sm_granted);
+/* k disjoint partitions of sms_each SMs from ONE split (config 4: concurrent
+ * tuners).  parts[k], granted[k] filled.  Not cached: close each. */
+tp_status tp_partition_split(int32_t device, int32_t k, int32_t sms_each, int32_t flags,
+                             tp_partition** parts, int32_t* granted);
+tp_status tp_partition_info(tp_partition* part, int32_t* device, int32_t* sm_requested,
+                            int32_t* sm_granted, void** cu_stream);
+tp_status tp_partition_sync(tp_partition* part);
+tp_status tp_partition_close(tp_partition* part);   /* only for tp_partition_split handles */
+/* %smid probe: launches `ctas` CTAs in the partition, each writes its SM id
+ * to smids[i] (device int32 buffer).  Used to verify partition membership. */
+tp_status tp_partition_probe(tp_partition* part, int32_t ctas, int32_t* smids_dev);
+/* STREAM-copy probe inside the partition: copies `bytes` from src to dst
+ * (device buffers) `reps` times; returns the best achieved GB/s (read+write). */
+tp_status tp_partition_copy_bw(tp_partition* part, const void* src, void* dst, size_t bytes,
+                               int32_t reps, double* gbps);
+
+/* ---- schedule space (host-only) ------------ */
+tp_status tp_output_shape(const tp_conv_desc* d, int32_t* p, int32_t* q);
+tp_status tp_layer_kind(const tp_conv_desc* d, int32_t* kind);
+tp_status tp_space_size(const tp_conv_desc* d, int64_t* n_valid);
+tp_status tp_space_get(const tp_conv_desc* d, int64_t idx, tp_schedule* out);
+/* trials >= |space| -> 0..n-1 in order; else SplitMix64(seed) partial
+ * Fisher-Yates (reading C17).  *n_out = min(trials, |space|) <= cap. */
+tp_status tp_space_sample(const tp_conv_desc* d, int32_t trials, uint64_t seed,
+                          int64_t* idx_out, int32_t cap, int32_t* n_out);
+/* argmin over status==TP_OK records by median_us, ties -> lowest space_index
+ * (reading C13).  *best = index into records, or -1 if none is OK. */
+tp_status tp_select_best(const tp_measurement* records, int32_t n, int32_t* best);
+
+/* ---- running the operator --------------------------------------------- */
+/* Bytes of device workspace a (desc, schedule) needs (split-K partials +
+ * counters, NCHW transpose buffers).  The workspace must be zero-filled
+ * before its first use; libtp leaves it zeroed after each completed call. */
+tp_status tp_workspace_size(const tp_conv_desc* d, const tp_schedule* s, size_t* bytes);
+/* Max workspace over the layer's whole space (for tuning). */
+tp_status tp_workspace_size_max(const tp_conv_desc* d, size_t* bytes);
+
+/* Run conv2d(desc) with schedule `s` inside partition `part` (NULL = whole
+ * device).  timing == NULL: one asynchronous launch on the partition stream
+ * (tp_partition_sync to wait).  timing != NULL: the C12 protocol, result in
+ * *out (synchronous).  s->grid_* != 0 are taken as frozen geometry (C15). */
+tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part,
+                        const void* x, const void* w, const void* bias, void* y,
+                        void* ws, size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
+
+/* Tune: select candidates (a3), profile each inside `part` (a11) behind the
+ * correctness gate (a10), record (a12), return the argmin.
+ *   check_idx/check_ref/n_check : flat output indices (NKPQ logical) and
+ *     reference values (e.g. the fp64 oracle's); a candidate fails the gate if
+ *     max|y - ref| > tol * max|ref|.  n_check == 0 -> consensus gate: the first
+ *     OK candidate's values at 4096 fixed points become the reference.
+ *   tol <= 0 -> 2e-2 for bf16 inputs, 1e-5 for fp32 (north_star).
+ *   records (cap records_cap) receive one tp_measurement per candidate in
+ *   selection order; *n_records = number measured.
+ * Candidates whose launch fails get status TP_ECUDA and are excluded. */
+tp_status tp_tune(const tp_conv_desc* d, tp_partition* part, int32_t trials, uint64_t seed,
+                  const void* x, const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
+                  const int64_t* check_idx, const double* check_ref, int32_t n_check, double tol,
+                  const tp_timing* timing, tp_schedule* best, tp_measurement* best_m,
+                  tp_measurement* records, int32_t records_cap, int32_t* n_records);
+/* Same loop over an explicit candidate list (the sharder's unit of work,
+ * rank r measures idx = r mod G). */
+tp_status tp_tune_subset(const tp_conv_desc* d, tp_partition* part, const int64_t* cand_idx,
+                         int32_t n_cand, const void* x, const void* w, const void* bias, void* y,
+                         void* ws, size_t ws_bytes, const int64_t* check_idx, const double* check_ref,
+                         int32_t n_check, double tol, const tp_timing* timing,
+                         tp_measurement* records, int32_t records_cap, int32_t* n_records);
+
+/* Cross-evaluation: run schedule tuned at p (frozen geometry, reading C15)
+ * inside partition `part_q` with the timing protocol (a13). */
+tp_status tp_cross_eval(const tp_conv_desc* d, const tp_schedule* tuned_at_p, tp_partition* part_q,
+                        const void* x, const void* w, const void* bias, void* y, void* ws,
+                        size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
+
+/* ---- operand preparation (a5; outside the timed region) ----------------
+ * fp32 logical NCHW x -> layout/dtype of desc (NHWC or NCHW, bf16 RNE or fp32).
+ * fp32 logical KCRS w -> KRSC in desc.dtype.  Asynchronous on part's stream. */
+tp_status tp_pack_input(const tp_conv_desc* d, tp_partition* part, const float* x_nchw_f32, void* x_out);
+tp_status tp_pack_weights(const tp_conv_desc* d, tp_partition* part, const float* w_kcrs_f32, void* w_out);
+/* Gather y at flat NKPQ logical indices into fp64 host values (a10). */
+tp_status tp_gather_output(const tp_conv_desc* d, tp_partition* part, const void* y,
+                           const int64_t* idx_host, int32_t n, double* vals_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TP_H_ */

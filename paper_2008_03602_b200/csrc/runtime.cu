@@ -1,0 +1,917 @@
+// runtime.cu -- libtp device runtime: partitions (green contexts), launch plans,
+// the profiling protocol, the tuner and the C-ABI entry points of include/tp.h.
+//
+// Paper mapping:
+//  * GPU% = "the number of GPU Streaming Multiprocessors (SMs) that an
+//    application can use", set per process with MPS.  Here a
+//    partition is a CUDA green context holding a fixed SM group (reading C14).
+//  * The long-lived server avoids ~300 ms of context creation per
+//    configuration: partitions are created once per (device, fraction) and
+//    cached for the life of the process.
+//  * Select -> profile -> keep the best: tp_tune.
+//  * Tuned-at-p run-at-q: tp_cross_eval with frozen geometry (C15).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "tp_kernels.h"
+
+struct tp_partition {
+  int device = 0;
+  double fraction = 1.0;
+  int flags = 0;
+  int sm_requested = 0, sm_granted = 0;
+  bool green = false, cached = false;
+  CUgreenCtx gctx = nullptr;
+  CUcontext ctx = nullptr;
+  cudaStream_t stream = nullptr;
+  void* flush_buf = nullptr;   // device-owned L2 flush buffer (cold-L2 timing)
+  size_t flush_bytes = 0;
+  std::mutex mu;
+};
+
+namespace tp {
+
+static std::atomic<int64_t> g_launches{0};
+
+#define TP_CK(expr)                                                                          \
+  do {                                                                                       \
+    cudaError_t e__ = (expr);                                                                \
+    if (e__ != cudaSuccess) {                                                                \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(e__));                        \
+      return TP_ECUDA;                                                                       \
+    }                                                                                        \
+  } while (0)
+#define TP_CU(expr)                                                                          \
+  do {                                                                                       \
+    CUresult r__ = (expr);                                                                   \
+    if (r__ != CUDA_SUCCESS) {                                                               \
+      set_error(std::string(#expr) + " failed: CUresult " + std::to_string((int)r__));       \
+      return TP_ECUDA;                                                                       \
+    }                                                                                        \
+  } while (0)
+
+// ---------------------------------------------------------------- driver API
+template <class F>
+static void resolve(const char* name, F*& fp, bool& ok) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+      !p)
+    ok = false;
+  fp = reinterpret_cast<F*>(p);
+}
+
+const DriverApi& driver() {
+  static DriverApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    bool ok = true;
+    resolve("cuTensorMapEncodeTiled", api.encodeTiled, ok);
+    resolve("cuTensorMapEncodeIm2col", api.encodeIm2col, ok);
+    resolve("cuCtxPushCurrent", api.ctxPush, ok);
+    resolve("cuCtxPopCurrent", api.ctxPop, ok);
+    resolve("cuCtxGetCurrent", api.ctxGetCurrent, ok);
+    resolve("cuDeviceGet", api.deviceGet, ok);
+    resolve("cuDevicePrimaryCtxRetain", api.devicePrimaryCtxRetain, ok);
+    resolve("cuDeviceGetDevResource", api.deviceGetDevResource, ok);
+    resolve("cuDevSmResourceSplitByCount", api.devSmResourceSplitByCount, ok);
+    resolve("cuDevResourceGenerateDesc", api.devResourceGenerateDesc, ok);
+    resolve("cuGreenCtxCreate", api.greenCtxCreate, ok);
+    resolve("cuGreenCtxDestroy", api.greenCtxDestroy, ok);
+    resolve("cuCtxFromGreenCtx", api.ctxFromGreenCtx, ok);
+    resolve("cuGreenCtxStreamCreate", api.greenCtxStreamCreate, ok);
+    resolve("cuGreenCtxGetDevResource", api.greenCtxGetDevResource, ok);
+    resolve("cuStreamDestroy", api.streamDestroy, ok);
+    api.ok = ok;
+  });
+  return api;
+}
+
+// ---------------------------------------------------------------- device state
+struct DeviceState {
+  bool init = false;
+  int sm_count = 0;
+  int l2_bytes = 0;
+  CUcontext primary = nullptr;
+  std::unique_ptr<tp_partition> whole;
+  std::map<std::tuple<int, int>, std::unique_ptr<tp_partition>> parts;  // (requested, flags)
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
+};
+static std::mutex g_mu;
+static std::map<int, DeviceState> g_dev;
+
+static tp_status init_device(int device, DeviceState** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DeviceState& ds = g_dev[device];
+  if (!ds.init) {
+    const DriverApi& drv = driver();
+    if (!drv.ok) { set_error("CUDA driver entry points unavailable (no GPU driver?)"); return TP_ECUDA; }
+    int n = 0;
+    TP_CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) { set_error("bad device ordinal"); return TP_EINVAL; }
+    TP_CK(cudaSetDevice(device));
+    TP_CK(cudaFree(nullptr));
+    cudaDeviceProp prop;
+    TP_CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+      set_error("libtp kernels are built for sm_100a (B200); device is sm_" + std::to_string(prop.major) +
+                std::to_string(prop.minor));
+      return TP_EUNSUPPORTED;
+    }
+    ds.sm_count = prop.multiProcessorCount;
+    ds.l2_bytes = prop.l2CacheSize;
+    TP_CU(drv.ctxGetCurrent(&ds.primary));
+    auto w = std::make_unique<tp_partition>();
+    w->device = device; w->fraction = 1.0; w->sm_requested = w->sm_granted = ds.sm_count;
+    w->green = false; w->cached = true; w->ctx = ds.primary;
+    TP_CK(cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking));
+    ds.whole = std::move(w);
+    ds.flush_bytes = (size_t)std::max(2 * ds.l2_bytes, 256 << 20);
+    TP_CK(cudaMalloc(&ds.flush_buf, ds.flush_bytes));
+    ds.whole->flush_buf = ds.flush_buf;
+    ds.whole->flush_bytes = ds.flush_bytes;
+    ds.init = true;
+  }
+  if (out) *out = &ds;
+  return TP_OK;
+}
+
+// RAII: make the partition's context current in this thread.
+struct CtxGuard {
+  bool pushed = false;
+  explicit CtxGuard(tp_partition* p) {
+    cudaSetDevice(p->device);
+    if (driver().ctxPush(p->ctx) == CUDA_SUCCESS) pushed = true;
+  }
+  ~CtxGuard() {
+    if (pushed) { CUcontext c; driver().ctxPop(&c); }
+  }
+};
+
+static tp_status create_green(int device, int requested, int flags, tp_partition** out) {
+  const DriverApi& drv = driver();
+  CUdevice dev;
+  TP_CU(drv.deviceGet(&dev, device));
+  CUdevResource full;
+  TP_CU(drv.deviceGetDevResource(dev, &full, CU_DEV_RESOURCE_TYPE_SM));
+  unsigned nb = 1;
+  CUdevResource grp, rem;
+  const unsigned use = (flags & TP_PART_FINE_GRAINED) ? CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING : 0;
+  CUresult r = drv.devSmResourceSplitByCount(&grp, &nb, &full, &rem, use, (unsigned)requested);
+  if (r != CUDA_SUCCESS || nb < 1 || (int)grp.sm.smCount < requested) {
+    set_error("cannot grant " + std::to_string(requested) + " SMs (CUresult " + std::to_string((int)r) + ")");
+    return TP_ECAPACITY;
+  }
+  CUdevResourceDesc desc;
+  TP_CU(drv.devResourceGenerateDesc(&desc, &grp, 1));
+  auto p = std::make_unique<tp_partition>();
+  p->device = device; p->flags = flags; p->sm_requested = requested; p->sm_granted = (int)grp.sm.smCount;
+  p->green = true;
+  TP_CU(drv.greenCtxCreate(&p->gctx, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM));
+  TP_CU(drv.ctxFromGreenCtx(&p->ctx, p->gctx));
+  CUstream s;
+  TP_CU(drv.greenCtxStreamCreate(&s, p->gctx, CU_STREAM_NON_BLOCKING, 0));
+  p->stream = reinterpret_cast<cudaStream_t>(s);
+  *out = p.release();
+  return TP_OK;
+}
+
+static void destroy_partition(tp_partition* p) {
+  if (!p) return;
+  const DriverApi& drv = driver();
+  if (p->green) {
+    if (p->stream) drv.streamDestroy(reinterpret_cast<CUstream>(p->stream));
+    if (p->gctx) drv.greenCtxDestroy(p->gctx);
+  } else if (p->stream) {
+    cudaStreamDestroy(p->stream);
+  }
+  p->stream = nullptr;
+}
+
+// ---------------------------------------------------------------- conv plans
+struct ConvPlan {
+  Layer L;
+  tp_schedule s;
+  TcPlan tc;
+  DirectPlan dp;
+  bool nchw = false;
+  const void* x_user = nullptr;
+  void* y_user = nullptr;
+  void* x_nhwc = nullptr;
+  void* y_nhwc = nullptr;
+  int in_eb = 2, out_eb = 2;
+  int kernels_per_call = 1;
+  int ctas_per_sm = 1;
+};
+
+struct WsLayout {
+  size_t counters = 0, partials = 0, xbuf = 0, ybuf = 0, total = 0;
+};
+
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static WsLayout ws_layout(const Layer& L, const tp_schedule& s) {
+  WsLayout w;
+  size_t off = 0;
+  if (s.kind == TP_KIND_IGEMM_TC && s.split_k > 1) {
+    // The counter region depends on the layer only (sized for the smallest tile,
+    // 64 x 32), so partials of one schedule never land on another schedule's
+    // counters: every counter stays zero between completed launches.
+    const int64_t max_tiles = cdiv(L.M, 64) * cdiv(L.d.k, 32);
+    const int64_t tiles = cdiv(L.M, s.bm) * cdiv(L.d.k, s.bn);
+    w.counters = off; off = align256(off + (size_t)max_tiles * 4);
+    w.partials = off; off = align256(off + (size_t)s.split_k * tiles * s.bm * s.bn * 4);
+  }
+  if (L.d.in_layout == TP_LAYOUT_NCHW) {
+    const int ieb = L.d.dtype == TP_DTYPE_BF16 ? 2 : 4, oeb = L.d.out_dtype == TP_DTYPE_BF16 ? 2 : 4;
+    w.xbuf = off; off = align256(off + (size_t)L.d.n * L.d.c * L.d.h * L.d.w * ieb);
+    w.ybuf = off; off = align256(off + (size_t)L.M * L.d.k * oeb);
+  }
+  w.total = off;
+  return w;
+}
+
+static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* x, const void* w,
+                           const void* bias, void* y, void* ws, size_t ws_bytes, ConvPlan* plan) {
+  tp_schedule s = s_in;
+  if (!schedule_in_space(L, s)) {
+    set_error("schedule is not in this layer's v0 space");
+    return TP_EINVALID_CONFIG;
+  }
+  if (!x || !w || !y || ((L.d.epilogue & TP_EPI_BIAS) && !bias)) { set_error("null operand pointer"); return TP_EINVAL; }
+  const WsLayout wl = ws_layout(L, s);
+  if (wl.total > 0 && (!ws || ws_bytes < wl.total)) {
+    set_error("workspace too small: need " + std::to_string(wl.total) + " bytes");
+    return TP_EINVAL;
+  }
+  plan->L = L;
+  plan->s = s;
+  plan->nchw = L.d.in_layout == TP_LAYOUT_NCHW;
+  plan->x_user = x;
+  plan->y_user = y;
+  plan->in_eb = L.d.dtype == TP_DTYPE_BF16 ? 2 : 4;
+  plan->out_eb = L.d.out_dtype == TP_DTYPE_BF16 ? 2 : 4;
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  const void* xk = x;
+  void* yk = y;
+  plan->kernels_per_call = 1;
+  if (plan->nchw) {
+    plan->x_nhwc = wsb + wl.xbuf;
+    plan->y_nhwc = wsb + wl.ybuf;
+    xk = plan->x_nhwc;
+    yk = plan->y_nhwc;
+    plan->kernels_per_call = 3;
+  }
+  if (s.kind == TP_KIND_IGEMM_TC) {
+    if ((reinterpret_cast<uintptr_t>(xk) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(yk)) & 15) {
+      set_error("x, w, y must be 16-byte aligned for the tensor-core path");
+      return TP_EINVAL;
+    }
+    TcProblem pb;
+    std::memset(&pb, 0, sizeof(pb));
+    pb.x = xk; pb.w = w; pb.bias = reinterpret_cast<const float*>(bias); pb.y = yk;
+    pb.N = L.d.n; pb.C = L.d.c; pb.H = L.d.h; pb.W = L.d.w; pb.K = L.d.k; pb.R = L.d.r; pb.S = L.d.s;
+    pb.P = L.P; pb.Q = L.Q; pb.sh = L.d.stride_h; pb.sw = L.d.stride_w; pb.ph = L.d.pad_h; pb.pw = L.d.pad_w;
+    pb.M = L.M;
+    pb.bm = s.bm; pb.bn = s.bn; pb.bk = s.bk; pb.stages = s.stages; pb.threads = s.threads; pb.split_k = s.split_k;
+    pb.grid_x = s.grid_x; pb.grid_y = s.grid_y; pb.grid_z = s.grid_z;
+    pb.out_f32 = L.d.out_dtype == TP_DTYPE_FP32;
+    pb.relu = (L.d.epilogue & TP_EPI_RELU) ? 1 : 0;
+    pb.has_bias = (L.d.epilogue & TP_EPI_BIAS) ? 1 : 0;
+    pb.ws_counters = s.split_k > 1 ? reinterpret_cast<int*>(wsb + wl.counters) : nullptr;
+    pb.ws_partial = s.split_k > 1 ? reinterpret_cast<float*>(wsb + wl.partials) : nullptr;
+    tp_status st = tc_prepare(pb, &plan->tc);
+    if (st != TP_OK) return st;
+    plan->ctas_per_sm = tc_occupancy(plan->tc);
+  } else {
+    tp_status st = direct_prepare(L, s, xk, w, reinterpret_cast<const float*>(bias), yk, &plan->dp);
+    if (st != TP_OK) return st;
+    plan->ctas_per_sm = direct_occupancy(plan->dp);
+  }
+  return TP_OK;
+}
+
+static cudaError_t launch_plan(const ConvPlan& p, cudaStream_t st) {
+  cudaError_t e;
+  if (p.nchw) {
+    e = launch_nchw_to_nhwc(p.x_user, p.x_nhwc, p.L.d.n, p.L.d.c, p.L.d.h, p.L.d.w, p.in_eb, st);
+    if (e != cudaSuccess) return e;
+  }
+  e = p.s.kind == TP_KIND_IGEMM_TC ? tc_launch(p.tc, st) : direct_launch(p.dp, st);
+  if (e != cudaSuccess) return e;
+  if (p.nchw) {
+    e = launch_nhwc_to_nchw(p.y_nhwc, p.y_user, p.L.d.n, p.L.d.k, p.L.P, p.L.Q, p.out_eb, st);
+    if (e != cudaSuccess) return e;
+  }
+  g_launches += p.kernels_per_call;
+  return cudaSuccess;
+}
+
+static void plan_geometry(const ConvPlan& p, int sm_granted, tp_measurement* m) {
+  const dim3 g = p.s.kind == TP_KIND_IGEMM_TC ? p.tc.grid : p.dp.grid;
+  m->ctas = (int64_t)g.x * g.y * g.z;
+  m->threads_per_cta = p.s.threads;
+  m->ctas_per_sm = p.ctas_per_sm;
+  m->waves = (int32_t)cdiv(m->ctas, (int64_t)sm_granted * std::max(1, p.ctas_per_sm));
+  m->kind = p.s.kind;
+  m->space_index = p.s.space_index;
+}
+
+// ---------------------------------------------------------------- timing (C12)
+static tp_timing default_timing() {
+  tp_timing t;
+  t.warmup = 3; t.groups = 5; t.n_min = 10; t.target_group_us = 20.0; t.use_graph = 1; t.flush_l2 = 0;
+  return t;
+}
+
+struct EventPool {
+  std::vector<cudaEvent_t> ev;
+  ~EventPool() { for (auto e : ev) cudaEventDestroy(e); }
+  cudaError_t ensure(size_t n) {
+    while (ev.size() < n) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      ev.push_back(e);
+    }
+    return cudaSuccess;
+  }
+};
+
+// Caller holds the partition lock and has its context current.
+static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_timing& tm, EventPool& pool,
+                           tp_measurement* out) {
+  cudaStream_t st = part->stream;
+  const bool cold = tm.flush_l2 != 0;
+  auto flush = [&]() { return launch_l2_flush(part->flush_buf, part->flush_bytes, 148 * 4, st); };
+  for (int i = 0; i < std::max(0, tm.warmup); ++i) {
+    if (cold) TP_CK(flush());
+    TP_CK(launch_plan(plan, st));
+  }
+  const int groups = std::max(1, tm.groups);
+  std::vector<double> per;   // per-launch microseconds, one entry per group
+  if (cold) {
+    // Cold L2: flush outside each timed launch; one event pair per launch.
+    const int n = std::max(1, std::min(tm.n_min, 20));
+    TP_CK(pool.ensure(2 * (size_t)n * groups));
+    for (int g = 0; g < groups; ++g)
+      for (int i = 0; i < n; ++i) {
+        TP_CK(flush());
+        TP_CK(cudaEventRecord(pool.ev[2 * (g * n + i)], st));
+        TP_CK(launch_plan(plan, st));
+        TP_CK(cudaEventRecord(pool.ev[2 * (g * n + i) + 1], st));
+      }
+    TP_CK(cudaStreamSynchronize(st));
+    for (int g = 0; g < groups; ++g) {
+      double sum = 0;
+      for (int i = 0; i < n; ++i) {
+        float ms = 0;
+        TP_CK(cudaEventElapsedTime(&ms, pool.ev[2 * (g * n + i)], pool.ev[2 * (g * n + i) + 1]));
+        sum += ms * 1000.0;
+      }
+      per.push_back(sum / n);
+    }
+    out->n_per_group = n;
+  } else {
+    // Estimate, then size groups to >= target_group_us.
+    TP_CK(pool.ensure(2 * (size_t)groups + 2));
+    const int n0 = std::max(1, tm.n_min);
+    TP_CK(cudaEventRecord(pool.ev[0], st));
+    for (int i = 0; i < n0; ++i) TP_CK(launch_plan(plan, st));
+    TP_CK(cudaEventRecord(pool.ev[1], st));
+    TP_CK(cudaEventSynchronize(pool.ev[1]));
+    float ms0 = 0;
+    TP_CK(cudaEventElapsedTime(&ms0, pool.ev[0], pool.ev[1]));
+    const double t_est = std::max(1e-3, ms0 * 1000.0 / n0);
+    int n = std::max(n0, (int)std::ceil(tm.target_group_us / t_est));
+    n = std::min(n, 4096);
+    cudaGraphExec_t exec = nullptr;
+    if (tm.use_graph) {
+      cudaGraph_t graph = nullptr;
+      TP_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      cudaError_t ce = cudaSuccess;
+      for (int i = 0; i < n && ce == cudaSuccess; ++i) ce = launch_plan(plan, st);
+      cudaError_t ee = cudaStreamEndCapture(st, &graph);
+      g_launches -= (int64_t)n * plan.kernels_per_call;   // capture does not launch
+      if (ce != cudaSuccess || ee != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        set_error(std::string("graph capture failed: ") + cudaGetErrorString(ce != cudaSuccess ? ce : ee));
+        return TP_ECUDA;
+      }
+      cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      TP_CK(ie);
+    }
+    for (int g = 0; g < groups; ++g) {
+      TP_CK(cudaEventRecord(pool.ev[2 + 2 * g], st));
+      if (exec) {
+        TP_CK(cudaGraphLaunch(exec, st));
+        g_launches += (int64_t)n * plan.kernels_per_call;
+      } else {
+        for (int i = 0; i < n; ++i) TP_CK(launch_plan(plan, st));
+      }
+      TP_CK(cudaEventRecord(pool.ev[3 + 2 * g], st));
+    }
+    cudaError_t se = cudaStreamSynchronize(st);
+    if (exec) cudaGraphExecDestroy(exec);
+    TP_CK(se);
+    for (int g = 0; g < groups; ++g) {
+      float ms = 0;
+      TP_CK(cudaEventElapsedTime(&ms, pool.ev[2 + 2 * g], pool.ev[3 + 2 * g]));
+      per.push_back(ms * 1000.0 / n);
+    }
+    out->n_per_group = n;
+  }
+  std::vector<double> sorted = per;
+  std::sort(sorted.begin(), sorted.end());
+  const size_t k = sorted.size();
+  out->median_us = (k % 2) ? sorted[k / 2] : 0.5 * (sorted[k / 2 - 1] + sorted[k / 2]);
+  out->min_us = sorted.front();
+  double mean = 0;
+  for (double v : per) mean += v;
+  mean /= k;
+  double var = 0;
+  for (double v : per) var += (v - mean) * (v - mean);
+  out->mean_us = mean;
+  out->std_us = k > 1 ? std::sqrt(var / (k - 1)) : 0.0;
+  out->groups = groups;
+  return TP_OK;
+}
+
+// ---------------------------------------------------------------- correctness gate (a10)
+struct Gate {
+  std::vector<int64_t> idx;
+  std::vector<double> ref;
+  bool have_ref = false;
+  double tol = 0;
+  int64_t* d_idx = nullptr;
+  double* d_vals = nullptr;
+  std::vector<double> vals;
+  ~Gate() {
+    if (d_idx) cudaFree(d_idx);
+    if (d_vals) cudaFree(d_vals);
+  }
+};
+
+static tp_status gate_setup(const Layer& L, const int64_t* check_idx, const double* check_ref, int32_t n_check,
+                            double tol, Gate* g) {
+  const int64_t total = L.M * L.d.k;
+  if (n_check > 0) {
+    g->idx.assign(check_idx, check_idx + n_check);
+    g->ref.assign(check_ref, check_ref + n_check);
+    g->have_ref = true;
+    for (int64_t v : g->idx)
+      if (v < 0 || v >= total) { set_error("check index out of range"); return TP_EINVAL; }
+  } else {
+    const int64_t n = std::min<int64_t>(4096, total);
+    g->idx.resize(n);
+    for (int64_t i = 0; i < n; ++i) g->idx[i] = (i * total) / n;   // fixed, spread points
+  }
+  g->tol = tol > 0 ? tol : (L.d.dtype == TP_DTYPE_BF16 || L.d.out_dtype == TP_DTYPE_BF16 ? 2e-2 : 1e-5);
+  g->vals.resize(g->idx.size());
+  TP_CK(cudaMalloc(&g->d_idx, g->idx.size() * sizeof(int64_t)));
+  TP_CK(cudaMalloc(&g->d_vals, g->idx.size() * sizeof(double)));
+  TP_CK(cudaMemcpy(g->d_idx, g->idx.data(), g->idx.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  return TP_OK;
+}
+
+// Poison y, run once, gather, compare.  Caller has the partition context current.
+static tp_status gate_check(tp_partition* part, const ConvPlan& plan, Gate* g, tp_measurement* m) {
+  cudaStream_t st = part->stream;
+  const Layer& L = plan.L;
+  const size_t ybytes = (size_t)L.M * L.d.k * plan.out_eb;
+  TP_CK(cudaMemsetAsync(plan.y_user, 0xFF, ybytes, st));   // NaN in bf16 and fp32
+  TP_CK(launch_plan(plan, st));
+  TP_CK(launch_gather(plan.y_user, L.d.in_layout == TP_LAYOUT_NHWC, L.d.out_dtype == TP_DTYPE_FP32, L.d.n, L.d.k,
+                      L.P, L.Q, g->d_idx, (int)g->idx.size(), g->d_vals, st));
+  g_launches += 1;
+  TP_CK(cudaMemcpyAsync(g->vals.data(), g->d_vals, g->vals.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  TP_CK(cudaStreamSynchronize(st));
+  if (!g->have_ref) {
+    for (double v : g->vals)
+      if (!std::isfinite(v)) { m->max_abs_err = NAN; return TP_EMISMATCH; }
+    g->ref = g->vals;
+    g->have_ref = true;
+  }
+  double err = 0, mref = 0;
+  bool finite = true;
+  for (size_t i = 0; i < g->vals.size(); ++i) {
+    if (!std::isfinite(g->vals[i])) finite = false;
+    err = std::max(err, std::fabs(g->vals[i] - g->ref[i]));
+    mref = std::max(mref, std::fabs(g->ref[i]));
+  }
+  m->max_abs_err = finite ? err : NAN;
+  m->max_ref = mref;
+  if (!finite || !(err <= g->tol * std::max(mref, 1e-30))) return TP_EMISMATCH;
+  return TP_OK;
+}
+
+// ---------------------------------------------------------------- tuner core
+static tp_status measure_candidates(const Layer& L, tp_partition* part, const int64_t* cand, int32_t n_cand,
+                                    const void* x, const void* w, const void* bias, void* y, void* ws,
+                                    size_t ws_bytes, Gate* gate, const tp_timing& tm, tp_measurement* records,
+                                    int32_t cap, int32_t* n_records) {
+  EventPool pool;
+  int32_t nrec = 0;
+  for (int32_t i = 0; i < n_cand; ++i) {
+    tp_measurement m;
+    std::memset(&m, 0, sizeof(m));
+    m.device = part->device;
+    m.sm_requested = part->sm_requested;
+    m.sm_granted = part->sm_granted;
+    m.space_index = cand[i];
+    tp_schedule s;
+    if (!space_get(L, cand[i], &s)) {
+      m.status = TP_EINVALID_CONFIG;
+    } else {
+      ConvPlan plan;
+      tp_status st = make_plan(L, s, x, w, bias, y, ws, ws_bytes, &plan);
+      if (st == TP_OK) {
+        plan_geometry(plan, part->sm_granted, &m);
+        st = gate_check(part, plan, gate, &m);
+        if (st == TP_OK) st = time_plan(part, plan, tm, pool, &m);
+      }
+      m.status = st;
+      if (st == TP_ECUDA) {
+        // A sticky device error poisons the context; surface it to the caller.
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess && cudaDeviceSynchronize() != cudaSuccess) {
+          if (nrec < cap) records[nrec++] = m;
+          *n_records = nrec;
+          return TP_ECUDA;
+        }
+      }
+    }
+    if (nrec < cap) records[nrec++] = m;
+  }
+  *n_records = nrec;
+  return TP_OK;
+}
+
+static tp_status get_part(tp_partition* part, tp_partition** out) {
+  if (part) { *out = part; return TP_OK; }
+  DeviceState* ds = nullptr;
+  tp_status st = init_device(0, &ds);
+  if (st != TP_OK) return st;
+  *out = ds->whole.get();
+  return TP_OK;
+}
+
+}  // namespace tp
+
+using namespace tp;
+
+extern "C" {
+
+tp_status tp_init(int32_t device) { return init_device(device, nullptr); }
+
+int64_t tp_launch_count(void) { return g_launches.load(); }
+
+void tp_shutdown(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& kv : g_dev) {
+    DeviceState& ds = kv.second;
+    if (!ds.init) continue;
+    cudaSetDevice(kv.first);
+    cudaDeviceSynchronize();
+    for (auto& p : ds.parts) destroy_partition(p.second.get());
+    ds.parts.clear();
+    destroy_partition(ds.whole.get());
+    ds.whole.reset();
+    if (ds.flush_buf) cudaFree(ds.flush_buf);
+    ds.flush_buf = nullptr;
+    ds.init = false;
+  }
+}
+
+tp_status tp_partition_get(int32_t device, double fraction, int32_t flags, tp_partition** part,
+                           int32_t* sm_requested, int32_t* sm_granted) {
+  if (!part || !(fraction > 0.0) || fraction > 1.0) { set_error("fraction must be in (0, 1]"); return TP_EINVAL; }
+  DeviceState* ds = nullptr;
+  tp_status st = init_device(device, &ds);
+  if (st != TP_OK) return st;
+  const int requested = std::max(1, (int)std::floor(ds->sm_count * fraction + 1e-9));
+  if (requested >= ds->sm_count) {
+    *part = ds->whole.get();
+  } else {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_tuple(requested, flags);
+    auto it = ds->parts.find(key);
+    if (it == ds->parts.end()) {
+      tp_partition* p = nullptr;
+      st = create_green(device, requested, flags, &p);
+      if (st != TP_OK) return st;
+      p->fraction = fraction;
+      p->cached = true;
+      p->flush_buf = ds->flush_buf;
+      p->flush_bytes = ds->flush_bytes;
+      it = ds->parts.emplace(key, std::unique_ptr<tp_partition>(p)).first;
+    }
+    *part = it->second.get();
+  }
+  if (sm_requested) *sm_requested = (*part)->sm_requested;
+  if (sm_granted) *sm_granted = (*part)->sm_granted;
+  return TP_OK;
+}
+
+tp_status tp_partition_split(int32_t device, int32_t k, int32_t sms_each, int32_t flags, tp_partition** parts,
+                             int32_t* granted) {
+  if (k < 1 || sms_each < 1 || !parts) { set_error("bad split arguments"); return TP_EINVAL; }
+  DeviceState* ds = nullptr;
+  tp_status st = init_device(device, &ds);
+  if (st != TP_OK) return st;
+  const DriverApi& drv = driver();
+  CUdevice dev;
+  TP_CU(drv.deviceGet(&dev, device));
+  CUdevResource full;
+  TP_CU(drv.deviceGetDevResource(dev, &full, CU_DEV_RESOURCE_TYPE_SM));
+  std::vector<CUdevResource> grp(k);
+  CUdevResource rem;
+  unsigned nb = (unsigned)k;
+  const unsigned use = (flags & TP_PART_FINE_GRAINED) ? CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING : 0;
+  CUresult r = drv.devSmResourceSplitByCount(grp.data(), &nb, &full, &rem, use, (unsigned)sms_each);
+  if (r != CUDA_SUCCESS || (int)nb < k) {
+    set_error("cannot split the device into " + std::to_string(k) + " x " + std::to_string(sms_each) + " SMs");
+    return TP_ECAPACITY;
+  }
+  for (int i = 0; i < k; ++i) {
+    CUdevResourceDesc desc;
+    TP_CU(drv.devResourceGenerateDesc(&desc, &grp[i], 1));
+    auto p = std::make_unique<tp_partition>();
+    p->device = device; p->flags = flags; p->sm_requested = sms_each; p->sm_granted = (int)grp[i].sm.smCount;
+    p->green = true; p->fraction = (double)sms_each / ds->sm_count;
+    TP_CU(drv.greenCtxCreate(&p->gctx, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM));
+    TP_CU(drv.ctxFromGreenCtx(&p->ctx, p->gctx));
+    CUstream s;
+    TP_CU(drv.greenCtxStreamCreate(&s, p->gctx, CU_STREAM_NON_BLOCKING, 0));
+    p->stream = reinterpret_cast<cudaStream_t>(s);
+    p->flush_buf = ds->flush_buf;
+    p->flush_bytes = ds->flush_bytes;
+    if (granted) granted[i] = p->sm_granted;
+    parts[i] = p.release();
+  }
+  return TP_OK;
+}
+
+tp_status tp_partition_info(tp_partition* part, int32_t* device, int32_t* req, int32_t* gr, void** stream) {
+  if (!part) { set_error("null partition"); return TP_EINVAL; }
+  if (device) *device = part->device;
+  if (req) *req = part->sm_requested;
+  if (gr) *gr = part->sm_granted;
+  if (stream) *stream = part->stream;
+  return TP_OK;
+}
+
+tp_status tp_partition_sync(tp_partition* part) {
+  tp_partition* p;
+  tp_status st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  CtxGuard g(p);
+  TP_CK(cudaStreamSynchronize(p->stream));
+  return TP_OK;
+}
+
+tp_status tp_partition_close(tp_partition* part) {
+  if (!part) return TP_OK;
+  if (part->cached) return TP_OK;   // cached partitions live until tp_shutdown
+  {
+    CtxGuard g(part);
+    cudaStreamSynchronize(part->stream);
+  }
+  destroy_partition(part);
+  delete part;
+  return TP_OK;
+}
+
+tp_status tp_partition_probe(tp_partition* part, int32_t ctas, int32_t* smids_dev) {
+  tp_partition* p;
+  tp_status st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  CtxGuard g(p);
+  TP_CK(launch_smid_probe(ctas, smids_dev, p->stream));
+  g_launches += 1;
+  TP_CK(cudaStreamSynchronize(p->stream));
+  return TP_OK;
+}
+
+tp_status tp_partition_copy_bw(tp_partition* part, const void* src, void* dst, size_t bytes, int32_t reps,
+                               double* gbps) {
+  tp_partition* p;
+  tp_status st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  CtxGuard g(p);
+  EventPool pool;
+  TP_CK(pool.ensure(2));
+  const int grid = p->sm_granted * 4;
+  TP_CK(launch_copy(src, dst, bytes, grid, p->stream));   // warm-up
+  double best = 0;
+  for (int i = 0; i < std::max(1, reps); ++i) {
+    TP_CK(cudaEventRecord(pool.ev[0], p->stream));
+    TP_CK(launch_copy(src, dst, bytes, grid, p->stream));
+    TP_CK(cudaEventRecord(pool.ev[1], p->stream));
+    TP_CK(cudaEventSynchronize(pool.ev[1]));
+    float ms = 0;
+    TP_CK(cudaEventElapsedTime(&ms, pool.ev[0], pool.ev[1]));
+    best = std::max(best, 2.0 * (double)bytes / (ms * 1e-3) / 1e9);
+  }
+  g_launches += 1 + std::max(1, reps);
+  *gbps = best;
+  return TP_OK;
+}
+
+tp_status tp_workspace_size(const tp_conv_desc* d, const tp_schedule* s, size_t* bytes) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  if (!s || !bytes) { set_error("null argument"); return TP_EINVAL; }
+  *bytes = ws_layout(L, *s).total;
+  return TP_OK;
+}
+
+tp_status tp_workspace_size_max(const tp_conv_desc* d, size_t* bytes) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  size_t mx = 0;
+  const int64_t n = space_size(L);
+  for (int64_t i = 0; i < n; ++i) {
+    tp_schedule s;
+    space_get(L, i, &s);
+    mx = std::max(mx, ws_layout(L, s).total);
+  }
+  *bytes = mx;
+  return TP_OK;
+}
+
+tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part, const void* x,
+                        const void* w, const void* bias, void* y, void* ws, size_t ws_bytes, const tp_timing* timing,
+                        tp_measurement* out) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  if (!s) { set_error("null schedule"); return TP_EINVAL; }
+  tp_partition* p;
+  st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  CtxGuard g(p);
+  ConvPlan plan;
+  st = make_plan(L, *s, x, w, bias, y, ws, ws_bytes, &plan);
+  if (st != TP_OK) return st;
+  if (!timing && !out) {
+    TP_CK(launch_plan(plan, p->stream));
+    return TP_OK;
+  }
+  tp_measurement m;
+  std::memset(&m, 0, sizeof(m));
+  m.device = p->device; m.sm_requested = p->sm_requested; m.sm_granted = p->sm_granted;
+  plan_geometry(plan, p->sm_granted, &m);
+  EventPool pool;
+  const tp_timing tm = timing ? *timing : default_timing();
+  st = time_plan(p, plan, tm, pool, &m);
+  m.status = st;
+  if (out) *out = m;
+  return st;
+}
+
+tp_status tp_tune_subset(const tp_conv_desc* d, tp_partition* part, const int64_t* cand, int32_t n_cand,
+                         const void* x, const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
+                         const int64_t* check_idx, const double* check_ref, int32_t n_check, double tol,
+                         const tp_timing* timing, tp_measurement* records, int32_t cap, int32_t* n_records) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  if ((n_cand > 0 && !cand) || !records || !n_records || (n_check > 0 && (!check_idx || !check_ref))) {
+    set_error("null argument");
+    return TP_EINVAL;
+  }
+  tp_partition* p;
+  st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  TP_CK(cudaSetDevice(p->device));
+  Gate gate;
+  st = gate_setup(L, check_idx, check_ref, n_check, tol, &gate);
+  if (st != TP_OK) return st;
+  CtxGuard g(p);
+  const tp_timing tm = timing ? *timing : default_timing();
+  return measure_candidates(L, p, cand, n_cand, x, w, bias, y, ws, ws_bytes, &gate, tm, records, cap, n_records);
+}
+
+tp_status tp_tune(const tp_conv_desc* d, tp_partition* part, int32_t trials, uint64_t seed, const void* x,
+                  const void* w, const void* bias, void* y, void* ws, size_t ws_bytes, const int64_t* check_idx,
+                  const double* check_ref, int32_t n_check, double tol, const tp_timing* timing, tp_schedule* best,
+                  tp_measurement* best_m, tp_measurement* records, int32_t cap, int32_t* n_records) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  const int64_t n = space_size(L);
+  std::vector<int64_t> cand((size_t)std::min<int64_t>(std::max(trials, 0), n));
+  int32_t nc = 0;
+  st = tp_space_sample(d, trials, seed, cand.data(), (int32_t)cand.size(), &nc);
+  if (st != TP_OK) return st;
+  std::vector<tp_measurement> local;
+  tp_measurement* recs = records;
+  int32_t rcap = cap;
+  if (!records || cap < nc) {
+    local.resize(nc);
+    recs = local.data();
+    rcap = nc;
+  }
+  int32_t nrec = 0;
+  st = tp_tune_subset(d, part, cand.data(), nc, x, w, bias, y, ws, ws_bytes, check_idx, check_ref, n_check, tol,
+                      timing, recs, rcap, &nrec);
+  if (records && recs != records) std::memcpy(records, recs, sizeof(tp_measurement) * std::min(cap, nrec));
+  if (n_records) *n_records = records ? std::min(cap, nrec) : nrec;
+  if (st != TP_OK) return st;
+  int32_t b = -1;
+  tp_select_best(recs, nrec, &b);
+  if (b < 0) { set_error("no candidate passed the correctness gate"); return TP_EMISMATCH; }
+  if (best_m) *best_m = recs[b];
+  if (best) {
+    space_get(L, recs[b].space_index, best);
+    tp_partition* p;
+    get_part(part, &p);
+    best->sm_tuned = p->sm_granted;
+    // Leave y holding the winner's output.
+    tp_conv2d_run(d, best, part, x, w, bias, y, ws, ws_bytes, nullptr, nullptr);
+    tp_partition_sync(part);
+  }
+  return TP_OK;
+}
+
+tp_status tp_cross_eval(const tp_conv_desc* d, const tp_schedule* tuned_at_p, tp_partition* part_q, const void* x,
+                        const void* w, const void* bias, void* y, void* ws, size_t ws_bytes, const tp_timing* timing,
+                        tp_measurement* out) {
+  if (!tuned_at_p || !out) { set_error("null argument"); return TP_EINVAL; }
+  // Frozen geometry (C15): the schedule carries grid_* from tuning time; make_plan
+  // uses it verbatim whatever the SM count of part_q.
+  return tp_conv2d_run(d, tuned_at_p, part_q, x, w, bias, y, ws, ws_bytes, timing ? timing : nullptr, out);
+}
+
+tp_status tp_pack_input(const tp_conv_desc* d, tp_partition* part, const float* x, void* out) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK && st != TP_EUNSUPPORTED) return st;
+  tp_partition* p;
+  st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  CtxGuard g(p);
+  TP_CK(launch_pack_input(x, out, d->n, d->c, d->h, d->w, d->in_layout == TP_LAYOUT_NHWC,
+                          d->dtype == TP_DTYPE_BF16, p->stream));
+  g_launches += 1;
+  return TP_OK;
+}
+
+tp_status tp_pack_weights(const tp_conv_desc* d, tp_partition* part, const float* w, void* out) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK && st != TP_EUNSUPPORTED) return st;
+  tp_partition* p;
+  st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  CtxGuard g(p);
+  TP_CK(launch_pack_weights(w, out, d->k, d->c / d->groups, d->r, d->s, d->dtype == TP_DTYPE_BF16, p->stream));
+  g_launches += 1;
+  return TP_OK;
+}
+
+tp_status tp_gather_output(const tp_conv_desc* d, tp_partition* part, const void* y, const int64_t* idx, int32_t n,
+                           double* vals) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  tp_partition* p;
+  st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  TP_CK(cudaSetDevice(p->device));
+  Gate gate;
+  st = gate_setup(L, idx, vals, n, 0, &gate);   // only uses idx + buffers
+  if (st != TP_OK) return st;
+  CtxGuard g(p);
+  TP_CK(launch_gather(y, d->in_layout == TP_LAYOUT_NHWC, d->out_dtype == TP_DTYPE_FP32, d->n, d->k, L.P, L.Q,
+                      gate.d_idx, n, gate.d_vals, p->stream));
+  g_launches += 1;
+  TP_CK(cudaMemcpyAsync(vals, gate.d_vals, sizeof(double) * n, cudaMemcpyDeviceToHost, p->stream));
+  TP_CK(cudaStreamSynchronize(p->stream));
+  return TP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,291 @@
+// space.cpp -- host-only schedule space of libtp.
+//
+// The paper's tuner searches "loop tiles and ordering, caching, and loop
+// unrolling ... CUDA threading", picks random candidates when
+// it has no data, profiles them and keeps the best per
+// operator.  The v0 knob table and validity predicate are DESIGN.md
+// "Schedule space v0"; this file and oracle/space.py implement that table
+// independently and tests/test_space.py checks them bit-exactly.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "tp_internal.h"
+
+namespace tp {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+const std::string& get_error() { return g_err; }
+
+static int32_t out_dim(int32_t in, int32_t k, int32_t st, int32_t pad, int32_t dil) {
+  const int32_t span = in + 2 * pad - dil * (k - 1) - 1;
+  if (span < 0 || st < 1) return 0;
+  return span / st + 1;
+}
+
+int32_t layer_kind(const tp_conv_desc& d) {
+  if (d.dtype == TP_DTYPE_BF16 && d.groups == 1 && d.c % 8 == 0 && d.k % 8 == 0 &&
+      d.dil_h == 1 && d.dil_w == 1)
+    return TP_KIND_IGEMM_TC;
+  return TP_KIND_DIRECT;
+}
+
+tp_status make_layer(const tp_conv_desc* d, Layer* L) {
+  if (!d) { set_error("null descriptor"); return TP_EINVAL; }
+  const tp_conv_desc& x = *d;
+  if (x.n < 1 || x.c < 1 || x.h < 1 || x.w < 1 || x.k < 1 || x.r < 1 || x.s < 1 ||
+      x.stride_h < 1 || x.stride_w < 1 || x.pad_h < 0 || x.pad_w < 0 || x.dil_h < 1 ||
+      x.dil_w < 1 || x.groups < 1) {
+    set_error("descriptor has a non-positive extent or negative padding");
+    return TP_EINVAL;
+  }
+  if (x.c % x.groups || x.k % x.groups) { set_error("groups must divide C and K"); return TP_EINVAL; }
+  if ((x.in_layout != TP_LAYOUT_NHWC && x.in_layout != TP_LAYOUT_NCHW) ||
+      (x.dtype != TP_DTYPE_BF16 && x.dtype != TP_DTYPE_FP32) ||
+      (x.out_dtype != TP_DTYPE_BF16 && x.out_dtype != TP_DTYPE_FP32) || (x.epilogue & ~3)) {
+    set_error("bad layout / dtype / epilogue code");
+    return TP_EINVAL;
+  }
+  L->d = x;
+  L->P = out_dim(x.h, x.r, x.stride_h, x.pad_h, x.dil_h);
+  L->Q = out_dim(x.w, x.s, x.stride_w, x.pad_w, x.dil_w);
+  if (L->P < 1 || L->Q < 1) { set_error("output size < 1 (reading C3)"); return TP_EINVAL; }
+  L->M = (int64_t)x.n * L->P * L->Q;
+  L->Cg = x.c / x.groups;
+  L->Kg = x.k / x.groups;
+  L->kind = layer_kind(x);
+  L->depthwise = (x.groups > 1);
+  if (x.dil_h != 1 || x.dil_w != 1) { set_error("dilation > 1 is not on the GPU path (C4)"); return TP_EUNSUPPORTED; }
+  if (x.groups != 1 && !(x.groups == x.c && x.k == x.c)) {
+    set_error("only groups in {1, C} with K == C are on the GPU path (C5)");
+    return TP_EUNSUPPORTED;
+  }
+  return TP_OK;
+}
+
+// ---- knob table ----
+static const int kTcBM[] = {64, 128};
+static const int kTcBN[] = {32, 64, 128, 256};
+static const int kTcBK[] = {16, 32, 64, 128};
+static const int kTcStages[] = {2, 3, 4, 6};
+static const int kTcThreads[] = {128, 256};
+static const int kTcSplit[] = {1, 2, 4, 8};
+static const int kDThreads[] = {64, 128, 256, 512};
+static const int kDTileQ[] = {1, 2, 4};
+static const int kDVecK[] = {1, 2, 4, 8};
+static const int kDTileP[] = {1, 2, 4, 8};
+static const int kDSmem[] = {0, 1};
+
+int64_t tc_smem_bytes(int bm, int bn, int bk, int stages) {
+  return (int64_t)stages * (bm + bn) * bk * 2 + 1024;
+}
+
+void direct_lanes(const Layer& L, int threads, int tile_q, int vec_k, int tile_p, int* lanes_k, int* lanes_q) {
+  const int64_t kv = cdiv(L.d.k, vec_k);
+  const int64_t lk = std::min<int64_t>(np2(kv), threads / tile_p);
+  *lanes_k = (int)lk;
+  *lanes_q = (int)(threads / (lk * tile_p));
+}
+
+int64_t direct_smem_bytes(const Layer& L, int threads, int tile_q, int vec_k, int tile_p) {
+  int lk, lq;
+  direct_lanes(L, threads, tile_q, vec_k, tile_p, &lk, &lq);
+  const int64_t qt = (int64_t)lq * tile_q, kt = (int64_t)lk * vec_k;
+  const int64_t rows_in = (int64_t)(tile_p - 1) * L.d.stride_h + L.d.r;
+  const int64_t cols_in = (qt - 1) * L.d.stride_w + L.d.s;
+  if (!L.depthwise) {
+    const int64_t cc = std::min<int64_t>(L.d.c, 16);
+    return 4 * (rows_in * cols_in * cc + (int64_t)L.d.r * L.d.s * cc * kt);
+  }
+  return 4 * (rows_in * cols_in * kt + (int64_t)L.d.r * L.d.s * kt);
+}
+
+static bool valid_tc(const Layer& L, int bm, int bn, int bk, int stages, int /*threads*/, int split) {
+  if (tc_smem_bytes(bm, bn, bk, stages) > kSmemLimit) return false;
+  if (bn > std::max<int64_t>(32, np2(L.d.k))) return false;
+  if (bm > std::max<int64_t>(64, np2(L.M))) return false;
+  if (bk > std::max<int64_t>(16, np2(L.d.c))) return false;
+  return split <= (int64_t)L.d.r * L.d.s * cdiv(L.d.c, bk);
+}
+
+static bool valid_direct(const Layer& L, int threads, int tq, int vk, int tpp, int sm) {
+  if (tq > L.Q || tpp > L.P || vk > L.d.k) return false;
+  if (L.depthwise && L.d.c % vk) return false;
+  if (sm && direct_smem_bytes(L, threads, tq, vk, tpp) > kSmemLimit) return false;
+  return true;
+}
+
+void fill_geometry(const Layer& L, tp_schedule* s) {
+  if (s->kind == TP_KIND_IGEMM_TC) {
+    s->grid_x = (int32_t)cdiv(L.M, s->bm);
+    s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
+    s->grid_z = s->split_k;
+  } else {
+    int lk, lq;
+    direct_lanes(L, s->threads, s->tile_q, s->vec_k, s->tile_p, &lk, &lq);
+    s->grid_x = (int32_t)(cdiv(L.Q, (int64_t)lq * s->tile_q) * cdiv(L.P, s->tile_p));
+    s->grid_y = (int32_t)cdiv(L.d.k, (int64_t)lk * s->vec_k);
+    s->grid_z = L.d.n;
+  }
+}
+
+// Enumerate in lexicographic order; visit(schedule) returns false to stop.
+template <class F>
+static void enumerate(const Layer& L, F visit) {
+  int64_t idx = 0;
+  if (L.kind == TP_KIND_IGEMM_TC) {
+    for (int bm : kTcBM) for (int bn : kTcBN) for (int bk : kTcBK) for (int st : kTcStages)
+      for (int th : kTcThreads) for (int sk : kTcSplit) {
+        if (!valid_tc(L, bm, bn, bk, st, th, sk)) continue;
+        tp_schedule s; std::memset(&s, 0, sizeof(s));
+        s.kind = TP_KIND_IGEMM_TC; s.bm = bm; s.bn = bn; s.bk = bk; s.stages = st;
+        s.threads = th; s.split_k = sk; s.space_index = idx++;
+        if (!visit(s)) return;
+      }
+  } else {
+    for (int th : kDThreads) for (int tq : kDTileQ) for (int vk : kDVecK) for (int tpp : kDTileP)
+      for (int sm : kDSmem) {
+        if (!valid_direct(L, th, tq, vk, tpp, sm)) continue;
+        tp_schedule s; std::memset(&s, 0, sizeof(s));
+        s.kind = TP_KIND_DIRECT; s.threads = th; s.tile_q = tq; s.vec_k = vk; s.tile_p = tpp;
+        s.smem_stage = sm; s.split_k = 1; s.space_index = idx++;
+        if (!visit(s)) return;
+      }
+  }
+}
+
+int64_t space_size(const Layer& L) {
+  int64_t n = 0;
+  enumerate(L, [&](const tp_schedule&) { ++n; return true; });
+  return n;
+}
+
+bool space_get(const Layer& L, int64_t idx, tp_schedule* out) {
+  bool found = false;
+  enumerate(L, [&](const tp_schedule& s) {
+    if (s.space_index == idx) { *out = s; found = true; return false; }
+    return true;
+  });
+  if (found) fill_geometry(L, out);
+  return found;
+}
+
+bool schedule_in_space(const Layer& L, const tp_schedule& s) {
+  if (s.kind != L.kind) return false;
+  if (s.kind == TP_KIND_IGEMM_TC) {
+    auto in = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };
+    return in(s.bm, kTcBM, 2) && in(s.bn, kTcBN, 4) && in(s.bk, kTcBK, 4) && in(s.stages, kTcStages, 4) &&
+           in(s.threads, kTcThreads, 2) && in(s.split_k, kTcSplit, 4) &&
+           valid_tc(L, s.bm, s.bn, s.bk, s.stages, s.threads, s.split_k);
+  }
+  auto in = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };
+  return in(s.threads, kDThreads, 4) && in(s.tile_q, kDTileQ, 3) && in(s.vec_k, kDVecK, 4) &&
+         in(s.tile_p, kDTileP, 4) && in(s.smem_stage, kDSmem, 2) &&
+         valid_direct(L, s.threads, s.tile_q, s.vec_k, s.tile_p, s.smem_stage);
+}
+
+static uint64_t splitmix64_next(uint64_t& state) {
+  state += 0x9E3779B97F4A7C15ull;
+  uint64_t z = state;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+}  // namespace tp
+
+using namespace tp;
+
+extern "C" {
+
+const char* tp_status_str(tp_status s) {
+  switch (s) {
+    case TP_OK: return "ok";
+    case TP_EINVAL: return "invalid argument";
+    case TP_EINVALID_CONFIG: return "invalid_config";
+    case TP_ECAPACITY: return "capacity";
+    case TP_ECUDA: return "server_error";
+    case TP_EMISMATCH: return "mismatch";
+    case TP_EUNSUPPORTED: return "unsupported";
+  }
+  return "unknown";
+}
+
+const char* tp_last_error(void) { return get_error().c_str(); }
+
+tp_status tp_output_shape(const tp_conv_desc* d, int32_t* p, int32_t* q) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st == TP_EINVAL) return st;
+  if (p) *p = L.P;
+  if (q) *q = L.Q;
+  return TP_OK;
+}
+
+tp_status tp_layer_kind(const tp_conv_desc* d, int32_t* kind) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  *kind = L.kind;
+  return TP_OK;
+}
+
+tp_status tp_space_size(const tp_conv_desc* d, int64_t* n_valid) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  *n_valid = space_size(L);
+  return TP_OK;
+}
+
+tp_status tp_space_get(const tp_conv_desc* d, int64_t idx, tp_schedule* out) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  if (idx < 0 || !space_get(L, idx, out)) {
+    set_error("space index out of range");
+    return TP_EINVALID_CONFIG;
+  }
+  return TP_OK;
+}
+
+tp_status tp_space_sample(const tp_conv_desc* d, int32_t trials, uint64_t seed, int64_t* idx_out,
+                          int32_t cap, int32_t* n_out) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  if (trials < 0 || !idx_out || !n_out) { set_error("bad sample arguments"); return TP_EINVAL; }
+  const int64_t n = space_size(L);
+  const int64_t t = std::min<int64_t>(trials, n);
+  if (t > cap) { set_error("sample output capacity too small"); return TP_EINVAL; }
+  std::vector<int64_t> a(n);
+  for (int64_t i = 0; i < n; ++i) a[i] = i;
+  if (trials < n) {
+    uint64_t state = seed;
+    for (int64_t i = 0; i < t; ++i) {
+      const int64_t j = i + (int64_t)(splitmix64_next(state) % (uint64_t)(n - i));
+      std::swap(a[i], a[j]);
+    }
+  }
+  for (int64_t i = 0; i < t; ++i) idx_out[i] = a[i];
+  *n_out = (int32_t)t;
+  return TP_OK;
+}
+
+tp_status tp_select_best(const tp_measurement* r, int32_t n, int32_t* best) {
+  if (!best || (n > 0 && !r)) { set_error("bad select arguments"); return TP_EINVAL; }
+  int32_t b = -1;
+  for (int32_t i = 0; i < n; ++i) {
+    if (r[i].status != TP_OK) continue;
+    if (b < 0 || r[i].median_us < r[b].median_us ||
+        (r[i].median_us == r[b].median_us && r[i].space_index < r[b].space_index))
+      b = i;
+  }
+  *best = b;
+  return TP_OK;
+}
+
+}  // extern "C"

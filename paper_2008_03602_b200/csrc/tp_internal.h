@@ -1,0 +1,42 @@
+// tp_internal.h -- shared declarations inside libtp (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include "../../include/tp.h"
+
+namespace tp {
+
+// Thread-local error message (tp_last_error).
+void set_error(const std::string& msg);
+const std::string& get_error();
+
+// Derived per-layer quantities.
+struct Layer {
+  tp_conv_desc d;
+  int32_t P, Q;
+  int64_t M;      // GEMM M = N*P*Q (output pixels)
+  int32_t Cg, Kg; // channels per group
+  int32_t kind;   // TP_KIND_*
+  bool depthwise;
+};
+
+// Validate + derive.  Returns TP_OK, TP_EINVAL or TP_EUNSUPPORTED.
+tp_status make_layer(const tp_conv_desc* d, Layer* L);
+int32_t layer_kind(const tp_conv_desc& d);
+
+// Space (space.cpp).
+int64_t space_size(const Layer& L);
+bool space_get(const Layer& L, int64_t idx, tp_schedule* out);
+void fill_geometry(const Layer& L, tp_schedule* s);
+void direct_lanes(const Layer& L, int threads, int tile_q, int vec_k, int tile_p, int* lanes_k, int* lanes_q);
+int64_t direct_smem_bytes(const Layer& L, int threads, int tile_q, int vec_k, int tile_p);
+int64_t tc_smem_bytes(int bm, int bn, int bk, int stages);
+bool schedule_in_space(const Layer& L, const tp_schedule& s);
+
+constexpr int64_t kSmemLimit = 232448;  // 227 KiB per CTA
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t np2(int64_t v) { int64_t p = 1; while (p < v) p *= 2; return p; }
+
+}  // namespace tp

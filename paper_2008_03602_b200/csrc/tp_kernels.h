@@ -1,0 +1,118 @@
+// tp_kernels.h -- kernel argument blocks and launch plans (internal to libtp).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+#include "tp_internal.h"
+
+namespace tp {
+
+// Driver entry points, resolved at run time through cudaGetDriverEntryPoint so
+// that libtp.so loads (and its host-only functions run) without libcuda.
+struct DriverApi {
+  bool ok = false;
+  CUresult (*encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                          CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill) = nullptr;
+  CUresult (*encodeIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                           const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                           CUtensorMapFloatOOBfill) = nullptr;
+  CUresult (*ctxPush)(CUcontext) = nullptr;
+  CUresult (*ctxPop)(CUcontext*) = nullptr;
+  CUresult (*ctxGetCurrent)(CUcontext*) = nullptr;
+  CUresult (*deviceGet)(CUdevice*, int) = nullptr;
+  CUresult (*devicePrimaryCtxRetain)(CUcontext*, CUdevice) = nullptr;
+  CUresult (*deviceGetDevResource)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*devSmResourceSplitByCount)(CUdevResource*, unsigned int*, const CUdevResource*, CUdevResource*,
+                                        unsigned int, unsigned int) = nullptr;
+  CUresult (*devResourceGenerateDesc)(CUdevResourceDesc*, CUdevResource*, unsigned int) = nullptr;
+  CUresult (*greenCtxCreate)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned int) = nullptr;
+  CUresult (*greenCtxDestroy)(CUgreenCtx) = nullptr;
+  CUresult (*ctxFromGreenCtx)(CUcontext*, CUgreenCtx) = nullptr;
+  CUresult (*greenCtxStreamCreate)(CUstream*, CUgreenCtx, unsigned int, int) = nullptr;
+  CUresult (*greenCtxGetDevResource)(CUgreenCtx, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*streamDestroy)(CUstream) = nullptr;
+};
+const DriverApi& driver();
+
+// ---------------------------------------------------------------- igemm_tc
+struct TcArgs {
+  int64_t M;
+  int K, P, Q, S, sh, sw, ph, pw;
+  int bk, stages, split_k, cblocks, kblocks;
+  const float* bias;
+  void* y;
+  int out_f32, relu, has_bias;
+  float* ws_partial;
+  int* ws_counters;
+};
+
+struct TcProblem {
+  const void* x;   // NHWC bf16
+  const void* w;   // KRSC bf16
+  const float* bias;
+  void* y;         // NHWC
+  int N, C, H, W, K, R, S, P, Q, sh, sw, ph, pw;
+  int64_t M;
+  int bm, bn, bk, stages, threads, split_k;
+  int grid_x, grid_y, grid_z;
+  int out_f32, relu, has_bias;
+  float* ws_partial;
+  int* ws_counters;
+};
+
+struct TcPlan {
+  CUtensorMap tmA, tmB;
+  TcArgs args;
+  const void* fn = nullptr;
+  dim3 grid, block;
+  size_t smem = 0;
+};
+
+tp_status tc_prepare(const TcProblem& pb, TcPlan* plan);
+cudaError_t tc_launch(const TcPlan& plan, cudaStream_t stream);
+int tc_occupancy(const TcPlan& plan);
+size_t tc_dyn_smem(int bm, int bn, int bk, int stages);
+
+// ---------------------------------------------------------------- direct
+struct DirectArgs {
+  const void* x;   // NHWC, bf16 or fp32
+  const void* w;   // KRSC
+  const float* bias;
+  void* y;         // NHWC
+  int N, C, H, W, K, R, S, sh, sw, ph, pw, P, Q;
+  int tile_p, lanes_k, lanes_q, n_qb, cc;
+  int relu, has_bias, out_f32;
+};
+
+struct DirectPlan {
+  DirectArgs args;
+  const void* fn = nullptr;
+  dim3 grid, block;
+  size_t smem = 0;
+};
+
+tp_status direct_prepare(const Layer& L, const tp_schedule& s, const void* x, const void* w, const float* bias,
+                         void* y, DirectPlan* plan);
+cudaError_t direct_launch(const DirectPlan& plan, cudaStream_t stream);
+int direct_occupancy(const DirectPlan& plan);
+
+// ---------------------------------------------------------------- aux kernels
+cudaError_t launch_nchw_to_nhwc(const void* src, void* dst, int N, int C, int H, int W, int elem_bytes,
+                                cudaStream_t st);
+cudaError_t launch_nhwc_to_nchw(const void* src, void* dst, int N, int C, int H, int W, int elem_bytes,
+                                cudaStream_t st);
+cudaError_t launch_pack_input(const float* x_nchw, void* out, int N, int C, int H, int W, int to_nhwc, int bf16,
+                              cudaStream_t st);
+cudaError_t launch_pack_weights(const float* w_kcrs, void* out, int K, int Cg, int R, int S, int bf16,
+                                cudaStream_t st);
+cudaError_t launch_gather(const void* y, int layout_nhwc, int out_f32, int N, int K, int P, int Q,
+                          const int64_t* idx, int n, double* vals, cudaStream_t st);
+cudaError_t launch_smid_probe(int ctas, int* smids, cudaStream_t st);
+cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
+cudaError_t launch_l2_flush(void* buf, size_t bytes, int grid, cudaStream_t st);
+
+}  // namespace tp

@@ -1,0 +1,171 @@
+"""GPU parity: libtp's CUDA path (through the C-ABI) vs the fp64 oracle.
+
+Bars (north_star): bf16 inputs with fp32 accumulation within 2e-2 max relative
+error (reading C10: max|y - ref| / max|ref|), fp32 path within 1e-5; integer
+data (x, w in {-3..3}) bit-exact for every schedule with fp32 output (O11,
+"the output of the inference remains the same").
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import conv as oc
+from oracle import space as sp
+from paper_2008_03602_b200 import datagen, tp, workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _init():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test without a GPU")
+    tp.init(0)
+    yield
+
+
+def bf16_round(a):
+    return torch.tensor(np.asarray(a, dtype=np.float32)).bfloat16().double().numpy()
+
+
+def oracle_ref(d, x, w, b):
+    if d["dtype"] == tp.BF16:
+        x, w = bf16_round(x), bf16_round(w)
+    return oc.conv2d_c(d, x, w, b if d["epilogue"] & 1 else None, relu=bool(d["epilogue"] & 2))
+
+
+def rel_err(y, ref):
+    return float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+def mk(n, c, h, w, k, r, s, st=1, pad=0, g=1, dtype=tp.BF16, out=None, epi=3, layout=tp.NHWC):
+    return dict(n=n, c=c, h=h, w=w, k=k, r=r, s=s, stride_h=st, stride_w=st, pad_h=pad, pad_w=pad, dil_h=1, dil_w=1,
+                groups=g, in_layout=layout, dtype=dtype, out_dtype=dtype if out is None else out, epilogue=epi)
+
+
+# ------------------------------------------------------------------ exhaustive integer sweeps (O11)
+TC_TINY = [mk(1, 64, 10, 9, 64, 3, 3, 1, 1, out=tp.FP32, epi=1),
+           mk(2, 32, 7, 7, 48, 1, 1, 1, 0, out=tp.FP32, epi=1),
+           mk(1, 136, 9, 11, 40, 3, 3, 2, 1, out=tp.FP32, epi=1)]
+
+
+@pytest.mark.parametrize("d", TC_TINY, ids=lambda d: f"tc_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_r{d['r']}s{d['stride_h']}")
+def test_tc_every_schedule_bit_exact_integer(d):
+    x, w, b = datagen.make_inputs(d, 11, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    n = tp.space_size(d)
+    assert sp.layer_kind(d) == tp.KIND_IGEMM_TC
+    bad = []
+    for i in range(n):
+        s = tp.space_get(d, i)
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        y = buf.output()
+        if not np.array_equal(y, ref):
+            bad.append((i, {k: s[k] for k in ("bm", "bn", "bk", "stages", "threads", "split_k")},
+                        float(np.nanmax(np.abs(y - ref)))))
+    assert not bad, f"{len(bad)}/{n} schedules differ, first: {bad[:5]}"
+
+
+DIRECT_TINY = [mk(1, 8, 9, 10, 12, 3, 3, 1, 1, dtype=tp.FP32, epi=1),
+               mk(2, 3, 11, 11, 16, 7, 7, 2, 3, dtype=tp.FP32, epi=1),
+               mk(1, 16, 9, 9, 16, 3, 3, 2, 1, g=16, dtype=tp.FP32, epi=1),
+               mk(1, 24, 7, 7, 24, 3, 3, 1, 1, g=24, dtype=tp.BF16, out=tp.FP32, epi=1)]
+
+
+@pytest.mark.parametrize("d", DIRECT_TINY, ids=lambda d: f"direct_{d['c']}_g{d['groups']}_s{d['stride_h']}_{d['dtype']}")
+def test_direct_every_schedule_bit_exact_integer(d):
+    x, w, b = datagen.make_inputs(d, 12, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    n = tp.space_size(d)
+    bad = []
+    for i in range(n):
+        s = tp.space_get(d, i)
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        y = buf.output()
+        if not np.array_equal(y, ref):
+            bad.append((i, s["threads"], s["tile_q"], s["vec_k"], s["tile_p"], s["smem_stage"]))
+    assert not bad, f"{len(bad)}/{n} schedules differ, first: {bad[:5]}"
+
+
+# ------------------------------------------------------------------ random data, tolerance bars
+def _sampled_scheds(d, k=12, seed=0):
+    n = tp.space_size(d)
+    return [tp.space_get(d, i) for i in sp.sample(n, k, seed)]
+
+
+CFG_SHAPES = (wl.catalog("cfg1") + wl.catalog("resnet50") + wl.catalog("mobilenetv2")[:12])
+
+
+@pytest.mark.parametrize("d", CFG_SHAPES, ids=[d["name"] for d in CFG_SHAPES])
+def test_layer_random_parity(d):
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(9, 0))
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    tol = 2e-2 if d["dtype"] == tp.BF16 else 1e-5
+    for s in _sampled_scheds(d, 6, 1):
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        err = rel_err(buf.output(), ref)
+        assert err <= tol, (s, err)
+
+
+@pytest.mark.parametrize("d", wl.catalog("vgg19_b16")[1:3], ids=lambda d: d["name"])
+def test_vgg_full_size_sampled_points(d):
+    """Full BASELINE size (batch 16): oracle evaluated at 4096 sampled outputs."""
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(4, 1))
+    buf = tp.LayerBuffers(d, x, w, b)
+    P, Q = tp.output_shape(d)
+    idx = datagen.sample_points(d["n"] * d["k"] * P * Q, 4096, 3)
+    ref = oc.conv2d_points_c(d, bf16_round(x), bf16_round(w), b, True, idx)
+    for s in _sampled_scheds(d, 4, 2):
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        got = buf.gather(idx)
+        assert rel_err(got, ref) <= 2e-2, s
+
+
+def test_nchw_layout_matches_nhwc():
+    d = mk(1, 64, 12, 12, 32, 3, 3, 1, 1, out=tp.FP32, epi=3)
+    dn = dict(d, in_layout=tp.NCHW)
+    x, w, b = datagen.make_inputs(d, 5)
+    ref = oracle_ref(d, x, w, b)
+    for dd in (d, dn):
+        buf = tp.LayerBuffers(dd, x, w, b)
+        for s in _sampled_scheds(dd, 4, 3):
+            tp.conv2d_run(buf, s)
+            torch.cuda.synchronize()
+            assert rel_err(buf.output(), ref) <= 2e-2
+
+
+def test_split_k_deterministic():
+    d = wl.catalog("resnet50")[18]
+    x, w, b = datagen.make_inputs(d, 8)
+    buf = tp.LayerBuffers(d, x, w, b)
+    s = next(tp.space_get(d, i) for i in range(tp.space_size(d)) if tp.space_get(d, i)["split_k"] == 8)
+    outs = []
+    for _ in range(3):
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        outs.append(buf.y.clone())
+    assert all(torch.equal(outs[0], o) for o in outs[1:])
+    # the workspace counters are left zeroed
+    assert int(buf.ws[:4 * 64].view(torch.int32).abs().sum()) == 0
+
+
+def test_pack_kernels_bit_exact():
+    d = mk(2, 24, 5, 7, 8, 3, 3, 1, 1)
+    x, w, b = datagen.make_inputs(d, 4)
+    buf = tp.LayerBuffers(d, x, w, b)
+    xb = buf.x.view(torch.bfloat16).cpu()
+    want = torch.tensor(x).permute(0, 2, 3, 1).contiguous().bfloat16().reshape(-1)
+    assert torch.equal(xb.view(torch.int16), want.view(torch.int16))
+    wb = buf.w.view(torch.bfloat16).cpu()
+    wwant = torch.tensor(w).permute(0, 2, 3, 1).contiguous().bfloat16().reshape(-1)
+    assert torch.equal(wb.view(torch.int16), wwant.view(torch.int16))
