@@ -171,6 +171,16 @@ tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partitio
                         const void* x, const void* w, const void* bias, void* y,
                         void* ws, size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
 
+/* Tracing (SURVEY 5 "tracing / profiling"): run one IGEMM_TC launch with an
+ * in-kernel timeline.  trace_host receives grid_x*grid_y*grid_z rows of 64
+ * uint64: [0] entry, [1] prologue done, [2] epilogue start, [3] end (SM
+ * clock64 cycles), [4..19] k-block arrival in the MMA thread, [20..35]
+ * producer past its empty-slot wait, [36..51] MMA thread after commit (first
+ * 16 k-blocks), [62] %smid, [63] %globaltimer at entry (ns).  cap = rows. */
+tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part, const void* x,
+                          const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
+                          uint64_t* trace_host, int32_t cap, int32_t* rows);
+
 /* Tune: select candidates (a3), profile each inside `part` (a11) behind the
  * correctness gate (a10), record (a12), return the argmin.
  *   check_idx/check_ref/n_check : flat output indices (NKPQ logical) and

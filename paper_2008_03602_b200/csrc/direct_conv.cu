@@ -69,6 +69,10 @@ __global__ void __launch_bounds__(512) direct_conv_kernel(DirectArgs a) {
   const T* __restrict__ x = reinterpret_cast<const T*>(a.x);
   const T* __restrict__ w = reinterpret_cast<const T*>(a.w);
   const int C = a.C, H = a.H, W = a.W, K = a.K, R = a.R, S = a.S;
+  // Programmatic dependent launch: let the next kernel get scheduled, and wait
+  // for the previous one before reading memory.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   float acc[TQ][VK];
 #pragma unroll
@@ -274,7 +278,7 @@ tp_status direct_prepare(const Layer& L, const tp_schedule& s, const void* x, co
   plan->block = dim3(s.threads);
   plan->smem = sm ? (size_t)direct_smem_bytes(L, s.threads, s.tile_q, s.vec_k, s.tile_p) : 0;
   if (plan->smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(plan->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem);
+    cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
       return TP_ECUDA;
@@ -285,14 +289,21 @@ tp_status direct_prepare(const Layer& L, const tp_schedule& s, const void* x, co
 
 cudaError_t direct_launch(const DirectPlan& plan, cudaStream_t stream) {
   DirectFn fn = reinterpret_cast<DirectFn>(const_cast<void*>(plan.fn));
-  fn<<<plan.grid, plan.block, plan.smem, stream>>>(plan.args);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = plan.grid;
+  cfg.blockDim = plan.block;
+  cfg.dynamicSmemBytes = plan.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fn, plan.args);
 }
 
 int direct_occupancy(const DirectPlan& plan) {
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, plan.fn, plan.block.x, plan.smem) != cudaSuccess) return 1;
-  return n < 1 ? 1 : n;
+  return cached_occupancy(plan.fn, plan.block.x, plan.smem);
 }
 
 }  // namespace tp

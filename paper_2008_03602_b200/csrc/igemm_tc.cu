@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "tp_kernels.h"
 
@@ -106,13 +107,6 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t swz_byte
   return d;
 }
 
-__device__ __forceinline__ float apply_epi(float v, int n, const float* __restrict__ bias, int has_bias,
-                                           int relu) {
-  if (has_bias) v += __ldg(bias + n);
-  if (relu) v = fmaxf(v, 0.0f);
-  return v;
-}
-
 // Store 16 consecutive output channels [n0, n0+16) of row m.
 __device__ __forceinline__ void store16(void* y, int64_t m, int K, int n0, const float (&v)[16], int out_f32) {
   if (out_f32) {
@@ -144,30 +138,91 @@ __device__ __forceinline__ void store16(void* y, int64_t m, int K, int n0, const
   }
 }
 
-template <int BM, int BN>
+// Timeline slots per CTA when tracing (SM clock64 cycles): 0 entry, 1 prologue
+// done, 2 epilogue start (tmem_full seen), 3 end, 4.. MMA-thread full-barrier
+// completions of the first kTraceK k-blocks; slot 31 = %globaltimer (ns) at
+// entry and slot 30 = %smid, for cross-CTA skew.
+constexpr int kTraceSlots = 64, kTraceK = 16;   // 4..19 MMA full-wait done, 20..35 producer
+                                                   // after empty-wait, 36..51 MMA after commit
+__device__ __forceinline__ unsigned long long gtimer() { return (unsigned long long)clock64(); }
+
+template <int BM, int BN, int BK>
 __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+  // Compile-time tile geometry: one swizzle row holds SUBK channels (32/64/128 B).
+  constexpr int SUBK = BK < 64 ? BK : 64;
+  constexpr int NSUB = BK / SUBK;
+  constexpr uint32_t SWZ = SUBK * 2;
+  constexpr uint32_t A_SUB = BM * SUBK * 2, B_SUB = BN * SUBK * 2;
+  constexpr uint32_t A_STAGE = A_SUB * NSUB, B_STAGE = B_SUB * NSUB;
+  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(BM >> 4) << 24);   // bf16 x bf16 -> f32, K-major A and B
+
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int bk = a.bk, stages = a.stages;
-  const int sub_k = bk < 64 ? bk : 64;             // channels per swizzle row
-  const int nsub = bk / sub_k;                     // 1, or 2 for BK = 128
-  const uint32_t swz = (uint32_t)sub_k * 2;        // 32 / 64 / 128 bytes
-  const uint32_t a_sub_bytes = BM * sub_k * 2, b_sub_bytes = BN * sub_k * 2;
-  const uint32_t a_stage_bytes = a_sub_bytes * nsub, b_stage_bytes = b_sub_bytes * nsub;
-
+  const int stages = a.stages;
   uint8_t* a_tiles = smem_raw;
-  uint8_t* b_tiles = a_tiles + (size_t)stages * a_stage_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(b_tiles + (size_t)stages * b_stage_bytes);
+  uint8_t* b_tiles = a_tiles + (size_t)stages * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(b_tiles + (size_t)stages * B_STAGE);
   uint64_t* empty = full + stages;
   uint64_t* tmem_full = empty + stages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
+  unsigned long long* trace =
+      a.trace ? a.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTraceSlots
+              : nullptr;
+  if (trace && threadIdx.x == 0) {
+    trace[0] = gtimer();
+    unsigned long long g;
+    unsigned sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    trace[63] = g;
+    trace[62] = sm;
+  }
+  // Let the next kernel in the stream be scheduled now (programmatic dependent
+  // launch); it waits in griddepcontrol.wait before touching memory.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
   const int kb0 = (int)(((int64_t)split * a.kblocks) / a.split_k);
   const int kb1 = (int)(((int64_t)(split + 1) * a.kblocks) / a.split_k);
-  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  const int nkb = kb1 - kb0;
+
+  // Output-pixel origin of this M tile -> im2col base coordinate (lower corner = -pad).
+  const int64_t m0 = (int64_t)m_tile * BM;
+  const int q0 = (int)(m0 % a.Q);
+  const int64_t t0 = m0 / a.Q;
+  const int p0 = (int)(t0 % a.P);
+  const int n0 = (int)(t0 / a.P);
+  const int cw = q0 * a.sw - a.pw, ch = p0 * a.sh - a.ph;
+  const int nbase = n_tile * BN;
+
+  // Producer state: filter tap (r, s) and channel block of the next k-block,
+  // advanced incrementally (no divisions in the loop).
+  int p_cb = 0, p_s = 0, p_r = 0, p_stage = 0, p_kb = kb0;
+  uint32_t p_phase = 0;
+  auto produce = [&](void) {
+    uint8_t* sa = a_tiles + (size_t)p_stage * A_STAGE;
+    uint8_t* sbp = b_tiles + (size_t)p_stage * B_STAGE;
+    mbar_arrive_expect_tx(full + p_stage, ((a.dbg & 1) ? 0u : A_STAGE) + ((a.dbg & 2) ? 0u : B_STAGE));
+    const int c0 = p_cb * BK;
+#pragma unroll
+    for (int sb = 0; sb < NSUB; ++sb) {
+      if (!(a.dbg & 1))
+        tma_load_im2col_4d(sa + sb * A_SUB, &tmA, full + p_stage, c0 + sb * SUBK, cw, ch, n0, (uint16_t)p_s,
+                           (uint16_t)p_r);
+      if (!(a.dbg & 2)) tma_load_tile_4d(sbp + sb * B_SUB, &tmB, full + p_stage, c0 + sb * SUBK, p_s, p_r, nbase);
+    }
+    if (++p_cb == a.cblocks) {
+      p_cb = 0;
+      if (++p_s == a.S) { p_s = 0; ++p_r; }
+    }
+    if (++p_stage == stages) { p_stage = 0; p_phase ^= 1u; }
+    ++p_kb;
+  };
 
   if (threadIdx.x == 0) {
     if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // swizzle atoms need 1 KiB alignment
@@ -176,6 +231,15 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    const int rs = kb0 / a.cblocks;
+    p_cb = kb0 - rs * a.cblocks;
+    p_s = rs % a.S;
+    p_r = rs / a.S;
+    // Wait for the previous grid (PDL), then fill the whole ring before the
+    // CTA-wide sync so the first loads overlap the TMEM allocation.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int pre = nkb < stages ? nkb : stages;
+    for (int i = 0; i < pre; ++i) produce();
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -187,63 +251,46 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-
-  // Output-pixel origin of this M tile -> im2col base coordinate (lower corner = -pad).
-  const int64_t m0 = (int64_t)m_tile * BM;
-  const int q0 = (int)(m0 % a.Q);
-  const int64_t t0 = m0 / a.Q;
-  const int p0 = (int)(t0 % a.P);
-  const int n0 = (int)(t0 / a.P);
-  const int cw = q0 * a.sw - a.pw, ch = p0 * a.sh - a.ph;
+  if (trace && threadIdx.x == 0) trace[1] = gtimer();
 
   if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int kb = kb0; kb < kb1; ++kb) {
-      mbar_wait(empty + stage, phase ^ 1u);
-      mbar_arrive_expect_tx(full + stage, a_stage_bytes + b_stage_bytes);
-      const int rs = kb / a.cblocks, cbi = kb - rs * a.cblocks;
-      const int r = rs / a.S, s = rs - r * a.S;
-      const int c0 = cbi * bk;
-      for (int sb = 0; sb < nsub; ++sb) {
-        tma_load_im2col_4d(a_tiles + (size_t)stage * a_stage_bytes + sb * a_sub_bytes, &tmA, full + stage,
-                           c0 + sb * sub_k, cw, ch, n0, (uint16_t)s, (uint16_t)r);
-        tma_load_tile_4d(b_tiles + (size_t)stage * b_stage_bytes + sb * b_sub_bytes, &tmB, full + stage,
-                         c0 + sb * sub_k, s, r, n_tile * BN);
-      }
-      if (++stage == stages) { stage = 0; phase ^= 1u; }
+    // ---------------- TMA producer (rest of the k-blocks) ----------------
+    while (p_kb < kb1) {
+      mbar_wait(empty + p_stage, p_phase ^ 1u);
+      if (trace && p_kb - kb0 < kTraceK) trace[20 + p_kb - kb0] = gtimer();
+      produce();
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread) ----------------
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+    const uint64_t adesc0 = make_sdesc(smem_u32(a_tiles), SWZ);
+    const uint64_t bdesc0 = make_sdesc(smem_u32(b_tiles), SWZ);
     int stage = 0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, soff_a = 0, soff_b = 0;
     for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(full + stage, phase);
       tc_fence_after();
-      const uint32_t a_base = smem_u32(a_tiles + (size_t)stage * a_stage_bytes);
-      const uint32_t b_base = smem_u32(b_tiles + (size_t)stage * b_stage_bytes);
-      for (int kk = 0; kk < bk / 16; ++kk) {
-        const int sb = (kk * 16) / sub_k;
-        const uint32_t koff = (uint32_t)((kk * 16) % sub_k) * 2;
-        const uint64_t ad = make_sdesc(a_base + sb * a_sub_bytes + koff, swz);
-        const uint64_t bd = make_sdesc(b_base + sb * b_sub_bytes + koff, swz);
-        tc_mma(tmem_base, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+      if (trace && kb - kb0 < kTraceK) trace[4 + kb - kb0] = gtimer();
+      const uint64_t ad = adesc0 + soff_a, bd = bdesc0 + soff_b;
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk) {
+        constexpr int kPerSub = SUBK / 16;
+        const uint32_t sb = kk / kPerSub, koff = (kk % kPerSub) * 32;   // compile-time after unroll
+        tc_mma(tmem_base, ad + ((sb * A_SUB + koff) >> 4), bd + ((sb * B_SUB + koff) >> 4), IDESC,
+               (kb > kb0 || kk > 0) ? 1u : 0u);
       }
       tc_commit(empty + stage);
-      if (++stage == stages) { stage = 0; phase ^= 1u; }
+      if (trace && kb - kb0 < kTraceK) trace[36 + kb - kb0] = gtimer();
+      soff_a += A_STAGE >> 4;
+      soff_b += B_STAGE >> 4;
+      if (++stage == stages) { stage = 0; phase ^= 1u; soff_a = 0; soff_b = 0; }
     }
     tc_commit(tmem_full);
   }
 
   // ---------------- epilogue (all warps) ----------------
-  __syncwarp();
-  mbar_wait(tmem_full, 0);
-  tc_fence_after();
   const int quad = warp & 3, ngroups = blockDim.x >> 7, cgroup = warp >> 2;
   const int cols = BN / ngroups;
+  const int c_begin = cgroup * cols, c_end = c_begin + cols;
   const int row = (BM == 128) ? quad * 32 + lane : quad * 16 + lane;
   const bool row_ok = (BM == 128 || lane < 16);
   const int64_t m = m0 + row;
@@ -251,17 +298,41 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   const int64_t tile = (int64_t)m_tile * gridDim.y + n_tile;
   const int64_t n_tiles = (int64_t)gridDim.x * gridDim.y;
 
-  for (int c = cgroup * cols; c < (cgroup + 1) * cols; c += 16) {
+  // Bias for a 16-column chunk (vector loads, broadcast across the warp).
+  auto load_bias16 = [&](int nb, float (&bv)[16]) {
+#pragma unroll
+    for (int g = 0; g < 16; g += 4) {
+      if (a.has_bias && nb + g + 4 <= a.K) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
+        bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
+      } else {
+        bv[g] = bv[g + 1] = bv[g + 2] = bv[g + 3] = 0.0f;
+      }
+    }
+  };
+  float bias_next[16];
+  load_bias16(nbase + c_begin, bias_next);   // prefetch while the mainloop runs
+
+  __syncwarp();
+  mbar_wait(tmem_full, 0);
+  tc_fence_after();
+  if (trace && threadIdx.x == 0) trace[2] = gtimer();
+
+  for (int c = c_begin; c < c_end; c += 16) {
     uint32_t raw[16];
     tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c, raw);
-    const int nb = n_tile * BN + c;
+    const int nb = nbase + c;
+    float bv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bv[i] = bias_next[i];
+    if (c + 16 < c_end) load_bias16(nb + 16, bias_next);
     if (a.split_k == 1) {
       if (m_ok && nb < a.K) {
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int n = nb + i < a.K ? nb + i : a.K - 1;
-          v[i] = apply_epi(__uint_as_float(raw[i]), n, a.bias, a.has_bias, a.relu);
+          float t = __uint_as_float(raw[i]) + bv[i];
+          v[i] = a.relu ? fmaxf(t, 0.0f) : t;
         }
         store16(a.y, m, a.K, nb, v, a.out_f32);
       }
@@ -285,10 +356,11 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     __syncthreads();
     if (*last_flag) {
       __threadfence();
-      for (int c = cgroup * cols; c < (cgroup + 1) * cols; c += 16) {
-        const int nb = n_tile * BN + c;
+      for (int c = c_begin; c < c_end; c += 16) {
+        const int nb = nbase + c;
         if (!m_ok || nb >= a.K) continue;
-        float v[16];
+        float v[16], bv[16];
+        load_bias16(nb, bv);
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = 0.0f;
         for (int sp = 0; sp < a.split_k; ++sp) {   // fixed order -> deterministic
@@ -301,8 +373,8 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int n = nb + i < a.K ? nb + i : a.K - 1;
-          v[i] = apply_epi(v[i], n, a.bias, a.has_bias, a.relu);
+          const float t = v[i] + bv[i];
+          v[i] = a.relu ? fmaxf(t, 0.0f) : t;
         }
         store16(a.y, m, a.K, nb, v, a.out_f32);
       }
@@ -312,6 +384,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 
   tc_fence_before();
   __syncthreads();
+  if (trace && threadIdx.x == 0) trace[3] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
@@ -322,9 +395,20 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 // ------------------------------------------------------------- host side
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
 
-static KernelFn pick_tc(int bm, int bn) {
+template <int BM, int BN>
+static KernelFn pick_bk(int bk) {
+  switch (bk) {
+    case 16: return igemm_tc_kernel<BM, BN, 16>;
+    case 32: return igemm_tc_kernel<BM, BN, 32>;
+    case 64: return igemm_tc_kernel<BM, BN, 64>;
+    case 128: return igemm_tc_kernel<BM, BN, 128>;
+  }
+  return nullptr;
+}
+
+static KernelFn pick_tc(int bm, int bn, int bk) {
 #define TP_TC_CASE(M_, N_) \
-  if (bm == M_ && bn == N_) return igemm_tc_kernel<M_, N_>;
+  if (bm == M_ && bn == N_) return pick_bk<M_, N_>(bk);
   TP_TC_CASE(64, 32) TP_TC_CASE(64, 64) TP_TC_CASE(64, 128) TP_TC_CASE(64, 256)
   TP_TC_CASE(128, 32) TP_TC_CASE(128, 64) TP_TC_CASE(128, 128) TP_TC_CASE(128, 256)
 #undef TP_TC_CASE
@@ -374,14 +458,19 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.kblocks = pb.R * pb.S * a.cblocks;
   a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
   a.ws_partial = pb.ws_partial; a.ws_counters = pb.ws_counters;
-  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn));
-  if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN"); return TP_EINVALID_CONFIG; }
+  a.trace = pb.trace;
+  {
+    static const int dbg = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
+    a.dbg = dbg;
+  }
+  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk));
+  if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN x BK"); return TP_EINVALID_CONFIG; }
   plan->grid = dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn),
                     (unsigned)pb.split_k);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
   plan->block = dim3(pb.threads);
   plan->smem = tc_dyn_smem(pb.bm, pb.bn, pb.bk, pb.stages);
-  cudaError_t e = cudaFuncSetAttribute(plan->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan->smem);
+  cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
   if (e != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     return TP_ECUDA;
@@ -391,14 +480,21 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
 
 cudaError_t tc_launch(const TcPlan& plan, cudaStream_t stream) {
   KernelFn fn = reinterpret_cast<KernelFn>(const_cast<void*>(plan.fn));
-  fn<<<plan.grid, plan.block, plan.smem, stream>>>(plan.tmA, plan.tmB, plan.args);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = plan.grid;
+  cfg.blockDim = plan.block;
+  cfg.dynamicSmemBytes = plan.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fn, plan.tmA, plan.tmB, plan.args);
 }
 
 int tc_occupancy(const TcPlan& plan) {
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, plan.fn, plan.block.x, plan.smem) != cudaSuccess) return 1;
-  return n < 1 ? 1 : n;
+  return cached_occupancy(plan.fn, plan.block.x, plan.smem);
 }
 
 }  // namespace tp

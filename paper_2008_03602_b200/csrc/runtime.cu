@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -96,6 +97,52 @@ const DriverApi& driver() {
     api.ok = ok;
   });
   return api;
+}
+
+bool pdl_enabled() {
+  static const bool on = !(getenv("TP_PDL") && atoi(getenv("TP_PDL")) == 0);
+  return on;
+}
+
+static std::mutex g_cache_mu;
+static std::map<std::pair<const void*, CUcontext>, size_t> g_smem_attr;
+static std::map<std::tuple<const void*, int, size_t, CUcontext>, int> g_occ;
+
+static CUcontext current_ctx() {
+  CUcontext c = nullptr;
+  driver().ctxGetCurrent(&c);
+  return c;
+}
+
+cudaError_t ensure_smem_attr(const void* fn, size_t smem) {
+  const auto key = std::make_pair(fn, current_ctx());
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_smem_attr.find(key);
+    if (it != g_smem_attr.end() && it->second >= smem) return cudaSuccess;
+  }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    size_t& v = g_smem_attr[key];
+    v = std::max(v, smem);
+  }
+  return e;
+}
+
+int cached_occupancy(const void* fn, int block, size_t smem) {
+  const auto key = std::make_tuple(fn, block, smem, current_ctx());
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+  }
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem) != cudaSuccess) n = 1;
+  n = std::max(1, n);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_occ[key] = n;
+  return n;
 }
 
 // ---------------------------------------------------------------- device state
@@ -519,43 +566,248 @@ static tp_status gate_check(tp_partition* part, const ConvPlan& plan, Gate* g, t
 }
 
 // ---------------------------------------------------------------- tuner core
+// Enumerate the layer's space once (space_get is O(|space|) per call).
+static std::vector<tp_schedule> space_table(const Layer& L) {
+  std::vector<tp_schedule> t;
+  const int64_t n = space_size(L);
+  t.reserve(n);
+  for (int64_t i = 0; i < n; ++i) {
+    tp_schedule s;
+    space_get(L, i, &s);
+    t.push_back(s);
+  }
+  return t;
+}
+
+// Pipelined profiling loop (a10 + a11 for a list of candidates).  No host
+// synchronisation per candidate: phase A enqueues every candidate's gate run
+// (poison y, one launch bracketed by events for t_est, gather the check
+// points) and syncs once per chunk; phase B keeps a window of candidates in
+// flight -- each one's timing groups are captured once as a CUDA graph of n
+// launches and replayed `groups` times between event records -- harvesting the
+// oldest when the window is full.  The GPU never waits for the host between
+// candidates, which is what the long-lived server of P:844-846 buys.
 static tp_status measure_candidates(const Layer& L, tp_partition* part, const int64_t* cand, int32_t n_cand,
                                     const void* x, const void* w, const void* bias, void* y, void* ws,
                                     size_t ws_bytes, Gate* gate, const tp_timing& tm, tp_measurement* records,
                                     int32_t cap, int32_t* n_records) {
-  EventPool pool;
-  int32_t nrec = 0;
-  for (int32_t i = 0; i < n_cand; ++i) {
+  cudaStream_t st = part->stream;
+  const std::vector<tp_schedule> table = space_table(L);
+  const int groups = std::max(1, tm.groups);
+  const int ncheck = (int)gate->idx.size();
+  const size_t ybytes = (size_t)L.M * L.d.k * (L.d.out_dtype == TP_DTYPE_BF16 ? 2 : 4);
+  const int kChunk = 128, kWindow = 24;
+
+  struct Cand {
     tp_measurement m;
+    ConvPlan plan;
+    bool live = false;       // passed make_plan + gate
+    double t_est = 0;
+    int n = 0;
+    cudaGraphExec_t exec = nullptr;
+    int slot = -1;           // event slot in phase B
+  };
+  std::vector<Cand> cs(n_cand);
+  for (int32_t i = 0; i < n_cand; ++i) {
+    tp_measurement& m = cs[i].m;
     std::memset(&m, 0, sizeof(m));
     m.device = part->device;
     m.sm_requested = part->sm_requested;
     m.sm_granted = part->sm_granted;
     m.space_index = cand[i];
-    tp_schedule s;
-    if (!space_get(L, cand[i], &s)) {
-      m.status = TP_EINVALID_CONFIG;
-    } else {
-      ConvPlan plan;
-      tp_status st = make_plan(L, s, x, w, bias, y, ws, ws_bytes, &plan);
-      if (st == TP_OK) {
-        plan_geometry(plan, part->sm_granted, &m);
-        st = gate_check(part, plan, gate, &m);
-        if (st == TP_OK) st = time_plan(part, plan, tm, pool, &m);
+  }
+  if (tm.flush_l2) {   // cold-L2 protocol: sequential path (one event pair per launch)
+    EventPool pool;
+    for (int32_t i = 0; i < n_cand; ++i) {
+      Cand& c = cs[i];
+      if (cand[i] < 0 || cand[i] >= (int64_t)table.size()) { c.m.status = TP_EINVALID_CONFIG; continue; }
+      tp_status s2 = make_plan(L, table[cand[i]], x, w, bias, y, ws, ws_bytes, &c.plan);
+      if (s2 == TP_OK) {
+        plan_geometry(c.plan, part->sm_granted, &c.m);
+        s2 = gate_check(part, c.plan, gate, &c.m);
+        if (s2 == TP_OK) s2 = time_plan(part, c.plan, tm, pool, &c.m);
       }
-      m.status = st;
-      if (st == TP_ECUDA) {
-        // A sticky device error poisons the context; surface it to the caller.
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess && cudaDeviceSynchronize() != cudaSuccess) {
-          if (nrec < cap) records[nrec++] = m;
-          *n_records = nrec;
-          return TP_ECUDA;
+      c.m.status = s2;
+    }
+  } else {
+    // ---------------- phase A: gate runs, chunked ----------------
+    double* d_vals = nullptr;
+    TP_CK(cudaMalloc(&d_vals, sizeof(double) * (size_t)std::max(1, ncheck) * kChunk));
+    std::vector<double> h_vals((size_t)std::max(1, ncheck) * kChunk);
+    EventPool pa;
+    TP_CK(pa.ensure(2 * kChunk));
+    tp_status err = TP_OK;
+    for (int32_t c0 = 0; c0 < n_cand && err == TP_OK; c0 += kChunk) {
+      const int32_t c1 = std::min(n_cand, c0 + kChunk);
+      for (int32_t i = c0; i < c1; ++i) {
+        Cand& c = cs[i];
+        if (cand[i] < 0 || cand[i] >= (int64_t)table.size()) { c.m.status = TP_EINVALID_CONFIG; continue; }
+        tp_status s2 = make_plan(L, table[cand[i]], x, w, bias, y, ws, ws_bytes, &c.plan);
+        if (s2 != TP_OK) { c.m.status = s2; continue; }
+        plan_geometry(c.plan, part->sm_granted, &c.m);
+        cudaError_t e = cudaMemsetAsync(y, 0xFF, ybytes, st);   // NaN in bf16 and fp32
+        if (e == cudaSuccess) e = cudaEventRecord(pa.ev[2 * (i - c0)], st);
+        if (e == cudaSuccess) e = launch_plan(c.plan, st);
+        if (e == cudaSuccess) e = cudaEventRecord(pa.ev[2 * (i - c0) + 1], st);
+        if (e == cudaSuccess)
+          e = launch_gather(y, L.d.in_layout == TP_LAYOUT_NHWC, L.d.out_dtype == TP_DTYPE_FP32, L.d.n, L.d.k, L.P,
+                            L.Q, gate->d_idx, ncheck, d_vals + (size_t)(i - c0) * ncheck, st);
+        if (e != cudaSuccess) {
+          c.m.status = TP_ECUDA;
+          set_error(std::string("gate launch: ") + cudaGetErrorString(e));
+          continue;
+        }
+        g_launches += 1;
+        c.live = true;
+      }
+      cudaError_t e = cudaMemcpyAsync(h_vals.data(), d_vals, sizeof(double) * (size_t)ncheck * (c1 - c0),
+                                      cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) {
+        set_error(std::string("gate sync: ") + cudaGetErrorString(e));
+        err = TP_ECUDA;
+        break;
+      }
+      for (int32_t i = c0; i < c1; ++i) {
+        Cand& c = cs[i];
+        if (!c.live) continue;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, pa.ev[2 * (i - c0)], pa.ev[2 * (i - c0) + 1]);
+        c.t_est = std::max(1e-3, ms * 1000.0);
+        const double* v = h_vals.data() + (size_t)(i - c0) * ncheck;
+        bool finite = true;
+        for (int j = 0; j < ncheck; ++j) finite = finite && std::isfinite(v[j]);
+        if (!gate->have_ref && finite) {
+          gate->ref.assign(v, v + ncheck);
+          gate->have_ref = true;
+        }
+        double e2 = 0, mref = 0;
+        if (gate->have_ref)
+          for (int j = 0; j < ncheck; ++j) {
+            e2 = std::max(e2, std::fabs(v[j] - gate->ref[j]));
+            mref = std::max(mref, std::fabs(gate->ref[j]));
+          }
+        c.m.max_abs_err = finite ? e2 : NAN;
+        c.m.max_ref = mref;
+        if (!finite || !(e2 <= gate->tol * std::max(mref, 1e-30))) {
+          c.m.status = TP_EMISMATCH;
+          c.live = false;
         }
       }
     }
-    if (nrec < cap) records[nrec++] = m;
+    cudaFree(d_vals);
+    if (err != TP_OK) {
+      for (int32_t i = 0; i < n_cand; ++i)
+        if (i < cap) records[i] = cs[i].m;
+      *n_records = std::min(cap, n_cand);
+      return err;
+    }
+
+    // ---------------- phase B: timing, windowed pipeline ----------------
+    EventPool pb;
+    TP_CK(pb.ensure((size_t)kWindow * 2 * groups));
+    std::vector<int> free_slots;
+    for (int i = kWindow - 1; i >= 0; --i) free_slots.push_back(i);
+    std::vector<int32_t> inflight;   // candidate indices, in enqueue order
+    auto harvest = [&](int32_t i) -> tp_status {
+      Cand& c = cs[i];
+      cudaEvent_t* ev = pb.ev.data() + (size_t)c.slot * 2 * groups;
+      cudaError_t e = cudaEventSynchronize(ev[2 * groups - 1]);
+      std::vector<double> per;
+      for (int g = 0; g < groups && e == cudaSuccess; ++g) {
+        float ms = 0;
+        e = cudaEventElapsedTime(&ms, ev[2 * g], ev[2 * g + 1]);
+        per.push_back(ms * 1000.0 / c.n);
+      }
+      if (c.exec) cudaGraphExecDestroy(c.exec);
+      c.exec = nullptr;
+      free_slots.push_back(c.slot);
+      if (e != cudaSuccess) {
+        c.m.status = TP_ECUDA;
+        set_error(std::string("timing: ") + cudaGetErrorString(e));
+        return TP_ECUDA;
+      }
+      std::vector<double> srt = per;
+      std::sort(srt.begin(), srt.end());
+      const size_t k = srt.size();
+      c.m.median_us = (k % 2) ? srt[k / 2] : 0.5 * (srt[k / 2 - 1] + srt[k / 2]);
+      c.m.min_us = srt.front();
+      double mean = 0, var = 0;
+      for (double v : per) mean += v;
+      mean /= k;
+      for (double v : per) var += (v - mean) * (v - mean);
+      c.m.mean_us = mean;
+      c.m.std_us = k > 1 ? std::sqrt(var / (k - 1)) : 0.0;
+      c.m.groups = groups;
+      c.m.n_per_group = c.n;
+      c.m.status = TP_OK;
+      return TP_OK;
+    };
+    for (int32_t i = 0; i < n_cand && err == TP_OK; ++i) {
+      Cand& c = cs[i];
+      if (!c.live) continue;
+      if (free_slots.empty()) {
+        err = harvest(inflight.front());
+        inflight.erase(inflight.begin());
+        if (err != TP_OK) break;
+      }
+      c.slot = free_slots.back();
+      free_slots.pop_back();
+      c.n = std::min(4096, std::max(std::max(1, tm.n_min), (int)std::ceil(tm.target_group_us / c.t_est)));
+      cudaError_t e = cudaSuccess;
+      for (int k = 0; k < std::max(0, tm.warmup) && e == cudaSuccess; ++k) e = launch_plan(c.plan, st);
+      if (e == cudaSuccess && tm.use_graph) {
+        cudaGraph_t graph = nullptr;
+        e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        cudaError_t ce = cudaSuccess;
+        for (int k = 0; k < c.n && ce == cudaSuccess && e == cudaSuccess; ++k) ce = launch_plan(c.plan, st);
+        if (e == cudaSuccess) {
+          cudaError_t ee = cudaStreamEndCapture(st, &graph);
+          g_launches -= (int64_t)c.n * c.plan.kernels_per_call;   // capture does not launch
+          e = ce != cudaSuccess ? ce : ee;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&c.exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+      }
+      cudaEvent_t* ev = pb.ev.data() + (size_t)c.slot * 2 * groups;
+      for (int g = 0; g < groups && e == cudaSuccess; ++g) {
+        e = cudaEventRecord(ev[2 * g], st);
+        if (e == cudaSuccess) {
+          if (c.exec) {
+            e = cudaGraphLaunch(c.exec, st);
+            g_launches += (int64_t)c.n * c.plan.kernels_per_call;
+          } else {
+            for (int k = 0; k < c.n && e == cudaSuccess; ++k) e = launch_plan(c.plan, st);
+          }
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(ev[2 * g + 1], st);
+      }
+      if (e != cudaSuccess) {
+        c.m.status = TP_ECUDA;
+        set_error(std::string("timing enqueue: ") + cudaGetErrorString(e));
+        if (c.exec) cudaGraphExecDestroy(c.exec);
+        c.exec = nullptr;
+        free_slots.push_back(c.slot);
+        cudaGetLastError();
+        if (cudaStreamSynchronize(st) != cudaSuccess) err = TP_ECUDA;
+        continue;
+      }
+      inflight.push_back(i);
+    }
+    for (int32_t i : inflight) {
+      tp_status h = harvest(i);
+      if (err == TP_OK) err = h;
+    }
+    if (err != TP_OK) {
+      for (int32_t i = 0; i < n_cand; ++i)
+        if (i < cap) records[i] = cs[i].m;
+      *n_records = std::min(cap, n_cand);
+      return err;
+    }
   }
+  int32_t nrec = 0;
+  for (int32_t i = 0; i < n_cand; ++i)
+    if (nrec < cap) records[nrec++] = cs[i].m;
   *n_records = nrec;
   return TP_OK;
 }
@@ -786,6 +1038,44 @@ tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partitio
   m.status = st;
   if (out) *out = m;
   return st;
+}
+
+tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part, const void* x,
+                          const void* w, const void* bias, void* y, void* ws, size_t ws_bytes, uint64_t* trace_host,
+                          int32_t cap, int32_t* rows) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  if (!s || !trace_host || !rows) { set_error("null argument"); return TP_EINVAL; }
+  if (s->kind != TP_KIND_IGEMM_TC) { set_error("tracing is implemented for IGEMM_TC"); return TP_EUNSUPPORTED; }
+  tp_partition* p;
+  st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  std::lock_guard<std::mutex> lk(p->mu);
+  TP_CK(cudaSetDevice(p->device));
+  ConvPlan plan;
+  {
+    CtxGuard g(p);
+    st = make_plan(L, *s, x, w, bias, y, ws, ws_bytes, &plan);
+  }
+  if (st != TP_OK) return st;
+  const int64_t ctas = (int64_t)plan.tc.grid.x * plan.tc.grid.y * plan.tc.grid.z;
+  if (ctas > cap) { set_error("trace capacity too small"); return TP_EINVAL; }
+  unsigned long long* dtr = nullptr;
+  TP_CK(cudaMalloc(&dtr, ctas * 64 * sizeof(unsigned long long)));
+  TP_CK(cudaMemset(dtr, 0, ctas * 64 * sizeof(unsigned long long)));
+  plan.tc.args.trace = dtr;
+  cudaError_t e;
+  {
+    CtxGuard g(p);
+    e = launch_plan(plan, p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(trace_host, dtr, ctas * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaFree(dtr);
+  TP_CK(e);
+  *rows = (int32_t)ctas;
+  return TP_OK;
 }
 
 tp_status tp_tune_subset(const tp_conv_desc* d, tp_partition* part, const int64_t* cand, int32_t n_cand,

@@ -38,6 +38,15 @@ struct DriverApi {
 };
 const DriverApi& driver();
 
+// Programmatic dependent launch (PDL) for back-to-back kernels in a stream:
+// on unless TP_PDL=0.  Kernels call griddepcontrol.wait before reading memory.
+bool pdl_enabled();
+
+// Per-(function, context) caches of launch-time queries (host-side hot path of
+// the tuner): the max-dynamic-smem attribute and the occupancy calculator.
+cudaError_t ensure_smem_attr(const void* fn, size_t smem);
+int cached_occupancy(const void* fn, int block, size_t smem);
+
 // ---------------------------------------------------------------- igemm_tc
 struct TcArgs {
   int64_t M;
@@ -48,6 +57,8 @@ struct TcArgs {
   int out_f32, relu, has_bias;
   float* ws_partial;
   int* ws_counters;
+  unsigned long long* trace;   // optional per-CTA timeline (tp_conv2d_trace), nullptr = off
+  int dbg;                     // TP_DEBUG_TC env (experiments only): bit0 skip A TMA, bit1 skip B TMA
 };
 
 struct TcProblem {
@@ -62,6 +73,7 @@ struct TcProblem {
   int out_f32, relu, has_bias;
   float* ws_partial;
   int* ws_counters;
+  unsigned long long* trace;
 };
 
 struct TcPlan {

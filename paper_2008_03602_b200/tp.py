@@ -94,6 +94,8 @@ _sig("tp_tune", _P(ConvDesc), _vp, _i32, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _P(
 _sig("tp_tune_subset", _P(ConvDesc), _vp, _P(_i64), _i32, _vp, _vp, _vp, _vp, _vp, _sz, _P(_i64), _P(_dbl), _i32,
      _dbl, _P(Timing), _P(Measurement), _i32, _P(_i32))
 _sig("tp_cross_eval", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(Timing), _P(Measurement))
+_sig("tp_conv2d_trace", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(_u64), _i32, _P(_i32))
+_sig("tp_conv2d_trace", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(_u64), _i32, _P(_i32))
 _sig("tp_pack_input", _P(ConvDesc), _vp, _vp, _vp)
 _sig("tp_pack_weights", _P(ConvDesc), _vp, _vp, _vp)
 _sig("tp_gather_output", _P(ConvDesc), _vp, _vp, _P(_i64), _i32, _P(_dbl))
@@ -351,6 +353,17 @@ def conv2d_run(buf: LayerBuffers, sched: dict, part: Partition | None = None, ti
                            ctypes.byref(timing_cfg) if timing_cfg is not None else None, ctypes.byref(m)),
         "tp_conv2d_run")
     return meas_to_dict(m)
+
+
+def conv2d_trace(buf: "LayerBuffers", sched: dict, part: Partition | None = None) -> np.ndarray:
+    """In-kernel timeline of one IGEMM_TC launch: (ctas, 64) uint64 (see tp.h)."""
+    x, w, b, y, ws, wsb = buf.ptrs()
+    cap = int(sched.get("grid_x", 0) * sched.get("grid_y", 0) * sched.get("grid_z", 0)) or 65536
+    out = np.zeros((cap, 64), dtype=np.uint64)
+    rows = _i32()
+    _ck(_lib.tp_conv2d_trace(ctypes.byref(buf.cd), ctypes.byref(dict_to_sched(sched)), _h(part), x, w, b, y, ws,
+                             wsb, out.ctypes.data_as(_P(_u64)), cap, ctypes.byref(rows)), "tp_conv2d_trace")
+    return out[:rows.value]
 
 
 def _check_arrays(check_idx, check_ref):

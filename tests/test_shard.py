@@ -1,0 +1,73 @@
+"""Sharder host logic on CPU with a world_size-2 gloo group."""
+import os
+import random
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import space as sp
+from paper_2008_03602_b200 import shard
+
+
+def _fake_records(n, seed):
+    rng = random.Random(seed)
+    return [dict(space_index=i, status=rng.choice([0, 0, 0, 5]), median_us=rng.choice([1.0, 1.5, 2.0, 2.5]),
+                 min_us=0.9, mean_us=1.0, std_us=0.1, sm_granted=148, ctas=10, threads_per_cta=128, waves=1)
+            for i in range(n)]
+
+
+def test_shards_disjoint_and_cover():
+    cand = sp.sample(920, 1000, 42)
+    for world in (1, 2, 3, 8):
+        parts = [shard.shard(cand, r, world) for r in range(world)]
+        flat = sorted(c for p in parts for c in p)
+        assert flat == sorted(cand)
+        assert sum(len(p) for p in parts) == len(set(flat))
+        assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+
+
+def test_merge_equals_single_list_argmin():
+    recs = _fake_records(300, 1)
+    single = sp.argmin(recs)
+    for world in (2, 4, 8):
+        blocks = [shard.pack(shard.shard(recs, r, world), 0, 7, r) for r in range(world)]
+        merged = shard.merge_best(shard.unpack(np.concatenate(blocks)))
+        assert merged[(0, 7)]["space_index"] == recs[single]["space_index"]
+
+
+def test_pack_roundtrip_exact():
+    recs = _fake_records(50, 2)
+    back = shard.unpack(shard.pack(recs, 3, 4, 1))
+    for a, b in zip(recs, back):
+        assert a["median_us"] == b["median_us"] and a["space_index"] == b["space_index"]
+        assert b["job"] == 3 and b["layer"] == 4 and b["rank"] == 1
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    recs = _fake_records(101, 9)
+    mine = shard.shard(recs, rank, world)
+    got = shard.gather_to_rank0(shard.pack(mine, 0, 0, rank))
+    if rank == 0:
+        merged = shard.merge_best(shard.unpack(got))
+        q.put((got.shape[0], merged[(0, 0)]["space_index"], recs[sp.argmin(recs)]["space_index"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_gather_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + random.randint(0, 2000)
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in ps)
+    n, merged_idx, single_idx = q.get(timeout=5)
+    assert n == 101
+    assert merged_idx == single_idx
