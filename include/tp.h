@@ -142,6 +142,15 @@ tp_status tp_partition_probe(tp_partition* part, int32_t ctas, int32_t* smids_de
 tp_status tp_partition_copy_bw(tp_partition* part, const void* src, void* dst, size_t bytes,
                                int32_t reps, double* gbps);
 
+/* Latency floor of the timing protocol inside the partition (SURVEY 8(d):
+ * the binding roof of a microsecond kernel is max(compute, HBM, this floor)).
+ * Times an EMPTY kernel of `ctas` x `threads` launched exactly like the conv
+ * kernels (same stream, PDL attribute, graph-captured groups, timing == NULL
+ * -> the C12 defaults) and returns the per-launch statistics in *out
+ * (space_index = -1, kind = 0).  Synchronous. */
+tp_status tp_partition_floor(tp_partition* part, int32_t ctas, int32_t threads, const tp_timing* timing,
+                             tp_measurement* out);
+
 /* ---- schedule space (host-only) ------------ */
 tp_status tp_output_shape(const tp_conv_desc* d, int32_t* p, int32_t* q);
 tp_status tp_layer_kind(const tp_conv_desc* d, int32_t* kind);

@@ -153,4 +153,25 @@ cudaError_t launch_l2_flush(void* buf, size_t bytes, int grid, cudaStream_t st) 
   return cudaGetLastError();
 }
 
+// Empty kernel with the same PDL protocol as the conv kernels: the measured
+// per-launch floor of the timing protocol (SURVEY 8(d) "empty-kernel floor").
+__global__ void empty_kernel(int* sink) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (sink && threadIdx.x == 0 && blockIdx.x == 0x7fffffff) *sink = 1;   // never taken
+}
+
+cudaError_t launch_empty(int ctas, int threads, int pdl, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, empty_kernel, (int*)nullptr);
+}
+
 }  // namespace tp

@@ -398,14 +398,16 @@ struct EventPool {
 };
 
 // Caller holds the partition lock and has its context current.
-static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_timing& tm, EventPool& pool,
-                           tp_measurement* out) {
+// `launch(st)` enqueues one call (kpc kernels) on st.
+template <class Launch>
+static tp_status time_launches(tp_partition* part, Launch launch, int kpc, const tp_timing& tm, EventPool& pool,
+                               tp_measurement* out) {
   cudaStream_t st = part->stream;
   const bool cold = tm.flush_l2 != 0;
   auto flush = [&]() { return launch_l2_flush(part->flush_buf, part->flush_bytes, 148 * 4, st); };
   for (int i = 0; i < std::max(0, tm.warmup); ++i) {
     if (cold) TP_CK(flush());
-    TP_CK(launch_plan(plan, st));
+    TP_CK(launch(st));
   }
   const int groups = std::max(1, tm.groups);
   std::vector<double> per;   // per-launch microseconds, one entry per group
@@ -417,7 +419,7 @@ static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_ti
       for (int i = 0; i < n; ++i) {
         TP_CK(flush());
         TP_CK(cudaEventRecord(pool.ev[2 * (g * n + i)], st));
-        TP_CK(launch_plan(plan, st));
+        TP_CK(launch(st));
         TP_CK(cudaEventRecord(pool.ev[2 * (g * n + i) + 1], st));
       }
     TP_CK(cudaStreamSynchronize(st));
@@ -436,7 +438,7 @@ static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_ti
     TP_CK(pool.ensure(2 * (size_t)groups + 2));
     const int n0 = std::max(1, tm.n_min);
     TP_CK(cudaEventRecord(pool.ev[0], st));
-    for (int i = 0; i < n0; ++i) TP_CK(launch_plan(plan, st));
+    for (int i = 0; i < n0; ++i) TP_CK(launch(st));
     TP_CK(cudaEventRecord(pool.ev[1], st));
     TP_CK(cudaEventSynchronize(pool.ev[1]));
     float ms0 = 0;
@@ -449,9 +451,9 @@ static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_ti
       cudaGraph_t graph = nullptr;
       TP_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       cudaError_t ce = cudaSuccess;
-      for (int i = 0; i < n && ce == cudaSuccess; ++i) ce = launch_plan(plan, st);
+      for (int i = 0; i < n && ce == cudaSuccess; ++i) ce = launch(st);
       cudaError_t ee = cudaStreamEndCapture(st, &graph);
-      g_launches -= (int64_t)n * plan.kernels_per_call;   // capture does not launch
+      g_launches -= (int64_t)n * kpc;   // capture does not launch
       if (ce != cudaSuccess || ee != cudaSuccess) {
         if (graph) cudaGraphDestroy(graph);
         set_error(std::string("graph capture failed: ") + cudaGetErrorString(ce != cudaSuccess ? ce : ee));
@@ -465,9 +467,9 @@ static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_ti
       TP_CK(cudaEventRecord(pool.ev[2 + 2 * g], st));
       if (exec) {
         TP_CK(cudaGraphLaunch(exec, st));
-        g_launches += (int64_t)n * plan.kernels_per_call;
+        g_launches += (int64_t)n * kpc;
       } else {
-        for (int i = 0; i < n; ++i) TP_CK(launch_plan(plan, st));
+        for (int i = 0; i < n; ++i) TP_CK(launch(st));
       }
       TP_CK(cudaEventRecord(pool.ev[3 + 2 * g], st));
     }
@@ -495,6 +497,12 @@ static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_ti
   out->std_us = k > 1 ? std::sqrt(var / (k - 1)) : 0.0;
   out->groups = groups;
   return TP_OK;
+}
+
+static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_timing& tm, EventPool& pool,
+                           tp_measurement* out) {
+  return time_launches(part, [&](cudaStream_t st) { return launch_plan(plan, st); }, plan.kernels_per_call, tm,
+                       pool, out);
 }
 
 // ---------------------------------------------------------------- correctness gate (a10)
@@ -983,6 +991,36 @@ tp_status tp_partition_copy_bw(tp_partition* part, const void* src, void* dst, s
   g_launches += 1 + std::max(1, reps);
   *gbps = best;
   return TP_OK;
+}
+
+tp_status tp_partition_floor(tp_partition* part, int32_t ctas, int32_t threads, const tp_timing* timing,
+                            tp_measurement* out) {
+  tp_partition* p;
+  tp_status st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  if (!out || ctas < 1 || threads < 1 || threads > 1024) { set_error("bad floor arguments"); return TP_EINVAL; }
+  std::memset(out, 0, sizeof(*out));
+  const tp_timing tm = timing ? *timing : default_timing();
+  std::lock_guard<std::mutex> lk(p->mu);
+  CtxGuard g(p);
+  EventPool pool;
+  const int pdl = pdl_enabled() ? 1 : 0;
+  st = time_launches(
+      p,
+      [&](cudaStream_t s) {
+        g_launches += 1;
+        return launch_empty(ctas, threads, pdl, s);
+      },
+      1, tm, pool, out);
+  out->ctas = ctas;
+  out->threads_per_cta = threads;
+  out->sm_requested = p->sm_requested;
+  out->sm_granted = p->sm_granted;
+  out->device = p->device;
+  out->waves = (int32_t)cdiv((int64_t)ctas, (int64_t)p->sm_granted);
+  out->status = st;
+  out->space_index = -1;
+  return st;
 }
 
 tp_status tp_workspace_size(const tp_conv_desc* d, const tp_schedule* s, size_t* bytes) {

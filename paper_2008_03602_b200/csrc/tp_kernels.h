@@ -126,5 +126,6 @@ cudaError_t launch_gather(const void* y, int layout_nhwc, int out_f32, int N, in
 cudaError_t launch_smid_probe(int ctas, int* smids, cudaStream_t st);
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, int grid, cudaStream_t st);
+cudaError_t launch_empty(int ctas, int threads, int pdl, cudaStream_t st);
 
 }  // namespace tp

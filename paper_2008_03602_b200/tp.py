@@ -79,6 +79,7 @@ _sig("tp_partition_info", _vp, _P(_i32), _P(_i32), _P(_i32), _P(_vp))
 _sig("tp_partition_sync", _vp)
 _sig("tp_partition_close", _vp)
 _sig("tp_partition_probe", _vp, _i32, _vp)
+_sig("tp_partition_floor", _vp, _i32, _i32, _P(Timing), _P(Measurement))
 _sig("tp_partition_copy_bw", _vp, _vp, _vp, _sz, _i32, _P(_dbl))
 _sig("tp_output_shape", _P(ConvDesc), _P(_i32), _P(_i32))
 _sig("tp_layer_kind", _P(ConvDesc), _P(_i32))
@@ -94,7 +95,6 @@ _sig("tp_tune", _P(ConvDesc), _vp, _i32, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _P(
 _sig("tp_tune_subset", _P(ConvDesc), _vp, _P(_i64), _i32, _vp, _vp, _vp, _vp, _vp, _sz, _P(_i64), _P(_dbl), _i32,
      _dbl, _P(Timing), _P(Measurement), _i32, _P(_i32))
 _sig("tp_cross_eval", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(Timing), _P(Measurement))
-_sig("tp_conv2d_trace", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(_u64), _i32, _P(_i32))
 _sig("tp_conv2d_trace", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(_u64), _i32, _P(_i32))
 _sig("tp_pack_input", _P(ConvDesc), _vp, _vp, _vp)
 _sig("tp_pack_weights", _P(ConvDesc), _vp, _vp, _vp)
@@ -265,6 +265,14 @@ class Partition:
         buf = torch.full((ctas,), -1, dtype=torch.int32, device=f"cuda:{self.device}")
         _ck(_lib.tp_partition_probe(self.handle, ctas, buf.data_ptr()), "tp_partition_probe")
         return buf.cpu().numpy()
+
+    def floor(self, ctas: int = 1, threads: int = 128, timing_cfg: "Timing | None" = None) -> dict:
+        """Per-launch latency of an empty kernel under the timing protocol."""
+        m = Measurement()
+        _ck(_lib.tp_partition_floor(self.handle, int(ctas), int(threads),
+                                    ctypes.byref(timing_cfg) if timing_cfg is not None else None, ctypes.byref(m)),
+            "tp_partition_floor")
+        return meas_to_dict(m)
 
     def copy_bw(self, nbytes: int = 1 << 30, reps: int = 5) -> float:
         import torch

@@ -1,0 +1,86 @@
+"""Summarise ncu outputs into profiles/ (run here, on the CPU box).
+
+  python tools/ncu_summary.py launches <launches.csv> <out.json>
+  python tools/ncu_summary.py full <prof.ncu-rep> <out.json>
+"""
+import collections
+import csv
+import io
+import json
+import subprocess
+import sys
+
+FULL_KEYS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+             "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size",
+             "launch__block_size", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
+             "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg",
+             "lts__t_bytes.sum", "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+             "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+             "smsp__average_warps_issue_stalled_membar_per_issue_active.ratio",
+             "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio")
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "usecond": 1, "msecond": 1e3,
+         "nsecond": 1e-3, "ms": 1e3}
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    gi = h.index("Grid Size")
+    agg = collections.OrderedDict()
+    total = 0.0
+    for r in rows[hi + 1:]:
+        us = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1e-3)
+        name = r[ki].split("(")[0]
+        key = f"{name} grid={r[gi]}"
+        a = agg.setdefault(key, {"kernel": name, "grid": r[gi], "launches": 0, "total_us": 0.0})
+        a["launches"] += 1
+        a["total_us"] += us
+        total += us
+    res = []
+    for a in agg.values():
+        a["mean_us"] = round(a["total_us"] / a["launches"], 3)
+        a["share"] = round(a["total_us"] / total, 4)
+        a["total_us"] = round(a["total_us"], 3)
+        res.append(a)
+    res.sort(key=lambda a: -a["total_us"])
+    by_kernel = collections.defaultdict(float)
+    for a in res:
+        by_kernel[a["kernel"].split("<")[0]] += a["total_us"]
+    json.dump({"source": path, "note": "ncu --metrics gpu__time_duration.sum --clock-control none: cold-cache, "
+                                       "serialised per-launch times; compare shares, not absolutes",
+               "total_us": round(total, 3),
+               "share_by_kernel": {k: round(v / total, 4) for k, v in sorted(by_kernel.items(), key=lambda t: -t[1])},
+               "launch_groups": res}, open(out, "w"), indent=1)
+
+
+def full(path, out):
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    h, u = rows[0], rows[1]
+    res = []
+    for v in rows[2:]:
+        d = {"kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else ""}
+        for k in FULL_KEYS:
+            if k in h:
+                i = h.index(k)
+                try:
+                    val = float(v[i].replace(",", ""))
+                except ValueError:
+                    val = v[i]
+                d[k] = val
+                d[k + ".unit"] = u[i]
+        # normalised per-launch DRAM traffic in bytes
+        rb = d.get("dram__bytes_read.sum", 0) * SCALE.get(d.get("dram__bytes_read.sum.unit", "byte"), 1)
+        wb = d.get("dram__bytes_write.sum", 0) * SCALE.get(d.get("dram__bytes_write.sum.unit", "byte"), 1)
+        d["dram_bytes_per_launch"] = rb + wb
+        res.append(d)
+    json.dump({"source": path, "kernels": res}, open(out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
