@@ -185,7 +185,9 @@ tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partitio
  * uint64: [0] entry, [1] prologue done, [2] epilogue start, [3] end (SM
  * clock64 cycles), [4..19] k-block arrival in the MMA thread, [20..35]
  * producer past its empty-slot wait, [36..51] MMA thread after commit (first
- * 16 k-blocks), [62] %smid, [63] %globaltimer at entry (ns).  cap = rows. */
+ * 16 k-blocks), [52] barriers initialised, [53] past griddepcontrol.wait, [54..57] after
+ * each of the first 4 ring-fill loads issued, [58] TMEM allocated (warp 2), [62] %smid,
+ * [63] %globaltimer at entry (ns).  cap = rows. */
 tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part, const void* x,
                           const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
                           uint64_t* trace_host, int32_t cap, int32_t* rows);

@@ -66,6 +66,62 @@ __device__ __forceinline__ void tma_load_tile_4d(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// Warp-uniform issue: the whole warp executes these (uniform control flow, so
+// descriptors/coordinates stay in uniform registers and no per-instruction
+// ELECT loop is generated); only the lane with lead != 0 issues.
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, e;\n\t}"
+      : "=r"(pred));
+  return pred;
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_p(uint64_t* bar, uint32_t bytes, uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(bytes), "r"(lead)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_im2col_4d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c,
+                                                     int32_t w, int32_t h, int32_t n, uint16_t off_w, uint16_t off_h,
+                                                     uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %9, 0;\n\t"
+      "@q cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w),
+      "h"(off_h), "r"(lead)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_tile_4d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                   int32_t c1, int32_t c2, int32_t c3, uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %7, 0;\n\t"
+      "@q cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(lead)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_p(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate, uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(lead)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_p(uint64_t* bar, uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(lead)
+      : "memory");
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -204,17 +260,18 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   // advanced incrementally (no divisions in the loop).
   int p_cb = 0, p_s = 0, p_r = 0, p_stage = 0, p_kb = kb0;
   uint32_t p_phase = 0;
-  auto produce = [&](void) {
+  auto produce = [&](uint32_t lead) {
     uint8_t* sa = a_tiles + (size_t)p_stage * A_STAGE;
     uint8_t* sbp = b_tiles + (size_t)p_stage * B_STAGE;
-    mbar_arrive_expect_tx(full + p_stage, ((a.dbg & 1) ? 0u : A_STAGE) + ((a.dbg & 2) ? 0u : B_STAGE));
+    mbar_arrive_expect_tx_p(full + p_stage, ((a.dbg & 1) ? 0u : A_STAGE) + ((a.dbg & 2) ? 0u : B_STAGE), lead);
     const int c0 = p_cb * BK;
 #pragma unroll
     for (int sb = 0; sb < NSUB; ++sb) {
       if (!(a.dbg & 1))
-        tma_load_im2col_4d(sa + sb * A_SUB, &tmA, full + p_stage, c0 + sb * SUBK, cw, ch, n0, (uint16_t)p_s,
-                           (uint16_t)p_r);
-      if (!(a.dbg & 2)) tma_load_tile_4d(sbp + sb * B_SUB, &tmB, full + p_stage, c0 + sb * SUBK, p_s, p_r, nbase);
+        tma_load_im2col_4d_p(sa + sb * A_SUB, &tmA, full + p_stage, c0 + sb * SUBK, cw, ch, n0, (uint16_t)p_s,
+                             (uint16_t)p_r, lead);
+      if (!(a.dbg & 2))
+        tma_load_tile_4d_p(sbp + sb * B_SUB, &tmB, full + p_stage, c0 + sb * SUBK, p_s, p_r, nbase, lead);
     }
     if (++p_cb == a.cblocks) {
       p_cb = 0;
@@ -224,13 +281,18 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     ++p_kb;
   };
 
-  if (threadIdx.x == 0) {
-    if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // swizzle atoms need 1 KiB alignment
-    for (int i = 0; i < stages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
-    mbar_init(tmem_full, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    prefetch_tmap(&tmA);
-    prefetch_tmap(&tmB);
+  if (warp == 0) {
+    if (lane == 0) {
+      if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // swizzle atoms need 1 KiB alignment
+      for (int i = 0; i < stages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+      mbar_init(tmem_full, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      prefetch_tmap(&tmA);
+      prefetch_tmap(&tmB);
+      if (trace) trace[52] = gtimer();
+    }
+    __syncwarp();
+    const uint32_t lead = elect_one();
     const int rs = kb0 / a.cblocks;
     p_cb = kb0 - rs * a.cblocks;
     p_s = rs % a.S;
@@ -238,30 +300,37 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     // Wait for the previous grid (PDL), then fill the whole ring before the
     // CTA-wide sync so the first loads overlap the TMEM allocation.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (trace && lane == 0) trace[53] = gtimer();
     const int pre = nkb < stages ? nkb : stages;
-    for (int i = 0; i < pre; ++i) produce();
+    for (int i = 0; i < pre; ++i) {
+      produce(lead);
+      if (trace && lane == 0 && i < 4) trace[54 + i] = gtimer();
+    }
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (trace && lane == 0) trace[58] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // provably warp-uniform
   if (trace && threadIdx.x == 0) trace[1] = gtimer();
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer (rest of the k-blocks) ----------------
+  if (warp == 0) {
+    // ---------------- TMA producer (rest of the k-blocks; one elected lane issues) ----------------
+    const uint32_t lead = elect_one();
     while (p_kb < kb1) {
       mbar_wait(empty + p_stage, p_phase ^ 1u);
-      if (trace && p_kb - kb0 < kTraceK) trace[20 + p_kb - kb0] = gtimer();
-      produce();
+      if (trace && lane == 0 && p_kb - kb0 < kTraceK) trace[20 + p_kb - kb0] = gtimer();
+      produce(lead);
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread) ----------------
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one elected lane of warp 1) ----------------
+    const uint32_t lead = elect_one();
     const uint64_t adesc0 = make_sdesc(smem_u32(a_tiles), SWZ);
     const uint64_t bdesc0 = make_sdesc(smem_u32(b_tiles), SWZ);
     int stage = 0;
@@ -269,22 +338,22 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(full + stage, phase);
       tc_fence_after();
-      if (trace && kb - kb0 < kTraceK) trace[4 + kb - kb0] = gtimer();
+      if (trace && lane == 0 && kb - kb0 < kTraceK) trace[4 + kb - kb0] = gtimer();
       const uint64_t ad = adesc0 + soff_a, bd = bdesc0 + soff_b;
 #pragma unroll
       for (int kk = 0; kk < BK / 16; ++kk) {
         constexpr int kPerSub = SUBK / 16;
         const uint32_t sb = kk / kPerSub, koff = (kk % kPerSub) * 32;   // compile-time after unroll
-        tc_mma(tmem_base, ad + ((sb * A_SUB + koff) >> 4), bd + ((sb * B_SUB + koff) >> 4), IDESC,
-               (kb > kb0 || kk > 0) ? 1u : 0u);
+        tc_mma_p(tmem_base, ad + ((sb * A_SUB + koff) >> 4), bd + ((sb * B_SUB + koff) >> 4), IDESC,
+                 (kb > kb0 || kk > 0) ? 1u : 0u, lead);
       }
-      tc_commit(empty + stage);
-      if (trace && kb - kb0 < kTraceK) trace[36 + kb - kb0] = gtimer();
+      tc_commit_p(empty + stage, lead);
+      if (trace && lane == 0 && kb - kb0 < kTraceK) trace[36 + kb - kb0] = gtimer();
       soff_a += A_STAGE >> 4;
       soff_b += B_STAGE >> 4;
       if (++stage == stages) { stage = 0; phase ^= 1u; soff_a = 0; soff_b = 0; }
     }
-    tc_commit(tmem_full);
+    tc_commit_p(tmem_full, lead);
   }
 
   // ---------------- epilogue (all warps) ----------------
