@@ -181,13 +181,16 @@ tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partitio
                         void* ws, size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
 
 /* Tracing (SURVEY 5 "tracing / profiling"): run one IGEMM_TC launch with an
- * in-kernel timeline.  trace_host receives grid_x*grid_y*grid_z rows of 64
+ * in-kernel timeline.  trace_host receives grid_x*grid_y*grid_z rows of 96
  * uint64: [0] entry, [1] prologue done, [2] epilogue start, [3] end (SM
  * clock64 cycles), [4..19] k-block arrival in the MMA thread, [20..35]
  * producer past its empty-slot wait, [36..51] MMA thread after commit (first
  * 16 k-blocks), [52] barriers initialised, [53] past griddepcontrol.wait, [54..57] after
- * each of the first 4 ring-fill loads issued, [58] TMEM allocated (warp 2), [62] %smid,
- * [63] %globaltimer at entry (ns).  cap = rows. */
+ * each of the first 4 ring-fill loads issued, [58] TMEM allocated (warp 2), [60] split-K via
+ * DSMEM cluster (1) or global workspace (0), [61] %cluster_nctarank, [62] %smid,
+ * [63] %globaltimer at entry (ns), [64] split-K slices sent (st.async), [65] past the
+ * cluster barrier, [66] all slices received, [67] reduction stored.
+ * cap = rows. */
 tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part, const void* x,
                           const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
                           uint64_t* trace_host, int32_t cap, int32_t* rows);

@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 
 #include "tp_kernels.h"
@@ -122,6 +123,31 @@ __device__ __forceinline__ void tc_commit_p(uint64_t* bar, uint32_t lead) {
       "r"(lead)
       : "memory");
 }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  return remote;
+}
+// 16-byte store into a peer CTA's shared memory that completes `bytes` on the
+// peer's mbarrier (both addresses in the shared::cluster window).
+__device__ __forceinline__ void st_async_v4(uint32_t dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+               ::"r"(dst), "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
+               : "memory");
+}
+// Store 4 consecutive output channels of row m.
+__device__ __forceinline__ void store4(void* y, int64_t m, int K, int n0, float4 v, int out_f32) {
+  if (out_f32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + m * K + n0) = v;
+  } else {
+    __nv_bfloat162 b0 = __floats2bfloat162_rn(v.x, v.y), b1 = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&b0);
+    u.y = *reinterpret_cast<uint32_t*>(&b1);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(y) + m * K + n0) = u;
+  }
+}
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -198,7 +224,7 @@ __device__ __forceinline__ void store16(void* y, int64_t m, int K, int n0, const
 // done, 2 epilogue start (tmem_full seen), 3 end, 4.. MMA-thread full-barrier
 // completions of the first kTraceK k-blocks; slot 31 = %globaltimer (ns) at
 // entry and slot 30 = %smid, for cross-CTA skew.
-constexpr int kTraceSlots = 64, kTraceK = 16;   // 4..19 MMA full-wait done, 20..35 producer
+constexpr int kTraceSlots = 96, kTraceK = 16;   // 4..19 MMA full-wait done, 20..35 producer
                                                    // after empty-wait, 36..51 MMA after commit
 __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long long)clock64(); }
 
@@ -220,10 +246,12 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   const int stages = a.stages;
   uint8_t* a_tiles = smem_raw;
   uint8_t* b_tiles = a_tiles + (size_t)stages * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(b_tiles + (size_t)stages * B_STAGE);
+  // Barriers live after max(pipeline ring, split-K reduction buffer) (a.bar_off).
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + a.bar_off);
   uint64_t* empty = full + stages;
   uint64_t* tmem_full = empty + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* red_bar = tmem_full + 1;   // split-K DSMEM reduction: all peers' slices landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_bar + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
@@ -238,6 +266,10 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
     trace[63] = g;
     trace[62] = sm;
+    unsigned ncta;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
+    trace[61] = ncta;
+    trace[60] = (unsigned long long)a.cluster_red;
   }
   // Let the next kernel in the stream be scheduled now (programmatic dependent
   // launch); it waits in griddepcontrol.wait before touching memory.
@@ -286,9 +318,13 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // swizzle atoms need 1 KiB alignment
       for (int i = 0; i < stages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
       mbar_init(tmem_full, 1);
+      mbar_init(red_bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       prefetch_tmap(&tmA);
       prefetch_tmap(&tmB);
+      // This CTA owns BM/split_k rows of the tile and receives them from the
+      // split_k - 1 other splits of the cluster.
+      if (a.cluster_red) mbar_arrive_expect_tx(red_bar, (uint32_t)((a.split_k - 1) * (BM / a.split_k) * BN * 4));
       if (trace) trace[52] = gtimer();
     }
     __syncwarp();
@@ -317,6 +353,9 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Publish the initialised reduction barrier to the cluster; the matching
+  // wait sits just before the first remote store, long after every peer arrived.
+  if (a.cluster_red) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // provably warp-uniform
   if (trace && threadIdx.x == 0) trace[1] = gtimer();
 
@@ -386,6 +425,10 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   mbar_wait(tmem_full, 0);
   tc_fence_after();
   if (trace && threadIdx.x == 0) trace[2] = gtimer();
+  if (a.cluster_red) {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (trace && threadIdx.x == 0) trace[65] = gtimer();
+  }
 
   for (int c = c_begin; c < c_end; c += 16) {
     uint32_t raw[16];
@@ -405,6 +448,27 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
         }
         store16(a.y, m, a.K, nb, v, a.out_f32);
       }
+    } else if (a.cluster_red) {
+      // Row segment -> the owner CTA's receive slot [split][row - owner_r0]:
+      // st.async into a peer (completes on the peer's red_bar), a plain
+      // shared store for the rows this CTA owns.  Every row is sent, so the
+      // byte count each owner expects is fixed.
+      if (row_ok) {
+        const int rows_per = BM / a.split_k;
+        const int owner = row / rows_per;
+        float* slot = reinterpret_cast<float*>(smem_raw + a.recv_off) +
+                      (split * rows_per + (row - owner * rows_per)) * (BN + 4) + c;
+        if (owner == split) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<uint4*>(slot + i) = make_uint4(raw[i], raw[i + 1], raw[i + 2], raw[i + 3]);
+        } else {
+          const uint32_t rdst = mapa_u32(smem_u32(slot), (uint32_t)owner);
+          const uint32_t rbar = mapa_u32(smem_u32(red_bar), (uint32_t)owner);
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) st_async_v4(rdst + i * 4, raw[i], raw[i + 1], raw[i + 2], raw[i + 3], rbar);
+        }
+      }
     } else if (row_ok) {
       float* part = a.ws_partial + (((int64_t)split * n_tiles + tile) * BM + row) * BN + c;
 #pragma unroll
@@ -415,7 +479,45 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     }
   }
 
-  if (a.split_k > 1) {
+  if (a.split_k > 1 && a.cluster_red) {
+    // Owner side: the threads whose row this CTA owns wait for the other
+    // splits' slices, sum all split_k slices in split order (deterministic),
+    // add bias, ReLU, store.  Same thread <-> row mapping as the send pass.
+    if (trace && threadIdx.x == 0) trace[64] = gtimer();
+    const int rows_per = BM / a.split_k;
+    const bool owns = row_ok && (row / rows_per) == split;
+    float bv[16];
+    if (owns) load_bias16(nbase + c_begin, bv);
+    mbar_wait(red_bar, 0);
+    if (trace && threadIdx.x == 0) trace[66] = gtimer();
+    if (owns && m < a.M) {
+      const float* recv = reinterpret_cast<const float*>(smem_raw + a.recv_off) + (row - split * rows_per) * (BN + 4);
+      for (int c = c_begin; c < c_end; c += 16) {
+        const int nb = nbase + c;
+        if (c > c_begin) load_bias16(nb, bv);
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        for (int j = 0; j < a.split_k; ++j) {
+          const float* sl = recv + j * rows_per * (BN + 4) + c;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(sl + i);
+            v[i] += t.x; v[i + 1] += t.y; v[i + 2] += t.z; v[i + 3] += t.w;
+          }
+        }
+        if (nb < a.K) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float t = v[i] + bv[i];
+            v[i] = a.relu ? fmaxf(t, 0.0f) : t;
+          }
+          store16(a.y, m, a.K, nb, v, a.out_f32);
+        }
+      }
+    }
+    if (trace && threadIdx.x == 0) trace[67] = gtimer();
+  } else if (a.split_k > 1) {
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -488,6 +590,16 @@ size_t tc_dyn_smem(int bm, int bn, int bk, int stages) {
   return (size_t)stages * (bm + bn) * bk * 2 + 1024;
 }
 
+// Shared-memory layout: [ring] [split-K receive buffer (cluster path)] [barriers, 1 KiB].
+// The receive buffer must not alias the ring: peers push their slices while
+// this CTA may still be in its mainloop.
+static size_t tc_ring_bytes(int bm, int bn, int bk, int stages) { return (size_t)stages * (bm + bn) * bk * 2; }
+static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red) {
+  size_t off = tc_ring_bytes(bm, bn, bk, stages);
+  if (cluster_red) off += (size_t)bm * (bn + 4) * 4;
+  return (off + 1023) & ~(size_t)1023;
+}
+
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   const DriverApi& drv = driver();
   const int sub_k = pb.bk < 64 ? pb.bk : 64;
@@ -538,7 +650,22 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
                     (unsigned)pb.split_k);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
   plan->block = dim3(pb.threads);
-  plan->smem = tc_dyn_smem(pb.bm, pb.bn, pb.bk, pb.stages);
+  // Split-K reduces through DSMEM inside a (1, 1, split_k) cluster when the
+  // context can co-schedule such clusters; otherwise (e.g. a green context
+  // split without SM co-scheduling) through the global workspace.
+  a.cluster_red = 0;
+  plan->cluster_z = 1;
+  if (pb.split_k > 1 && plan->grid.z % (unsigned)pb.split_k == 0 && !getenv("TP_NO_CLUSTER")) {
+    const size_t smem_c = tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, true) + 1024;
+    if (smem_c <= 232448 && ensure_smem_attr(plan->fn, smem_c) == cudaSuccess &&
+        cached_max_clusters(plan->fn, plan->block.x, smem_c, pb.split_k) > 0) {
+      a.cluster_red = 1;
+      plan->cluster_z = pb.split_k;
+    }
+  }
+  a.bar_off = (int)tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, a.cluster_red != 0);
+  a.recv_off = (int)tc_ring_bytes(pb.bm, pb.bn, pb.bk, pb.stages);
+  plan->smem = (size_t)a.bar_off + 1024;
   cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
   if (e != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -554,11 +681,22 @@ cudaError_t tc_launch(const TcPlan& plan, cudaStream_t stream) {
   cfg.blockDim = plan.block;
   cfg.dynamicSmemBytes = plan.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (plan.cluster_z > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = (unsigned)plan.cluster_z;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, fn, plan.tmA, plan.tmB, plan.args);
 }
 

@@ -145,6 +145,36 @@ int cached_occupancy(const void* fn, int block, size_t smem) {
   return n;
 }
 
+static std::map<std::tuple<const void*, int, size_t, int, CUcontext>, int> g_clu;
+
+int cached_max_clusters(const void* fn, int block, size_t smem, int cz) {
+  const auto key = std::make_tuple(fn, block, smem, cz, current_ctx());
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_clu.find(key);
+    if (it != g_clu.end()) return it->second;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1, 1, (unsigned)cz);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = (unsigned)cz;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_clu[key] = n;
+  return n;
+}
+
 // ---------------------------------------------------------------- device state
 struct DeviceState {
   bool init = false;
@@ -1100,8 +1130,8 @@ tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partit
   const int64_t ctas = (int64_t)plan.tc.grid.x * plan.tc.grid.y * plan.tc.grid.z;
   if (ctas > cap) { set_error("trace capacity too small"); return TP_EINVAL; }
   unsigned long long* dtr = nullptr;
-  TP_CK(cudaMalloc(&dtr, ctas * 64 * sizeof(unsigned long long)));
-  TP_CK(cudaMemset(dtr, 0, ctas * 64 * sizeof(unsigned long long)));
+  TP_CK(cudaMalloc(&dtr, ctas * 96 * sizeof(unsigned long long)));
+  TP_CK(cudaMemset(dtr, 0, ctas * 96 * sizeof(unsigned long long)));
   plan.tc.args.trace = dtr;
   cudaError_t e;
   {
@@ -1109,7 +1139,7 @@ tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partit
     e = launch_plan(plan, p->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
   }
-  if (e == cudaSuccess) e = cudaMemcpy(trace_host, dtr, ctas * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(trace_host, dtr, ctas * 96 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   cudaFree(dtr);
   TP_CK(e);
   *rows = (int32_t)ctas;

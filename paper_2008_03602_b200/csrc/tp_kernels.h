@@ -46,6 +46,8 @@ bool pdl_enabled();
 // the tuner): the max-dynamic-smem attribute and the occupancy calculator.
 cudaError_t ensure_smem_attr(const void* fn, size_t smem);
 int cached_occupancy(const void* fn, int block, size_t smem);
+// cudaOccupancyMaxActiveClusters for a (1, 1, cz) cluster in the current context (0 = cannot launch).
+int cached_max_clusters(const void* fn, int block, size_t smem, int cz);
 
 // ---------------------------------------------------------------- igemm_tc
 struct TcArgs {
@@ -58,6 +60,9 @@ struct TcArgs {
   float* ws_partial;
   int* ws_counters;
   unsigned long long* trace;   // optional per-CTA timeline (tp_conv2d_trace), nullptr = off
+  int cluster_red;             // 1: split-K reduced through DSMEM in a (1,1,split_k) cluster
+  int bar_off;                 // byte offset of the mbarriers in dynamic shared memory
+  int recv_off;                // byte offset of the split-K receive buffer (cluster path)
   int dbg;                     // TP_DEBUG_TC env (experiments only): bit0 skip A TMA, bit1 skip B TMA
 };
 
@@ -82,6 +87,7 @@ struct TcPlan {
   const void* fn = nullptr;
   dim3 grid, block;
   size_t smem = 0;
+  int cluster_z = 1;
 };
 
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan);

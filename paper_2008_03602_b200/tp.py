@@ -364,10 +364,10 @@ def conv2d_run(buf: LayerBuffers, sched: dict, part: Partition | None = None, ti
 
 
 def conv2d_trace(buf: "LayerBuffers", sched: dict, part: Partition | None = None) -> np.ndarray:
-    """In-kernel timeline of one IGEMM_TC launch: (ctas, 64) uint64 (see tp.h)."""
+    """In-kernel timeline of one IGEMM_TC launch: (ctas, 96) uint64 (see tp.h)."""
     x, w, b, y, ws, wsb = buf.ptrs()
     cap = int(sched.get("grid_x", 0) * sched.get("grid_y", 0) * sched.get("grid_z", 0)) or 65536
-    out = np.zeros((cap, 64), dtype=np.uint64)
+    out = np.zeros((cap, 96), dtype=np.uint64)
     rows = _i32()
     _ck(_lib.tp_conv2d_trace(ctypes.byref(buf.cd), ctypes.byref(dict_to_sched(sched)), _h(part), x, w, b, y, ws,
                              wsb, out.ctypes.data_as(_P(_u64)), cap, ctypes.byref(rows)), "tp_conv2d_trace")
