@@ -368,7 +368,7 @@ def main():
         f, by = layer_work(d, P, Q)
         lat_sum += d["mult"] * b["median_us"]
         kind = tp.space_get(d, b["space_index"])["kind"]
-        if kind == tp.KIND_IGEMM_TC:
+        if kind != tp.KIND_DIRECT:
             flops_tc += f
             bytes_tc += by
             t_tc += b["median_us"]

@@ -58,7 +58,12 @@ typedef enum {
 enum { TP_LAYOUT_NHWC = 0, TP_LAYOUT_NCHW = 1 };
 enum { TP_DTYPE_BF16 = 0, TP_DTYPE_FP32 = 1 };
 enum { TP_EPI_BIAS = 1, TP_EPI_RELU = 2 };
-enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1 };
+/* Kernel kinds: IGEMM_TC = tcgen05 implicit GEMM fed by
+ * TMA im2col (bf16, g = 1, C % 8 == 0); DIRECT = CUDA-core FFMA direct conv
+ * (fp32, depthwise); IGEMM_TC_GATHER = tcgen05 implicit GEMM whose A/B tiles
+ * are gathered into shared memory by CUDA-core warps over the flattened
+ * (r, s, c) axis (bf16, g = 1, C % 8 != 0: the C = 3 stems). */
+enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2 };
 
 /* One conv2d operator ("tuning task", P:947 [src]).  P/Q follow reading C3:
  * P = floor((h + 2 pad_h - dil_h (r-1) - 1) / stride_h) + 1; P < 1 -> TP_EINVAL. */

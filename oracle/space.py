@@ -21,6 +21,7 @@ import math
 
 KIND_IGEMM_TC = 0
 KIND_DIRECT = 1
+KIND_IGEMM_TC_GATHER = 2
 DTYPE_BF16 = 0
 DTYPE_FP32 = 1
 SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
@@ -49,12 +50,14 @@ def out_pq(d: dict) -> tuple[int, int]:
 
 
 def layer_kind(d: dict) -> int:
-    """One kind per layer: tensor cores for bf16 dense layers whose
-    channel counts meet the TMA/vector alignment, CUDA cores otherwise."""
-    if (d["dtype"] == DTYPE_BF16 and d.get("groups", 1) == 1 and d["c"] % 8 == 0
-            and d["k"] % 8 == 0 and d.get("dil_h", 1) == 1 and d.get("dil_w", 1) == 1):
-        return KIND_IGEMM_TC
-    return KIND_DIRECT
+    """One kind per layer: bf16 dense (g = 1, d = 1,
+    K % 8 == 0) layers go to the tensor cores -- TMA im2col when C % 8 == 0,
+    the gathered variant otherwise; everything else to the CUDA cores."""
+    dense_bf16 = (d["dtype"] == DTYPE_BF16 and d.get("groups", 1) == 1 and d["k"] % 8 == 0
+                  and d.get("dil_h", 1) == 1 and d.get("dil_w", 1) == 1)
+    if not dense_bf16:
+        return KIND_DIRECT
+    return KIND_IGEMM_TC if d["c"] % 8 == 0 else KIND_IGEMM_TC_GATHER
 
 
 def direct_lanes(d: dict, threads: int, tile_q: int, vec_k: int, tile_p: int) -> tuple[int, int]:
@@ -87,6 +90,21 @@ def _valid_tc(d: dict, bm, bn, bk, stages, threads, split_k) -> bool:
     return split_k <= d["r"] * d["s"] * _cdiv(d["c"], bk)
 
 
+def _valid_tc_gather(d: dict, bm, bn, bk, stages, threads, split_k) -> bool:
+    """Gathered tensor-core kind: reduction axis = R*S*C flattened; shared
+    memory also holds a 16-B-per-row pixel table and an 8-B-per-k table over
+    the k-blocks' padded extent."""
+    P, Q = out_pq(d)
+    M = d["n"] * P * Q
+    kg = d["r"] * d["s"] * d["c"]
+    nkb = _cdiv(kg, bk)
+    if stages * (bm + bn) * bk * 2 + 1024 + 16 * bm + 8 * nkb * bk > SMEM_LIMIT:
+        return False
+    if bn > max(32, _np2(d["k"])) or bm > max(64, _np2(M)) or bk > max(16, _np2(kg)):
+        return False
+    return split_k <= nkb
+
+
 def _valid_direct(d: dict, threads, tile_q, vec_k, tile_p, smem_stage) -> bool:
     P, Q = out_pq(d)
     if tile_q > Q or tile_p > P or vec_k > d["k"]:
@@ -102,7 +120,8 @@ def enumerate_space(d: dict) -> list[dict]:
     """Valid schedules in lexicographic knob order (outermost knob first);
     ``space_index`` is the rank among the valid tuples."""
     kind = layer_kind(d)
-    knobs, valid = (TC_KNOBS, _valid_tc) if kind == KIND_IGEMM_TC else (DIRECT_KNOBS, _valid_direct)
+    knobs, valid = {KIND_IGEMM_TC: (TC_KNOBS, _valid_tc), KIND_IGEMM_TC_GATHER: (TC_KNOBS, _valid_tc_gather),
+                    KIND_DIRECT: (DIRECT_KNOBS, _valid_direct)}[kind]
     names = [k for k, _ in knobs]
     out = []
     for combo in itertools.product(*[v for _, v in knobs]):
@@ -118,7 +137,7 @@ def enumerate_space(d: dict) -> list[dict]:
 def geometry(d: dict, s: dict) -> dict:
     """Frozen launch geometry of a schedule (grid, threads per CTA)."""
     P, Q = out_pq(d)
-    if s.get("kind", layer_kind(d)) == KIND_IGEMM_TC:
+    if s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER):
         M = d["n"] * P * Q
         g = (_cdiv(M, s["bm"]), _cdiv(d["k"], s["bn"]), s["split_k"])
     else:

@@ -24,6 +24,8 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <climits>
 
 #include "tp_kernels.h"
 
@@ -35,6 +37,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -228,7 +233,13 @@ constexpr int kTraceSlots = 96, kTraceK = 16;   // 4..19 MMA full-wait done, 20.
                                                    // after empty-wait, 36..51 MMA after commit
 __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long long)clock64(); }
 
-template <int BM, int BN, int BK>
+// GATHER = false: A by TMA im2col per filter tap, B by TMA tiled (C % 8 == 0).
+// GATHER = true : the reduction axis is (r, s, c) flattened (c fastest) and
+//   every warp but the MMA warp gathers the A (im2col) and B (weight) tiles
+//   element by element into the same swizzled K-major shared-memory layout the
+//   TMA would produce (the C = 3 stems, where a pixel row is 6 bytes and
+//   neither TMA mode applies).
+template <int BM, int BN, int BK, bool GATHER>
 __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB, TcArgs a) {
   // Compile-time tile geometry: one swizzle row holds SUBK channels (32/64/128 B).
@@ -275,16 +286,16 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   // launch); it waits in griddepcontrol.wait before touching memory.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  const int kb0 = (int)(((int64_t)split * a.kblocks) / a.split_k);
-  const int kb1 = (int)(((int64_t)(split + 1) * a.kblocks) / a.split_k);
+  const int kb0 = (split * a.kblocks) / a.split_k;   // 32-bit: M, k-blocks < 2^31 (checked on the host)
+  const int kb1 = ((split + 1) * a.kblocks) / a.split_k;
   const int nkb = kb1 - kb0;
 
   // Output-pixel origin of this M tile -> im2col base coordinate (lower corner = -pad).
-  const int64_t m0 = (int64_t)m_tile * BM;
-  const int q0 = (int)(m0 % a.Q);
-  const int64_t t0 = m0 / a.Q;
-  const int p0 = (int)(t0 % a.P);
-  const int n0 = (int)(t0 / a.P);
+  const int m0 = m_tile * BM;
+  const int q0 = m0 % a.Q;
+  const int t0 = m0 / a.Q;
+  const int p0 = t0 % a.P;
+  const int n0 = t0 / a.P;
   const int cw = q0 * a.sw - a.pw, ch = p0 * a.sh - a.ph;
   const int nbase = n_tile * BN;
 
@@ -316,31 +327,63 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   if (warp == 0) {
     if (lane == 0) {
       if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // swizzle atoms need 1 KiB alignment
-      for (int i = 0; i < stages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+      // GATHER: every producer warp arrives once per stage.
+      const uint32_t full_count = GATHER ? (blockDim.x >> 5) - 1 : 1;
+      for (int i = 0; i < stages; ++i) { mbar_init(full + i, full_count); mbar_init(empty + i, 1); }
       mbar_init(tmem_full, 1);
       mbar_init(red_bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      prefetch_tmap(&tmA);
-      prefetch_tmap(&tmB);
+      if constexpr (!GATHER) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+      }
       // This CTA owns BM/split_k rows of the tile and receives them from the
       // split_k - 1 other splits of the cluster.
       if (a.cluster_red) mbar_arrive_expect_tx(red_bar, (uint32_t)((a.split_k - 1) * (BM / a.split_k) * BN * 4));
       if (trace) trace[52] = gtimer();
     }
     __syncwarp();
-    const uint32_t lead = elect_one();
-    const int rs = kb0 / a.cblocks;
-    p_cb = kb0 - rs * a.cblocks;
-    p_s = rs % a.S;
-    p_r = rs / a.S;
-    // Wait for the previous grid (PDL), then fill the whole ring before the
-    // CTA-wide sync so the first loads overlap the TMEM allocation.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (trace && lane == 0) trace[53] = gtimer();
-    const int pre = nkb < stages ? nkb : stages;
-    for (int i = 0; i < pre; ++i) {
-      produce(lead);
-      if (trace && lane == 0 && i < 4) trace[54 + i] = gtimer();
+    if constexpr (!GATHER) {
+      const uint32_t lead = elect_one();
+      const int rs = kb0 / a.cblocks;
+      p_cb = kb0 - rs * a.cblocks;
+      p_s = rs % a.S;
+      p_r = rs / a.S;
+      // Wait for the previous grid (PDL), then fill the whole ring before the
+      // CTA-wide sync so the first loads overlap the TMEM allocation.
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      if (trace && lane == 0) trace[53] = gtimer();
+      const int pre = nkb < stages ? nkb : stages;
+      for (int i = 0; i < pre; ++i) {
+        produce(lead);
+        if (trace && lane == 0 && i < 4) trace[54 + i] = gtimer();
+      }
+    }
+  }
+  if constexpr (GATHER) {
+    // Pixel table (rowbase, h0, w0) for the BM rows of this tile and k table
+    // (offset of (r, s, c) relative to the row base, (r << 16) | s) over the
+    // padded reduction extent; built once per CTA.  Rows past M and k past
+    // R*S*C get coordinates that fail every bounds check (zero fill).
+    int4* rowtab = reinterpret_cast<int4*>(smem_raw + a.tab_off);
+    int2* ktab = reinterpret_cast<int2*>(smem_raw + a.tab_off + BM * 16);
+    for (int r = threadIdx.x; r < BM; r += blockDim.x) {
+      const int m = (int)m0 + r;
+      int4 e = make_int4(0, -(1 << 20), -(1 << 20), 0);
+      if (m < (int)a.M) {
+        const int q = m % a.Q, t = m / a.Q, pp = t % a.P, n = t / a.P;
+        const int h0 = pp * a.sh - a.ph, w0 = q * a.sw - a.pw;
+        e = make_int4(((n * a.H + h0) * a.W + w0) * a.C, h0, w0, 0);
+      }
+      rowtab[r] = e;
+    }
+    for (int k = threadIdx.x; k < a.kblocks * BK; k += blockDim.x) {
+      int2 e = make_int2(0, 0x7FFF7FFF);
+      if (k < a.Kg) {
+        const int c = k % a.C, rs = k / a.C, ss = rs % a.S, rr = rs / a.S;
+        e = make_int2((rr * a.W + ss) * a.C + c, (rr << 16) | ss);
+      }
+      ktab[k] = e;
     }
   }
   if (warp == 2) {
@@ -359,7 +402,67 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // provably warp-uniform
   if (trace && threadIdx.x == 0) trace[1] = gtimer();
 
-  if (warp == 0) {
+  if (GATHER && warp != 1) {
+    // ---------------- gather producers (all warps but the MMA warp) ----------------
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int pt = warp == 0 ? lane : (int)threadIdx.x - 32;
+    const int np = (int)blockDim.x - 32;
+    const int4* rowtab = reinterpret_cast<const int4*>(smem_raw + a.tab_off);
+    const int2* ktab = reinterpret_cast<const int2*>(smem_raw + a.tab_off + BM * 16);
+    const uint16_t* xg = reinterpret_cast<const uint16_t*>(a.xg);
+    const uint16_t* wg = reinterpret_cast<const uint16_t*>(a.wg);
+    constexpr int CPR = BK / 8;                 // 16-byte chunks per tile row
+    constexpr uint32_t SWM = SWZ / 16 - 1;      // swizzle: chunk ^= (offset >> 7) & SWM
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(empty + stage, phase ^ 1u);
+      uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
+      uint8_t* sbt = b_tiles + (size_t)stage * B_STAGE;
+      const int kbase = kb * BK;
+      for (int id = pt; id < (BM + BN) * CPR; id += np) {
+        const bool is_a = id < BM * CPR;
+        const int rid = is_a ? id : id - BM * CPR;
+        const int row = rid / CPR, kc = rid % CPR;
+        const int k0 = kbase + kc * 8;
+        uint32_t v[4];
+        if (is_a) {
+          const int4 rt = rowtab[row];
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            uint32_t lo = 0, hi = 0;
+            const int2 e0 = ktab[k0 + j], e1 = ktab[k0 + j + 1];
+            if ((unsigned)(rt.y + (e0.y >> 16)) < (unsigned)a.H && (unsigned)(rt.z + (e0.y & 0xFFFF)) < (unsigned)a.W)
+              lo = __ldg(xg + rt.x + e0.x);
+            if ((unsigned)(rt.y + (e1.y >> 16)) < (unsigned)a.H && (unsigned)(rt.z + (e1.y & 0xFFFF)) < (unsigned)a.W)
+              hi = __ldg(xg + rt.x + e1.x);
+            v[j / 2] = lo | (hi << 16);
+          }
+        } else {
+          const int kn = nbase + row;
+          const uint16_t* wr = wg + (int64_t)kn * a.Kg;
+#pragma unroll
+          for (int j = 0; j < 8; j += 2) {
+            uint32_t lo = 0, hi = 0;
+            if (kn < a.K && k0 + j < a.Kg) lo = __ldg(wr + k0 + j);
+            if (kn < a.K && k0 + j + 1 < a.Kg) hi = __ldg(wr + k0 + j + 1);
+            v[j / 2] = lo | (hi << 16);
+          }
+        }
+        const int sub = (kc * 8) / SUBK, ch = ((kc * 8) % SUBK) / 8;
+        uint32_t off = (uint32_t)row * SWZ + (uint32_t)ch * 16;
+        off ^= ((off >> 7) & SWM) << 4;
+        uint8_t* dst = (is_a ? sa + sub * A_SUB : sbt + sub * B_SUB) + off;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+      }
+      // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full + stage);
+      if (trace && threadIdx.x == 0 && kb - kb0 < kTraceK) trace[20 + kb - kb0] = gtimer();
+      if (++stage == stages) { stage = 0; phase ^= 1u; }
+    }
+  } else if (!GATHER && warp == 0) {
     // ---------------- TMA producer (rest of the k-blocks; one elected lane issues) ----------------
     const uint32_t lead = elect_one();
     while (p_kb < kb1) {
@@ -566,20 +669,20 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 // ------------------------------------------------------------- host side
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
 
-template <int BM, int BN>
+template <int BM, int BN, bool G>
 static KernelFn pick_bk(int bk) {
   switch (bk) {
-    case 16: return igemm_tc_kernel<BM, BN, 16>;
-    case 32: return igemm_tc_kernel<BM, BN, 32>;
-    case 64: return igemm_tc_kernel<BM, BN, 64>;
-    case 128: return igemm_tc_kernel<BM, BN, 128>;
+    case 16: return igemm_tc_kernel<BM, BN, 16, G>;
+    case 32: return igemm_tc_kernel<BM, BN, 32, G>;
+    case 64: return igemm_tc_kernel<BM, BN, 64, G>;
+    case 128: return igemm_tc_kernel<BM, BN, 128, G>;
   }
   return nullptr;
 }
 
-static KernelFn pick_tc(int bm, int bn, int bk) {
+static KernelFn pick_tc(int bm, int bn, int bk, bool gather) {
 #define TP_TC_CASE(M_, N_) \
-  if (bm == M_ && bn == N_) return pick_bk<M_, N_>(bk);
+  if (bm == M_ && bn == N_) return gather ? pick_bk<M_, N_, true>(bk) : pick_bk<M_, N_, false>(bk);
   TP_TC_CASE(64, 32) TP_TC_CASE(64, 64) TP_TC_CASE(64, 128) TP_TC_CASE(64, 256)
   TP_TC_CASE(128, 32) TP_TC_CASE(128, 64) TP_TC_CASE(128, 128) TP_TC_CASE(128, 256)
 #undef TP_TC_CASE
@@ -603,6 +706,15 @@ static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red) {
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   const DriverApi& drv = driver();
   const int sub_k = pb.bk < 64 ? pb.bk : 64;
+  if (pb.M > INT32_MAX / 2 || (int64_t)pb.N * pb.H * pb.W * pb.C > INT32_MAX) {
+    set_error("tensor too large for 32-bit tile indexing");
+    return TP_EUNSUPPORTED;
+  }
+  if (pb.gather) {
+    // Gathered kind: no tensor maps (the kernel never touches tmA / tmB).
+    std::memset(&plan->tmA, 0, sizeof(plan->tmA));
+    std::memset(&plan->tmB, 0, sizeof(plan->tmB));
+  } else {
   const CUtensorMapSwizzle swz = sub_k == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
                                              : (sub_k == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
   // A: im2col over NHWC x, dims (C, W, H, N).
@@ -631,12 +743,16 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return TP_ECUDA;
   }
+  }
   TcArgs& a = plan->args;
   a.M = pb.M; a.K = pb.K; a.P = pb.P; a.Q = pb.Q; a.S = pb.S;
   a.sh = pb.sh; a.sw = pb.sw; a.ph = pb.ph; a.pw = pb.pw;
   a.bk = pb.bk; a.stages = pb.stages; a.split_k = pb.split_k;
   a.cblocks = (pb.C + pb.bk - 1) / pb.bk;
   a.kblocks = pb.R * pb.S * a.cblocks;
+  a.xg = pb.x; a.wg = pb.w;
+  a.H = pb.H; a.W = pb.W; a.C = pb.C; a.Kg = pb.R * pb.S * pb.C;
+  if (pb.gather) a.kblocks = (a.Kg + pb.bk - 1) / pb.bk;
   a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
   a.ws_partial = pb.ws_partial; a.ws_counters = pb.ws_counters;
   a.trace = pb.trace;
@@ -644,7 +760,7 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     static const int dbg = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
     a.dbg = dbg;
   }
-  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk));
+  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.gather != 0));
   if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN x BK"); return TP_EINVALID_CONFIG; }
   plan->grid = dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn),
                     (unsigned)pb.split_k);
@@ -656,7 +772,8 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.cluster_red = 0;
   plan->cluster_z = 1;
   if (pb.split_k > 1 && plan->grid.z % (unsigned)pb.split_k == 0 && !getenv("TP_NO_CLUSTER")) {
-    const size_t smem_c = tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, true) + 1024;
+    const size_t tabs = pb.gather ? (size_t)pb.bm * 16 + (size_t)a.kblocks * pb.bk * 8 : 0;
+    const size_t smem_c = tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, true) + 1024 + tabs;
     if (smem_c <= 232448 && ensure_smem_attr(plan->fn, smem_c) == cudaSuccess &&
         cached_max_clusters(plan->fn, plan->block.x, smem_c, pb.split_k) > 0) {
       a.cluster_red = 1;
@@ -665,7 +782,8 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   }
   a.bar_off = (int)tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, a.cluster_red != 0);
   a.recv_off = (int)tc_ring_bytes(pb.bm, pb.bn, pb.bk, pb.stages);
-  plan->smem = (size_t)a.bar_off + 1024;
+  a.tab_off = a.bar_off + 1024;
+  plan->smem = (size_t)a.tab_off + (pb.gather ? (size_t)pb.bm * 16 + (size_t)a.kblocks * pb.bk * 8 : 0);
   cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
   if (e != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));

@@ -302,7 +302,7 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 static WsLayout ws_layout(const Layer& L, const tp_schedule& s) {
   WsLayout w;
   size_t off = 0;
-  if (s.kind == TP_KIND_IGEMM_TC && s.split_k > 1) {
+  if ((s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) && s.split_k > 1) {
     // The counter region depends on the layer only (sized for the smallest tile,
     // 64 x 32), so partials of one schedule never land on another schedule's
     // counters: every counter stays zero between completed launches.
@@ -351,7 +351,7 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     yk = plan->y_nhwc;
     plan->kernels_per_call = 3;
   }
-  if (s.kind == TP_KIND_IGEMM_TC) {
+  if (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) {
     if ((reinterpret_cast<uintptr_t>(xk) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(yk)) & 15) {
       set_error("x, w, y must be 16-byte aligned for the tensor-core path");
       return TP_EINVAL;
@@ -369,6 +369,7 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     pb.has_bias = (L.d.epilogue & TP_EPI_BIAS) ? 1 : 0;
     pb.ws_counters = s.split_k > 1 ? reinterpret_cast<int*>(wsb + wl.counters) : nullptr;
     pb.ws_partial = s.split_k > 1 ? reinterpret_cast<float*>(wsb + wl.partials) : nullptr;
+    pb.gather = s.kind == TP_KIND_IGEMM_TC_GATHER ? 1 : 0;
     tp_status st = tc_prepare(pb, &plan->tc);
     if (st != TP_OK) return st;
     plan->ctas_per_sm = tc_occupancy(plan->tc);
@@ -386,7 +387,7 @@ static cudaError_t launch_plan(const ConvPlan& p, cudaStream_t st) {
     e = launch_nchw_to_nhwc(p.x_user, p.x_nhwc, p.L.d.n, p.L.d.c, p.L.d.h, p.L.d.w, p.in_eb, st);
     if (e != cudaSuccess) return e;
   }
-  e = p.s.kind == TP_KIND_IGEMM_TC ? tc_launch(p.tc, st) : direct_launch(p.dp, st);
+  e = p.s.kind != TP_KIND_DIRECT ? tc_launch(p.tc, st) : direct_launch(p.dp, st);
   if (e != cudaSuccess) return e;
   if (p.nchw) {
     e = launch_nhwc_to_nchw(p.y_nhwc, p.y_user, p.L.d.n, p.L.d.k, p.L.P, p.L.Q, p.out_eb, st);
@@ -397,7 +398,7 @@ static cudaError_t launch_plan(const ConvPlan& p, cudaStream_t st) {
 }
 
 static void plan_geometry(const ConvPlan& p, int sm_granted, tp_measurement* m) {
-  const dim3 g = p.s.kind == TP_KIND_IGEMM_TC ? p.tc.grid : p.dp.grid;
+  const dim3 g = p.s.kind != TP_KIND_DIRECT ? p.tc.grid : p.dp.grid;
   m->ctas = (int64_t)g.x * g.y * g.z;
   m->threads_per_cta = p.s.threads;
   m->ctas_per_sm = p.ctas_per_sm;
@@ -1115,7 +1116,7 @@ tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partit
   tp_status st = make_layer(d, &L);
   if (st != TP_OK) return st;
   if (!s || !trace_host || !rows) { set_error("null argument"); return TP_EINVAL; }
-  if (s->kind != TP_KIND_IGEMM_TC) { set_error("tracing is implemented for IGEMM_TC"); return TP_EUNSUPPORTED; }
+  if (s->kind == TP_KIND_DIRECT) { set_error("tracing is implemented for the tensor-core kinds"); return TP_EUNSUPPORTED; }
   tp_partition* p;
   st = get_part(part, &p);
   if (st != TP_OK) return st;

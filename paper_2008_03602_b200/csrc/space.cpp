@@ -27,9 +27,8 @@ static int32_t out_dim(int32_t in, int32_t k, int32_t st, int32_t pad, int32_t d
 }
 
 int32_t layer_kind(const tp_conv_desc& d) {
-  if (d.dtype == TP_DTYPE_BF16 && d.groups == 1 && d.c % 8 == 0 && d.k % 8 == 0 &&
-      d.dil_h == 1 && d.dil_w == 1)
-    return TP_KIND_IGEMM_TC;
+  if (d.dtype == TP_DTYPE_BF16 && d.groups == 1 && d.k % 8 == 0 && d.dil_h == 1 && d.dil_w == 1)
+    return d.c % 8 == 0 ? TP_KIND_IGEMM_TC : TP_KIND_IGEMM_TC_GATHER;
   return TP_KIND_DIRECT;
 }
 
@@ -103,10 +102,25 @@ int64_t direct_smem_bytes(const Layer& L, int threads, int tile_q, int vec_k, in
   return 4 * (rows_in * cols_in * kt + (int64_t)L.d.r * L.d.s * kt);
 }
 
+// Gather kind: the reduction axis is R*S*C flattened (c fastest), cut into
+// BK-wide k-blocks; the CTA also holds a pixel table (16 B per row) and a
+// k table (8 B per padded k).
+int64_t tcg_table_bytes(const Layer& L, int bm, int bk) {
+  const int64_t kg = (int64_t)L.d.r * L.d.s * L.d.c;
+  return (int64_t)bm * 16 + cdiv(kg, bk) * bk * 8;
+}
+
 static bool valid_tc(const Layer& L, int bm, int bn, int bk, int stages, int /*threads*/, int split) {
-  if (tc_smem_bytes(bm, bn, bk, stages) > kSmemLimit) return false;
+  const bool gather = L.kind == TP_KIND_IGEMM_TC_GATHER;
+  const int64_t extra = gather ? tcg_table_bytes(L, bm, bk) : 0;
+  if (tc_smem_bytes(bm, bn, bk, stages) + extra > kSmemLimit) return false;
   if (bn > std::max<int64_t>(32, np2(L.d.k))) return false;
   if (bm > std::max<int64_t>(64, np2(L.M))) return false;
+  if (gather) {
+    const int64_t kg = (int64_t)L.d.r * L.d.s * L.d.c;
+    if (bk > std::max<int64_t>(16, np2(kg))) return false;
+    return split <= cdiv(kg, bk);
+  }
   if (bk > std::max<int64_t>(16, np2(L.d.c))) return false;
   return split <= (int64_t)L.d.r * L.d.s * cdiv(L.d.c, bk);
 }
@@ -119,7 +133,7 @@ static bool valid_direct(const Layer& L, int threads, int tq, int vk, int tpp, i
 }
 
 void fill_geometry(const Layer& L, tp_schedule* s) {
-  if (s->kind == TP_KIND_IGEMM_TC) {
+  if (s->kind == TP_KIND_IGEMM_TC || s->kind == TP_KIND_IGEMM_TC_GATHER) {
     s->grid_x = (int32_t)cdiv(L.M, s->bm);
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = s->split_k;
@@ -136,12 +150,12 @@ void fill_geometry(const Layer& L, tp_schedule* s) {
 template <class F>
 static void enumerate(const Layer& L, F visit) {
   int64_t idx = 0;
-  if (L.kind == TP_KIND_IGEMM_TC) {
+  if (L.kind == TP_KIND_IGEMM_TC || L.kind == TP_KIND_IGEMM_TC_GATHER) {
     for (int bm : kTcBM) for (int bn : kTcBN) for (int bk : kTcBK) for (int st : kTcStages)
       for (int th : kTcThreads) for (int sk : kTcSplit) {
         if (!valid_tc(L, bm, bn, bk, st, th, sk)) continue;
         tp_schedule s; std::memset(&s, 0, sizeof(s));
-        s.kind = TP_KIND_IGEMM_TC; s.bm = bm; s.bn = bn; s.bk = bk; s.stages = st;
+        s.kind = L.kind; s.bm = bm; s.bn = bn; s.bk = bk; s.stages = st;
         s.threads = th; s.split_k = sk; s.space_index = idx++;
         if (!visit(s)) return;
       }
@@ -175,7 +189,7 @@ bool space_get(const Layer& L, int64_t idx, tp_schedule* out) {
 
 bool schedule_in_space(const Layer& L, const tp_schedule& s) {
   if (s.kind != L.kind) return false;
-  if (s.kind == TP_KIND_IGEMM_TC) {
+  if (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) {
     auto in = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };
     return in(s.bm, kTcBM, 2) && in(s.bn, kTcBN, 4) && in(s.bk, kTcBK, 4) && in(s.stages, kTcStages, 4) &&
            in(s.threads, kTcThreads, 2) && in(s.split_k, kTcSplit, 4) &&

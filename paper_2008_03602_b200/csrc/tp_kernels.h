@@ -60,6 +60,10 @@ struct TcArgs {
   float* ws_partial;
   int* ws_counters;
   unsigned long long* trace;   // optional per-CTA timeline (tp_conv2d_trace), nullptr = off
+  const void* xg;              // gathered kind: NHWC x and dense [K][R*S*C] weights
+  const void* wg;
+  int H, W, C, Kg;             // gathered kind: input extent, channels, reduction length R*S*C
+  int tab_off;                 // gathered kind: byte offset of the pixel / k tables
   int cluster_red;             // 1: split-K reduced through DSMEM in a (1,1,split_k) cluster
   int bar_off;                 // byte offset of the mbarriers in dynamic shared memory
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
@@ -79,6 +83,7 @@ struct TcProblem {
   float* ws_partial;
   int* ws_counters;
   unsigned long long* trace;
+  int gather;      // 1: TP_KIND_IGEMM_TC_GATHER (C % 8 != 0)
 };
 
 struct TcPlan {

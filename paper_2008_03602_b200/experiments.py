@@ -1,0 +1,260 @@
+"""The paper's experiments on the hot path, driven through the C-ABI (tp.py).
+
+* ``tune_layers``      -- tune every layer of a catalog inside one partition
+                          (a3-a12; "tune a DNN model at a GPU%").
+* ``cross_eval``       -- tuned-at-p x run-at-q latency matrix per layer and
+                          for the model (a13; T1-T3; frozen schedule
+                          geometry, reading C15).
+* ``concurrent_tune``  -- k tuners on k disjoint green-context partitions,
+                          one host thread each (a14; "multiple TCIs/TSIs on
+                          one GPU with distinct GPU%"),
+                          with solo vs co-running latency of the winners
+                          (isolation, reading C22).
+* ``roofline``         -- the three fractions of SURVEY 8(d) for one layer at
+                          its SM share: tensor, ALU (FP32 FFMA) and HBM
+                          (against the copy bandwidth measured inside the same
+                          partition), plus the measured launch floor.
+
+Everything here is orchestration: every step of the path runs in libtp's
+kernels.  Correctness gating uses libtp's consensus gate (the first OK
+candidate's values at 4096 fixed points); oracle parity of the winners is
+checked by tests/ and bench.py.
+"""
+from __future__ import annotations
+
+import json
+import os
+import threading
+import time
+
+from . import datagen, tp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SM_COUNT = 148
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}
+
+
+def peaks() -> dict:
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written) else the
+    B200_PROFILING.md fallback; FP32 FFMA peak = SMs x 128 lanes x 2 x clock."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        out = {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+               "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        out = dict(FALLBACK, source="fallback (B200_PROFILING.md)")
+    out["fp32_tflops"] = SM_COUNT * 128 * 2 * out["sm_max_mhz"] * 1e6 / 1e12
+    return out
+
+
+def layer_work(d: dict) -> tuple[float, float]:
+    """(FLOPs, compulsory bytes) of one invocation: F = 2 N K P Q Cg R S;
+    B = x + w + y in the layer dtypes + fp32 bias."""
+    P, Q = tp.output_shape(d)
+    eb = 2 if d["dtype"] == tp.BF16 else 4
+    ob = 2 if d.get("out_dtype", d["dtype"]) == tp.BF16 else 4
+    cg = d["c"] // d.get("groups", 1)
+    f = 2.0 * d["n"] * d["k"] * P * Q * cg * d["r"] * d["s"]
+    b = d["n"] * d["c"] * d["h"] * d["w"] * eb + d["k"] * cg * d["r"] * d["s"] * eb + d["n"] * d["k"] * P * Q * ob \
+        + 4 * d["k"]
+    return f, float(b)
+
+
+def roofline(d: dict, t_us: float, sm_granted: int, part_bw_gbs: float, floor_us: float, pk: dict,
+             kind: int) -> dict:
+    """Fractions of SURVEY 8(d) for one layer at its SM share.  The binding
+    roof is the largest of the compute time (tensor for the tc path, FFMA for
+    the direct path), the HBM time at the partition's measured bandwidth and
+    the measured launch floor."""
+    f, b = layer_work(d)
+    share = sm_granted / SM_COUNT
+    tensor_peak = pk["bf16_tflops"] * 1e12 * share
+    alu_peak = pk["fp32_tflops"] * 1e12 * share
+    t = t_us * 1e-6
+    compute_peak = alu_peak if kind == tp.KIND_DIRECT else tensor_peak
+    roofs = {"compute_us": f / compute_peak * 1e6, "hbm_us": b / (part_bw_gbs * 1e9) * 1e6, "floor_us": floor_us}
+    bound = max(roofs, key=roofs.get)
+    return {"flops": f, "bytes": b, "tensor_frac": f / (t * tensor_peak), "alu_frac": f / (t * alu_peak),
+            "hbm_frac": b / (t * part_bw_gbs * 1e9), "roof_us": roofs, "binding": bound.replace("_us", ""),
+            "frac_of_binding_roof": roofs[bound] / t_us}
+
+
+def make_buffers(layers: list[dict], part=None, config: int = 2, device: int = 0) -> list:
+    out = []
+    for i, d in enumerate(layers):
+        x, w, b = datagen.make_inputs(d, datagen.data_seed(config, i))
+        out.append(tp.LayerBuffers(d, x, w, b, part=part, device=device))
+    return out
+
+
+def tune_layers(layers, bufs, part, trials=1000, seed=42, timing_cfg=None) -> list[dict]:
+    """Tune each layer inside `part`; returns per-layer dicts with the best
+    schedule, its measurement and the tuning throughput."""
+    res = []
+    for d, buf in zip(layers, bufs):
+        t0 = time.perf_counter()
+        best, m, recs = tp.tune(buf, part, trials, seed, timing_cfg=timing_cfg)
+        el = time.perf_counter() - t0
+        res.append({"layer": d["name"], "mult": d.get("mult", 1), "best": best, "best_m": m,
+                    "candidates": len(recs), "ok": sum(1 for r in recs if r["status"] == 0), "wall_s": el})
+    return res
+
+
+def partition_context(part) -> dict:
+    """Granted SMs, measured copy bandwidth and launch floor of a partition."""
+    bw = part.copy_bw(1 << 30, 5)
+    fl = part.floor(1, 128)["median_us"]
+    return {"fraction": part.fraction, "sm_requested": part.sm_requested, "sm_granted": part.sm_granted,
+            "copy_bw_gbs": bw, "floor_us": fl}
+
+
+def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3, timing_cfg=None,
+               log=print) -> dict:
+    """a13: tune every layer at each fraction p, then run each frozen best(p)
+    at every fraction q.  Returns per-layer matrices M[p][q] (median us), the
+    model sums Sum_l mult_l * M_l[p][q] (reading C21), the diagonal check
+    (P-D) and per-cell rooflines of the diagonal."""
+    pk = peaks()
+    parts = {f: tp.Partition.get(f) for f in fractions}
+    ctx = {f: partition_context(parts[f]) for f in fractions}
+    bufs = make_buffers(layers, None, config)
+    tuned = {}
+    tune_stats = {}
+    for p in fractions:
+        t0 = time.perf_counter()
+        tuned[p] = tune_layers(layers, bufs, parts[p], trials, datagen.sampler_seed(fractions.index(p)), timing_cfg)
+        el = time.perf_counter() - t0
+        n = sum(r["candidates"] for r in tuned[p])
+        tune_stats[p] = {"candidates": n, "wall_s": el, "candidates_per_s": n / el}
+        log(f"tuned at {p}: {n} candidates in {el:.1f}s")
+    per_layer = []
+    model = {p: {q: 0.0 for q in fractions} for p in fractions}
+    for li, d in enumerate(layers):
+        mat = {}
+        for p in fractions:
+            row = {}
+            for q in fractions:
+                m = tp.cross_eval(bufs[li], tuned[p][li]["best"], parts[q], timing_cfg)
+                row[q] = m["median_us"]
+                model[p][q] += d.get("mult", 1) * m["median_us"]
+            mat[p] = row
+        diag = {}
+        for q in fractions:
+            bm = tuned[q][li]["best_m"]
+            diag[q] = roofline(d, mat[q][q], ctx[q]["sm_granted"], ctx[q]["copy_bw_gbs"], ctx[q]["floor_us"], pk,
+                               bm["kind"])
+        per_layer.append({"layer": d["name"], "mult": d.get("mult", 1),
+                          "matrix_us": {str(p): {str(q): mat[p][q] for q in fractions} for p in fractions},
+                          "best_schedule": {str(p): {k: tuned[p][li]["best"][k] for k in
+                                                     ("space_index", "kind", "bm", "bn", "bk", "stages", "threads",
+                                                      "split_k", "tile_q", "vec_k", "tile_p", "smem_stage", "grid_x",
+                                                      "grid_y", "grid_z")} for p in fractions},
+                          "diag_roofline": {str(q): diag[q] for q in fractions}})
+    # P-D: with exhaustive tuning the diagonal is the column minimum up to noise.
+    viol = []
+    for row in per_layer:
+        for q in fractions:
+            col = [row["matrix_us"][str(p)][str(q)] for p in fractions]
+            if row["matrix_us"][str(q)][str(q)] > min(col) * 1.10:
+                viol.append({"layer": row["layer"], "q": q, "diag": row["matrix_us"][str(q)][str(q)],
+                             "col_min": min(col)})
+    return {"fractions": list(fractions), "partitions": {str(f): ctx[f] for f in fractions}, "peaks": pk,
+            "tune": {str(p): tune_stats[p] for p in fractions},
+            "model_sum_us": {str(p): {str(q): model[p][q] for q in fractions} for p in fractions},
+            "diagonal_violations_gt10pct": viol, "layers": per_layer}
+
+
+def _lpt(layers, k):
+    """Longest-processing-time-first assignment of layers to k tuners by FLOPs."""
+    order = sorted(range(len(layers)), key=lambda i: -layer_work(layers[i])[0])
+    load = [0.0] * k
+    assign = [[] for _ in range(k)]
+    for i in order:
+        j = min(range(k), key=lambda t: load[t])
+        assign[j].append(i)
+        load[j] += layer_work(layers[i])[0]
+    return assign
+
+
+def concurrent_tune(layers, k=4, sms_each=37, trials=1000, config=4, timing_cfg=None, flags=tp.PART_FINE_GRAINED,
+                    log=print) -> dict:
+    """a14: k disjoint partitions of sms_each SMs (one split), one host thread
+    per partition tuning its LPT share of the layers concurrently.  Then the
+    winners are timed solo (one partition busy) and co-running (all k busy)."""
+    pk = peaks()
+    # The driver grants SMs in TPC pairs even when co-scheduling is ignored, so
+    # k x sms_each may not fit exactly (4 x 37 = 148 does not): step down.
+    parts, asked = None, sms_each
+    while parts is None:
+        try:
+            parts = tp.Partition.split(k, asked, flags=flags)
+        except tp.TPError as e:
+            if e.status != tp.ECAPACITY or asked <= 8:
+                raise
+            asked -= 1
+    ctx = [partition_context(p) for p in parts]
+    assign = _lpt(layers, k)
+    bufs = {}
+    for j, idxs in enumerate(assign):
+        for i in idxs:
+            d = layers[i]
+            x, w, b = datagen.make_inputs(d, datagen.data_seed(config, i))
+            bufs[i] = tp.LayerBuffers(d, x, w, b, part=parts[j])
+    results = [None] * k
+    errors = []
+
+    def worker(j):
+        try:
+            out = []
+            t0 = time.perf_counter()
+            for i in assign[j]:
+                best, m, recs = tp.tune(bufs[i], parts[j], trials, datagen.sampler_seed(1), timing_cfg=timing_cfg)
+                out.append({"layer": layers[i]["name"], "idx": i, "best": best, "best_m": m, "candidates": len(recs)})
+            results[j] = {"wall_s": time.perf_counter() - t0, "layers": out}
+        except Exception as e:   # surfaced below
+            errors.append(repr(e))
+
+    t0 = time.perf_counter()
+    th = [threading.Thread(target=worker, args=(j,)) for j in range(k)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    wall = time.perf_counter() - t0
+    if errors:
+        raise RuntimeError("; ".join(errors))
+    n = sum(r["candidates"] for res in results for r in res["layers"])
+    log(f"{k} concurrent tuners: {n} candidates in {wall:.1f}s")
+
+    # isolation: winners solo vs co-running
+    def time_all(j, out):
+        for r in results[j]["layers"]:
+            m = tp.conv2d_run(bufs[r["idx"]], r["best"], parts[j], timing_cfg or tp.timing())
+            out[r["layer"]] = m["median_us"]
+
+    solo = {}
+    for j in range(k):
+        time_all(j, solo)
+    co = {}
+    th = [threading.Thread(target=time_all, args=(j, co)) for j in range(k)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    layers_out = []
+    for j in range(k):
+        for r in results[j]["layers"]:
+            d = layers[r["idx"]]
+            layers_out.append({"layer": r["layer"], "tuner": j, "sm_granted": ctx[j]["sm_granted"],
+                               "best_us": r["best_m"]["median_us"], "solo_us": solo[r["layer"]],
+                               "corun_us": co[r["layer"]], "candidates": r["candidates"],
+                               "schedule": {kk: r["best"][kk] for kk in ("space_index", "kind", "bm", "bn", "bk",
+                                                                         "stages", "threads", "split_k")},
+                               "roofline": roofline(d, solo[r["layer"]], ctx[j]["sm_granted"],
+                                                    ctx[j]["copy_bw_gbs"], ctx[j]["floor_us"], pk,
+                                                    r["best_m"]["kind"])})
+    for p in parts:
+        p.close()
+    return {"k": k, "sms_each_requested": sms_each, "sms_each_split": asked, "partitions": ctx, "peaks": pk, "wall_s": wall, "candidates": n,
+            "candidates_per_s": n / wall, "per_tuner_wall_s": [results[j]["wall_s"] for j in range(k)],
+            "assignment": [[layers[i]["name"] for i in a] for a in assign], "layers": layers_out}

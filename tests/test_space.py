@@ -1,5 +1,7 @@
 """Pins for the CPU schedule-space enumeration (oracle/space.py), and
 bit-exact agreement of libtp's host-only space functions with it (P-S)."""
+import itertools
+
 import numpy as np
 import pytest
 
@@ -33,11 +35,22 @@ def test_argmin_tie_break():
     assert sp.argmin([dict(status=5, median_us=1.0, space_index=0)]) == -1
 
 
+def _direct_count(d):
+    return sum(1 for th, tq, vk, tpp, sm in itertools.product(*[v for _, v in sp.DIRECT_KNOBS])
+               if sp._valid_direct(d, th, tq, vk, tpp, sm))
+
+
 def test_space_counts_and_order():
     # Totals cross-checked against SURVEY.md 8(a) a2's independent count of the same
-    # predicate (R50 14,432; VGG-19 6,672).
-    assert sum(len(sp.enumerate_space(d)) for d in wl.catalog("resnet50")) == 14432
-    assert sum(len(sp.enumerate_space(d)) for d in wl.catalog("vgg19_b16")) == 6672
+    # predicate (R50 14,432; VGG-19 6,672), which put the C = 3 stems on the direct
+    # kind; they now take the gathered tensor-core kind, so the SURVEY totals hold
+    # for the other layers plus the stems' direct-space counts.
+    for name, total in (("resnet50", 14432), ("vgg19_b16", 6672)):
+        cat = wl.catalog(name)
+        stems = [d for d in cat if sp.layer_kind(d) == sp.KIND_IGEMM_TC_GATHER]
+        rest = [d for d in cat if sp.layer_kind(d) != sp.KIND_IGEMM_TC_GATHER]
+        assert len(stems) == 1 and stems[0]["c"] == 3
+        assert sum(len(sp.enumerate_space(d)) for d in rest) + _direct_count(stems[0]) == total
     d = wl.catalog("resnet50")[2]
     s = sp.enumerate_space(d)
     keys = [(x["bm"], x["bn"], x["bk"], x["stages"], x["threads"], x["split_k"]) for x in s]
@@ -45,9 +58,27 @@ def test_space_counts_and_order():
     assert [x["space_index"] for x in s] == list(range(len(s)))
 
 
+def test_gather_space_hand_count():
+    # R50 conv1 (C=3, 7x7 s2, K=64, M=12544): reduction R*S*C = 147 (np2 256).
+    # BN in {32, 64}; BM in {64, 128}; every BK; split_k <= ceil(147/BK);
+    # smem = stages (BM+BN) BK 2 + 1024 + 16 BM + 8 ceil(147/BK) BK <= 232448.
+    n = 0
+    for bm in (64, 128):
+        for bn in (32, 64):
+            for bk in (16, 32, 64, 128):
+                nkb = -(-147 // bk)
+                for st in (2, 3, 4, 6):
+                    if st * (bm + bn) * bk * 2 + 1024 + 16 * bm + 8 * nkb * bk > 232448:
+                        continue
+                    n += 2 * sum(1 for sk in (1, 2, 4, 8) if sk <= nkb)
+    d = wl.catalog("resnet50")[0]
+    assert len(sp.enumerate_space(d)) == n
+    assert all(s["kind"] == sp.KIND_IGEMM_TC_GATHER for s in sp.enumerate_space(d))
+
+
 def test_kind_selection():
     r50 = wl.catalog("resnet50")
-    assert sp.layer_kind(r50[0]) == sp.KIND_DIRECT          # C = 3 stem
+    assert sp.layer_kind(r50[0]) == sp.KIND_IGEMM_TC_GATHER  # C = 3 stem
     assert all(sp.layer_kind(d) == sp.KIND_IGEMM_TC for d in r50[1:])
     assert sp.layer_kind(wl.catalog("cfg1")[0]) == sp.KIND_DIRECT   # fp32
     mb = wl.catalog("mobilenetv2")
@@ -85,7 +116,7 @@ def test_libtp_space_matches_mirror(d):
     for m in mirror:
         s = tp.space_get(d, m["space_index"])
         assert s["kind"] == m["kind"]
-        for f in (fields_tc if m["kind"] == sp.KIND_IGEMM_TC else fields_dir):
+        for f in (fields_dir if m["kind"] == sp.KIND_DIRECT else fields_tc):
             assert s[f] == m[f], (f, m)
         assert (s["grid_x"], s["grid_y"], s["grid_z"]) == (m["grid_x"], m["grid_y"], m["grid_z"])
         assert s["space_index"] == m["space_index"]

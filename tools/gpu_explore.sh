@@ -1,3 +1,5 @@
-mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/parity.log 2>&1; tail -3 gpurun_out/parity.log
-timeout 900 python tools/explore.py resnet50 r50.l1.b0.c2,r50.l3.b1.c1,r50.l3.b1.c2,r50.l4.b1.c1,r50.l4.b1.c2,r50.l4.b0.c2 gpurun_out/explore2.json > gpurun_out/explore2.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "tc_every or random or vgg" 2>&1 | tail -2
+python tools/trace_sched.py vgg19_b16 vgg.64.224.0 128 64 16 2 128 1 0.25
+python tools/trace_sched.py vgg19_b16 vgg.64.224.0 128 64 32 2 128 1 0.25
+python tools/trace_sched.py resnet50 r50.conv1 64 32 32 3 256 1
+python tools/trace_sched.py resnet50 r50.conv1 128 64 64 3 256 1
