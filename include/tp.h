@@ -194,7 +194,9 @@ tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partitio
  * each of the first 4 ring-fill loads issued, [58] TMEM allocated (warp 2), [60] split-K via
  * DSMEM cluster (1) or global workspace (0), [61] %cluster_nctarank, [62] %smid,
  * [63] %globaltimer at entry (ns), [64] split-K slices sent (st.async), [65] past the
- * cluster barrier, [66] all slices received, [67] reduction stored.
+ * cluster barrier, [66] all slices received, [67] reduction stored; gathered kind,
+ * first 8 k-blocks: [68..75] chunks stored, [76..83] past the proxy fence, [84..91]
+ * past the empty-slot wait.
  * cap = rows. */
 tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part, const void* x,
                           const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,

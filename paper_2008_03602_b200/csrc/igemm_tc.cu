@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     uint32_t phase = 0;
     for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(empty + stage, phase ^ 1u);
+      if (trace && threadIdx.x == 0 && kb - kb0 < 8) trace[84 + kb - kb0] = gtimer();
       uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
       uint8_t* sbt = b_tiles + (size_t)stage * B_STAGE;
       const int kbase = kb * BK;
@@ -455,8 +456,10 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
         uint8_t* dst = (is_a ? sa + sub * A_SUB : sbt + sub * B_SUB) + off;
         *reinterpret_cast<uint4*>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
       }
+      if (trace && threadIdx.x == 0 && kb - kb0 < 8) trace[68 + kb - kb0] = gtimer();
       // generic-proxy smem writes -> visible to the tensor core (async proxy)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (trace && threadIdx.x == 0 && kb - kb0 < 8) trace[76 + kb - kb0] = gtimer();
       __syncwarp();
       if (lane == 0) mbar_arrive(full + stage);
       if (trace && threadIdx.x == 0 && kb - kb0 < kTraceK) trace[20 + kb - kb0] = gtimer();

@@ -23,3 +23,7 @@ print("  kb arrivals (MMA)", [int(np.median(tr[:, 4 + i] - tr[:, 0])) for i in r
 print("  producer kb done", [int(np.median(tr[:, 20 + i] - tr[:, 0])) for i in range(16) if (tr[:, 20 + i] > 0).all()])
 print("  start times us: span", round(float(g.max()), 2), "per-SM CTAs:", np.bincount(tr[:, 62].astype(int)).max(),
       "concurrency est", round(float(np.sum(life) / 1.9e3 / max(g.max(), 1e-9)), 1))
+if (tr[:, 84] > 0).any():
+    print("  gather: past empty-wait", [int(np.median(tr[:, 84 + i] - tr[:, 0])) for i in range(8) if (tr[:, 84 + i] > 0).all()])
+    print("  gather: chunks stored  ", [int(np.median(tr[:, 68 + i] - tr[:, 0])) for i in range(8) if (tr[:, 68 + i] > 0).all()])
+    print("  gather: past fence     ", [int(np.median(tr[:, 76 + i] - tr[:, 0])) for i in range(8) if (tr[:, 76 + i] > 0).all()])
