@@ -101,7 +101,7 @@ typedef struct {
     double max_abs_err, max_ref;                 /* correctness gate (a10)               */
 } tp_measurement;
 
-/* Timing protocol (reading C12). NULL -> defaults {3, 5, 10, 20.0, 1, 0}. */
+/* Timing protocol (reading C12). NULL -> defaults {3, 5, 10, 20.0, 1, 0, 2.0}. */
 typedef struct {
     int32_t warmup;           /* untimed launches before timing                      */
     int32_t groups;           /* r: number of timed groups (median over groups)      */
@@ -109,6 +109,11 @@ typedef struct {
     double target_group_us;   /* n = max(n_min, ceil(target / t_est))                */
     int32_t use_graph;        /* capture each group's n launches as one CUDA graph    */
     int32_t flush_l2;         /* 1: write a > L2 buffer before every launch (cold L2) */
+    double prune_ratio;       /* tuner only (reading C12b): a candidate whose gate-run time
+                                 exceeds prune_ratio x the fastest gate-run time of the same
+                                 tp_tune / tp_tune_subset call is timed with ONE group of n
+                                 launches instead of `groups` (its record says groups = 1);
+                                 0 = every candidate gets `groups`.  Default 2.0.           */
 } tp_timing;
 
 typedef struct tp_partition tp_partition;   /* opaque: green context + stream (or whole device) */

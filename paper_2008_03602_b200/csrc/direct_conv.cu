@@ -53,6 +53,46 @@ __device__ __forceinline__ void st_out(void* y, int64_t off, float v, int out_f3
   else reinterpret_cast<__nv_bfloat16*>(y)[off] = __float2bfloat16_rn(v);
 }
 
+// Depthwise 3x3, compile-time stride: the 3 x VK weights of a filter row and
+// the (TQ-1)*SW+3 input columns of an input row are loaded once per row, with
+// every load of the row issued before the FMAs (one memory latency per filter
+// row instead of one per tap).
+template <typename T, int TQ, int VK, int SW>
+__device__ __forceinline__ void dw3x3_rows(const DirectArgs& a, const T* __restrict__ x, const T* __restrict__ w,
+                                           int n, int p, int q0, int k0, float (&acc)[TQ][VK]) {
+  constexpr int NC = (TQ - 1) * SW + 3;
+  const int H = a.H, W = a.W, C = a.C;
+  const int wbase = q0 * SW - a.pw;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int hi = p * a.sh - a.ph + r;
+    if ((unsigned)hi >= (unsigned)H) continue;
+    const T* xrow = x + ((int64_t)n * H + hi) * W * C + k0;
+    float wv[3][VK];
+#pragma unroll
+    for (int s = 0; s < 3; ++s)
+#pragma unroll
+      for (int j = 0; j < VK; ++j) wv[s][j] = ld_f<T>(w + (int64_t)(k0 + j) * 9 + r * 3 + s);
+    float xc[NC][VK];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int wi = wbase + c;
+      if ((unsigned)wi < (unsigned)W) {
+        ld_vec<T, VK>(xrow + (int64_t)wi * C, xc[c]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < VK; ++j) xc[c][j] = 0.0f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TQ; ++i)
+#pragma unroll
+      for (int s = 0; s < 3; ++s)
+#pragma unroll
+        for (int j = 0; j < VK; ++j) acc[i][j] = fmaf(xc[i * SW + s][j], wv[s][j], acc[i][j]);
+  }
+}
+
 template <typename T, int TQ, int VK, bool DW, bool SMEM>
 __global__ void __launch_bounds__(512) direct_conv_kernel(DirectArgs a) {
   extern __shared__ float dsm[];
@@ -80,7 +120,15 @@ __global__ void __launch_bounds__(512) direct_conv_kernel(DirectArgs a) {
 #pragma unroll
     for (int j = 0; j < VK; ++j) acc[i][j] = 0.0f;
 
-  if constexpr (!SMEM) {
+  // Depthwise 3x3 with stride 1 or 2 (every MobileNet depthwise layer): the
+  // unrolled row-at-a-time path.
+  const bool dw33 = DW && !SMEM && R == 3 && S == 3 && (a.sw == 1 || a.sw == 2);
+  if (dw33) {
+    if (p < a.P && k0 < K) {
+      if (a.sw == 1) dw3x3_rows<T, TQ, VK, 1>(a, x, w, n, p, q0, k0, acc);
+      else dw3x3_rows<T, TQ, VK, 2>(a, x, w, n, p, q0, k0, acc);
+    }
+  } else if constexpr (!SMEM) {
     if (p < a.P) {
       for (int r = 0; r < R; ++r) {
         const int hi = p * a.sh - a.ph + r;

@@ -421,40 +421,58 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
       uint8_t* sbt = b_tiles + (size_t)stage * B_STAGE;
       const int kbase = kb * BK;
-      for (int id = pt; id < (BM + BN) * CPR; id += np) {
-        const bool is_a = id < BM * CPR;
-        const int rid = is_a ? id : id - BM * CPR;
-        const int row = rid / CPR, kc = rid % CPR;
-        const int k0 = kbase + kc * 8;
-        uint32_t v[4];
-        if (is_a) {
-          const int4 rt = rowtab[row];
+      // np is a multiple of 32 and CPR divides 32, so this thread's 16-byte
+      // chunk column kc is the same for every row it fills: its 8 k-table
+      // entries are read once per k-block, and the rows (pixel rows of A, then
+      // weight rows of B) are visited 4 at a time with all 32 element loads
+      // issued before any shared-memory store.
+      const int kc = pt % CPR, rstep = np / CPR;
+      const int k0 = kbase + kc * 8;
+      int2 kt[8];
 #pragma unroll
-          for (int j = 0; j < 8; j += 2) {
-            uint32_t lo = 0, hi = 0;
-            const int2 e0 = ktab[k0 + j], e1 = ktab[k0 + j + 1];
-            if ((unsigned)(rt.y + (e0.y >> 16)) < (unsigned)a.H && (unsigned)(rt.z + (e0.y & 0xFFFF)) < (unsigned)a.W)
-              lo = __ldg(xg + rt.x + e0.x);
-            if ((unsigned)(rt.y + (e1.y >> 16)) < (unsigned)a.H && (unsigned)(rt.z + (e1.y & 0xFFFF)) < (unsigned)a.W)
-              hi = __ldg(xg + rt.x + e1.x);
-            v[j / 2] = lo | (hi << 16);
-          }
-        } else {
-          const int kn = nbase + row;
-          const uint16_t* wr = wg + (int64_t)kn * a.Kg;
+      for (int j = 0; j < 8; ++j) kt[j] = ktab[k0 + j];
+      const int sub = (kc * 8) / SUBK, ch = ((kc * 8) % SUBK) / 8;
+      for (int row0 = pt / CPR; row0 < BM + BN; row0 += 4 * rstep) {
+        uint32_t v[4][4];
 #pragma unroll
-          for (int j = 0; j < 8; j += 2) {
-            uint32_t lo = 0, hi = 0;
-            if (kn < a.K && k0 + j < a.Kg) lo = __ldg(wr + k0 + j);
-            if (kn < a.K && k0 + j + 1 < a.Kg) hi = __ldg(wr + k0 + j + 1);
-            v[j / 2] = lo | (hi << 16);
+        for (int u = 0; u < 4; ++u) {
+          const int rr = row0 + u * rstep;
+          if (rr < BM) {
+            const int4 rt = rowtab[rr];
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+              uint32_t lo = 0, hi = 0;
+              if ((unsigned)(rt.y + (kt[j].y >> 16)) < (unsigned)a.H &&
+                  (unsigned)(rt.z + (kt[j].y & 0xFFFF)) < (unsigned)a.W)
+                lo = __ldg(xg + rt.x + kt[j].x);
+              if ((unsigned)(rt.y + (kt[j + 1].y >> 16)) < (unsigned)a.H &&
+                  (unsigned)(rt.z + (kt[j + 1].y & 0xFFFF)) < (unsigned)a.W)
+                hi = __ldg(xg + rt.x + kt[j + 1].x);
+              v[u][j / 2] = lo | (hi << 16);
+            }
+          } else if (rr < BM + BN) {
+            const int kn = nbase + rr - BM;
+            const uint16_t* wr = wg + (int64_t)kn * a.Kg + k0;
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+              uint32_t lo = 0, hi = 0;
+              if (kn < a.K && k0 + j < a.Kg) lo = __ldg(wr + j);
+              if (kn < a.K && k0 + j + 1 < a.Kg) hi = __ldg(wr + j + 1);
+              v[u][j / 2] = lo | (hi << 16);
+            }
           }
         }
-        const int sub = (kc * 8) / SUBK, ch = ((kc * 8) % SUBK) / 8;
-        uint32_t off = (uint32_t)row * SWZ + (uint32_t)ch * 16;
-        off ^= ((off >> 7) & SWM) << 4;
-        uint8_t* dst = (is_a ? sa + sub * A_SUB : sbt + sub * B_SUB) + off;
-        *reinterpret_cast<uint4*>(dst) = make_uint4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rr = row0 + u * rstep;
+          if (rr >= BM + BN) break;
+          const bool is_a = rr < BM;
+          const int row = is_a ? rr : rr - BM;
+          uint32_t off = (uint32_t)row * SWZ + (uint32_t)ch * 16;
+          off ^= ((off >> 7) & SWM) << 4;
+          uint8_t* dst = (is_a ? sa + sub * A_SUB : sbt + sub * B_SUB) + off;
+          *reinterpret_cast<uint4*>(dst) = make_uint4(v[u][0], v[u][1], v[u][2], v[u][3]);
+        }
       }
       if (trace && threadIdx.x == 0 && kb - kb0 < 8) trace[68 + kb - kb0] = gtimer();
       // generic-proxy smem writes -> visible to the tensor core (async proxy)

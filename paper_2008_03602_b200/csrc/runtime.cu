@@ -114,18 +114,28 @@ static CUcontext current_ctx() {
   return c;
 }
 
+// The max-dynamic-smem attribute may be shared by every context that uses the
+// function (green contexts included), so it is only ever raised, always to the
+// largest value requested for that function in any context: a partition that
+// needs less can never lower it under another context's cached entry.
+static std::map<const void*, size_t> g_smem_fn_max;
+
 cudaError_t ensure_smem_attr(const void* fn, size_t smem) {
   const auto key = std::make_pair(fn, current_ctx());
+  size_t want;
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_smem_attr.find(key);
     if (it != g_smem_attr.end() && it->second >= smem) return cudaSuccess;
+    size_t& m = g_smem_fn_max[fn];
+    m = std::max(m, smem);
+    want = m;
   }
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want);
   if (e == cudaSuccess) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     size_t& v = g_smem_attr[key];
-    v = std::max(v, smem);
+    v = std::max(v, want);
   }
   return e;
 }
@@ -411,6 +421,7 @@ static void plan_geometry(const ConvPlan& p, int sm_granted, tp_measurement* m) 
 static tp_timing default_timing() {
   tp_timing t;
   t.warmup = 3; t.groups = 5; t.n_min = 10; t.target_group_us = 20.0; t.use_graph = 1; t.flush_l2 = 0;
+  t.prune_ratio = 2.0;
   return t;
 }
 
@@ -643,6 +654,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     bool live = false;       // passed make_plan + gate
     double t_est = 0;
     int n = 0;
+    int groups = 1;          // timed groups (C12 / C12b)
     cudaGraphExec_t exec = nullptr;
     int slot = -1;           // event slot in phase B
   };
@@ -684,16 +696,23 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         tp_status s2 = make_plan(L, table[cand[i]], x, w, bias, y, ws, ws_bytes, &c.plan);
         if (s2 != TP_OK) { c.m.status = s2; continue; }
         plan_geometry(c.plan, part->sm_granted, &c.m);
+        const char* step = "poison";
         cudaError_t e = cudaMemsetAsync(y, 0xFF, ybytes, st);   // NaN in bf16 and fp32
-        if (e == cudaSuccess) e = cudaEventRecord(pa.ev[2 * (i - c0)], st);
-        if (e == cudaSuccess) e = launch_plan(c.plan, st);
-        if (e == cudaSuccess) e = cudaEventRecord(pa.ev[2 * (i - c0) + 1], st);
-        if (e == cudaSuccess)
+        if (e == cudaSuccess) { step = "event"; e = cudaEventRecord(pa.ev[2 * (i - c0)], st); }
+        if (e == cudaSuccess) { step = "conv"; e = launch_plan(c.plan, st); }
+        if (e == cudaSuccess) { step = "event"; e = cudaEventRecord(pa.ev[2 * (i - c0) + 1], st); }
+        if (e == cudaSuccess) {
+          step = "gather";
           e = launch_gather(y, L.d.in_layout == TP_LAYOUT_NHWC, L.d.out_dtype == TP_DTYPE_FP32, L.d.n, L.d.k, L.P,
                             L.Q, gate->d_idx, ncheck, d_vals + (size_t)(i - c0) * ncheck, st);
+        }
         if (e != cudaSuccess) {
+          cudaGetLastError();   // a failed launch must not poison the next candidate's error check
           c.m.status = TP_ECUDA;
-          set_error(std::string("gate launch: ") + cudaGetErrorString(e));
+          set_error(std::string("gate ") + step + " launch (space_index " + std::to_string(cand[i]) + ", grid " +
+                    std::to_string(c.plan.tc.grid.x) + "x" + std::to_string(c.plan.tc.grid.y) + "x" +
+                    std::to_string(c.plan.tc.grid.z) + ", cluster_z " + std::to_string(c.plan.tc.cluster_z) +
+                    ", smem " + std::to_string(c.plan.tc.smem) + "): " + cudaGetErrorString(e));
           continue;
         }
         g_launches += 1;
@@ -743,6 +762,11 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     }
 
     // ---------------- phase B: timing, windowed pipeline ----------------
+    // Reading C12b: candidates far slower than the fastest gate run of this
+    // call get one timed group (still a warm, graph-timed median of n launches).
+    double t_best_est = 1e30;
+    for (int32_t i = 0; i < n_cand; ++i)
+      if (cs[i].live) t_best_est = std::min(t_best_est, cs[i].t_est);
     EventPool pb;
     TP_CK(pb.ensure((size_t)kWindow * 2 * groups));
     std::vector<int> free_slots;
@@ -751,9 +775,9 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     auto harvest = [&](int32_t i) -> tp_status {
       Cand& c = cs[i];
       cudaEvent_t* ev = pb.ev.data() + (size_t)c.slot * 2 * groups;
-      cudaError_t e = cudaEventSynchronize(ev[2 * groups - 1]);
+      cudaError_t e = cudaEventSynchronize(ev[2 * c.groups - 1]);
       std::vector<double> per;
-      for (int g = 0; g < groups && e == cudaSuccess; ++g) {
+      for (int g = 0; g < c.groups && e == cudaSuccess; ++g) {
         float ms = 0;
         e = cudaEventElapsedTime(&ms, ev[2 * g], ev[2 * g + 1]);
         per.push_back(ms * 1000.0 / c.n);
@@ -777,7 +801,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       for (double v : per) var += (v - mean) * (v - mean);
       c.m.mean_us = mean;
       c.m.std_us = k > 1 ? std::sqrt(var / (k - 1)) : 0.0;
-      c.m.groups = groups;
+      c.m.groups = c.groups;
       c.m.n_per_group = c.n;
       c.m.status = TP_OK;
       return TP_OK;
@@ -793,6 +817,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       c.slot = free_slots.back();
       free_slots.pop_back();
       c.n = std::min(4096, std::max(std::max(1, tm.n_min), (int)std::ceil(tm.target_group_us / c.t_est)));
+      c.groups = (tm.prune_ratio > 0 && c.t_est > tm.prune_ratio * t_best_est) ? 1 : groups;
       cudaError_t e = cudaSuccess;
       for (int k = 0; k < std::max(0, tm.warmup) && e == cudaSuccess; ++k) e = launch_plan(c.plan, st);
       if (e == cudaSuccess && tm.use_graph) {
@@ -809,7 +834,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         if (graph) cudaGraphDestroy(graph);
       }
       cudaEvent_t* ev = pb.ev.data() + (size_t)c.slot * 2 * groups;
-      for (int g = 0; g < groups && e == cudaSuccess; ++g) {
+      for (int g = 0; g < c.groups && e == cudaSuccess; ++g) {
         e = cudaEventRecord(ev[2 * g], st);
         if (e == cudaSuccess) {
           if (c.exec) {
@@ -836,6 +861,26 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     for (int32_t i : inflight) {
       tp_status h = harvest(i);
       if (err == TP_OK) err = h;
+    }
+    // C12b: a raced candidate that beat every fully-timed one is re-timed with
+    // the full protocol, so the winner's record is always a full measurement.
+    if (err == TP_OK && groups > 1) {
+      double best_full = 1e30;
+      for (int32_t i = 0; i < n_cand; ++i)
+        if (cs[i].live && cs[i].m.status == TP_OK && cs[i].groups == groups)
+          best_full = std::min(best_full, cs[i].m.median_us);
+      EventPool pr;
+      for (int32_t i = 0; i < n_cand && err == TP_OK; ++i) {
+        Cand& c = cs[i];
+        if (!c.live || c.m.status != TP_OK || c.groups == groups || !(c.m.median_us < best_full)) continue;
+        tp_measurement m = c.m;
+        err = time_plan(part, c.plan, tm, pr, &m);
+        if (err == TP_OK) {
+          c.m = m;
+          c.groups = groups;
+          best_full = std::min(best_full, m.median_us);
+        }
+      }
     }
     if (err != TP_OK) {
       for (int32_t i = 0; i < n_cand; ++i)

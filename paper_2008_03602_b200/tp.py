@@ -53,7 +53,8 @@ class Measurement(ctypes.Structure):
 
 class Timing(ctypes.Structure):
     _fields_ = [("warmup", ctypes.c_int32), ("groups", ctypes.c_int32), ("n_min", ctypes.c_int32),
-                ("target_group_us", ctypes.c_double), ("use_graph", ctypes.c_int32), ("flush_l2", ctypes.c_int32)]
+                ("target_group_us", ctypes.c_double), ("use_graph", ctypes.c_int32), ("flush_l2", ctypes.c_int32),
+                ("prune_ratio", ctypes.c_double)]
 
 
 _P = ctypes.POINTER
@@ -221,8 +222,8 @@ def shutdown():
     _lib.tp_shutdown()
 
 
-def timing(warmup=3, groups=5, n_min=10, target_group_us=20.0, use_graph=1, flush_l2=0) -> Timing:
-    return Timing(warmup, groups, n_min, target_group_us, use_graph, flush_l2)
+def timing(warmup=3, groups=5, n_min=10, target_group_us=20.0, use_graph=1, flush_l2=0, prune_ratio=2.0) -> Timing:
+    return Timing(warmup, groups, n_min, target_group_us, use_graph, flush_l2, prune_ratio)
 
 
 @dataclass

@@ -134,3 +134,18 @@ def test_launch_counter_advances():
     tp.conv2d_run(buf, tp.space_get(d, 0))
     torch.cuda.synchronize()
     assert tp.launch_count() == c0 + 1
+
+
+def test_prune_ratio_times_slow_candidates_with_one_group():
+    """Reading C12b: with prune_ratio > 0 the clearly-slow candidates get one
+    timed group; the winner always gets the full protocol; 0 disables it."""
+    d = wl.catalog("resnet50")[2]
+    buf, _ = _layer_with_ref(d)
+    best, m, recs = tp.tune(buf, None, trials=10 ** 6, seed=42, timing_cfg=tp.timing(**dict(FAST, prune_ratio=2.0)))
+    groups = FAST.get("groups", 5)
+    bad = [(r["space_index"], r["status"], r["groups"]) for r in recs if r["status"] != 0]
+    assert not bad, (bad[:10], tp._lib.tp_last_error())
+    assert any(r["groups"] == 1 for r in recs) and all(r["groups"] in (1, groups) for r in recs)
+    assert m["groups"] == groups
+    _, _, recs0 = tp.tune(buf, None, trials=50, seed=42, timing_cfg=tp.timing(**dict(FAST, prune_ratio=0.0)))
+    assert all(r["groups"] == groups for r in recs0)
