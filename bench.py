@@ -380,11 +380,11 @@ def main():
     ach_gbs = bytes_tc / (t_tc * 1e-6) / 1e9 if t_tc else 0.0
     ach_tfs = flops_tc / (t_tc * 1e-6) / 1e12 if t_tc else 0.0
     hbm_bound = bytes_tc / pk["hbm_gbs"] > flops_tc / (pk["bf16_tflops"] * 1e3)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    traffic = None   # mean DRAM bytes per launch of the tuned layers (committed ncu capture)
+    prof = os.path.join(ROOT, "profiles", "r01_ncu_dram_r50.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("igemm_tc_dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("mean_dram_bytes_per_launch")
         except Exception:
             traffic = None
     if hbm_bound:

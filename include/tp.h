@@ -202,7 +202,8 @@ tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partitio
  * cluster barrier, [66] all slices received, [67] reduction stored; gathered kind,
  * first 8 k-blocks: [68..75] chunks stored, [76..83] past the proxy fence, [84..91]
  * past the empty-slot wait.
- * cap = rows. */
+ * cap >= grid CTAs: one launch, *rows = CTAs.  cap >= 2 x grid CTAs: two back-to-back
+ * launches (rows [0, CTAs) the first, [CTAs, 2 CTAs) the second; exposes the PDL overlap). */
 tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part, const void* x,
                           const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
                           uint64_t* trace_host, int32_t cap, int32_t* rows);

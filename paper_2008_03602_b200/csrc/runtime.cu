@@ -1175,20 +1175,27 @@ tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partit
   if (st != TP_OK) return st;
   const int64_t ctas = (int64_t)plan.tc.grid.x * plan.tc.grid.y * plan.tc.grid.z;
   if (ctas > cap) { set_error("trace capacity too small"); return TP_EINVAL; }
+  // cap >= 2 * ctas: trace two back-to-back launches (PDL overlap is visible
+  // in the second launch's entry times against the first launch's end times).
+  const int launches = cap >= 2 * ctas ? 2 : 1;
+  const size_t slots = (size_t)ctas * 96;
   unsigned long long* dtr = nullptr;
-  TP_CK(cudaMalloc(&dtr, ctas * 96 * sizeof(unsigned long long)));
-  TP_CK(cudaMemset(dtr, 0, ctas * 96 * sizeof(unsigned long long)));
-  plan.tc.args.trace = dtr;
-  cudaError_t e;
+  TP_CK(cudaMalloc(&dtr, launches * slots * sizeof(unsigned long long)));
+  TP_CK(cudaMemset(dtr, 0, launches * slots * sizeof(unsigned long long)));
+  cudaError_t e = cudaSuccess;
   {
     CtxGuard g(p);
-    e = launch_plan(plan, p->stream);
+    for (int l = 0; l < launches && e == cudaSuccess; ++l) {
+      plan.tc.args.trace = dtr + l * slots;
+      e = launch_plan(plan, p->stream);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
   }
-  if (e == cudaSuccess) e = cudaMemcpy(trace_host, dtr, ctas * 96 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(trace_host, dtr, launches * slots * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   cudaFree(dtr);
   TP_CK(e);
-  *rows = (int32_t)ctas;
+  *rows = (int32_t)(launches * ctas);
   return TP_OK;
 }
 

@@ -125,7 +125,8 @@ def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3,
         tuned[p] = tune_layers(layers, bufs, parts[p], trials, datagen.sampler_seed(fractions.index(p)), timing_cfg)
         el = time.perf_counter() - t0
         n = sum(r["candidates"] for r in tuned[p])
-        tune_stats[p] = {"candidates": n, "wall_s": el, "candidates_per_s": n / el}
+        tune_stats[p] = {"candidates": n, "ok": sum(r["ok"] for r in tuned[p]), "wall_s": el,
+                         "candidates_per_s": n / el}
         log(f"tuned at {p}: {n} candidates in {el:.1f}s")
     per_layer = []
     model = {p: {q: 0.0 for q in fractions} for p in fractions}

@@ -364,10 +364,12 @@ def conv2d_run(buf: LayerBuffers, sched: dict, part: Partition | None = None, ti
     return meas_to_dict(m)
 
 
-def conv2d_trace(buf: "LayerBuffers", sched: dict, part: Partition | None = None) -> np.ndarray:
-    """In-kernel timeline of one IGEMM_TC launch: (ctas, 96) uint64 (see tp.h)."""
+def conv2d_trace(buf: "LayerBuffers", sched: dict, part: Partition | None = None, launches: int = 1) -> np.ndarray:
+    """In-kernel timeline of one (or two back-to-back) tensor-core launches:
+    (launches * ctas, 96) uint64 (see tp.h)."""
     x, w, b, y, ws, wsb = buf.ptrs()
     cap = int(sched.get("grid_x", 0) * sched.get("grid_y", 0) * sched.get("grid_z", 0)) or 65536
+    cap *= max(1, min(2, launches))
     out = np.zeros((cap, 96), dtype=np.uint64)
     rows = _i32()
     _ck(_lib.tp_conv2d_trace(ctypes.byref(buf.cd), ctypes.byref(dict_to_sched(sched)), _h(part), x, w, b, y, ws,

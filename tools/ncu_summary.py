@@ -2,6 +2,7 @@
 
   python tools/ncu_summary.py launches <launches.csv> <out.json>
   python tools/ncu_summary.py full <prof.ncu-rep> <out.json>
+  python tools/ncu_summary.py dram <dram.csv> <out.json> [catalog]   (one launch per layer, catalog order)
 """
 import collections
 import csv
@@ -82,5 +83,34 @@ def full(path, out):
     json.dump({"source": path, "kernels": res}, open(out, "w"), indent=1)
 
 
+def dram(path, out, catalog="resnet50"):
+    """Per-launch DRAM traffic (ncu replays with cold caches: the compulsory
+    bytes each tuned layer really moves) next to its algorithmic bytes."""
+    sys.path.insert(0, ".")
+    from paper_2008_03602_b200 import experiments as ex, workloads as wl
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ii, mi, vi, ui, ki = (h.index(k) for k in ("ID", "Metric Name", "Metric Value", "Metric Unit", "Kernel Name"))
+    per = collections.OrderedDict()
+    for r in rows[hi + 1:]:
+        e = per.setdefault(r[ii], {"kernel": r[ki].split("(")[0]})
+        e[r[mi]] = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1)
+    layers = wl.catalog(catalog)
+    res = []
+    for d, e in zip(layers, per.values()):
+        alg = ex.layer_work(d)[1]
+        traffic = e.get("dram__bytes_read.sum", 0) + e.get("dram__bytes_write.sum", 0)
+        res.append({"layer": d["name"], "kernel": e["kernel"], "dram_bytes": traffic, "algorithmic_bytes": alg,
+                    "ratio": traffic / alg, "cold_us": e.get("gpu__time_duration.sum")})
+    n = len(res)
+    json.dump({"source": path, "note": "ncu default cache control (caches flushed before each replay): DRAM bytes are "
+                                       "the cold-cache traffic of one launch of each tuned layer",
+               "launches": n, "mean_dram_bytes_per_launch": sum(r["dram_bytes"] for r in res) / max(n, 1),
+               "mean_algorithmic_bytes_per_launch": sum(r["algorithmic_bytes"] for r in res) / max(n, 1),
+               "layers": res}, open(out, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    fn = {"launches": launches, "full": full, "dram": dram}[sys.argv[1]]
+    fn(*sys.argv[2:])

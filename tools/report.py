@@ -52,7 +52,8 @@ def main():
                          "roofline": ex.roofline(d, r["best_m"]["median_us"], ctx["sm_granted"], ctx["copy_bw_gbs"],
                                                  ctx["floor_us"], pk, r["best_m"]["kind"])})
         n = sum(r["candidates"] for r in tuned)
-        res = {"partition": ctx, "peaks": pk, "candidates": n, "wall_s": el, "candidates_per_s": n / el,
+        res = {"partition": ctx, "peaks": pk, "candidates": n, "ok": sum(r["ok"] for r in tuned), "wall_s": el,
+               "candidates_per_s": n / el,
                "model_sum_us": sum(d["mult"] * r["best_m"]["median_us"] for d, r in zip(layers, tuned)),
                "layers": rows}
     res["workload"] = wlname
