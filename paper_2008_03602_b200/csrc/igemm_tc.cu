@@ -367,19 +367,13 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     // R*S*C get coordinates that fail every bounds check (zero fill).
     int4* rowtab = reinterpret_cast<int4*>(smem_raw + a.tab_off);
     int2* ktab = reinterpret_cast<int2*>(smem_raw + a.tab_off + BM * 16);
-    // Staged variant (a.stage_rows > 0): the R input rows of each output row the
-    // tile touches are copied to shared memory once; offsets are then into
-    // that buffer ([local output row][r][w][c]) and only w needs a bounds check
-    // (rows outside the image are staged as zeros).
-    const int t_first = (int)m0 / a.Q;
     for (int r = threadIdx.x; r < BM; r += blockDim.x) {
       const int m = (int)m0 + r;
       int4 e = make_int4(0, -(1 << 20), -(1 << 20), 0);
       if (m < (int)a.M) {
         const int q = m % a.Q, t = m / a.Q, pp = t % a.P, n = t / a.P;
         const int h0 = pp * a.sh - a.ph, w0 = q * a.sw - a.pw;
-        if (a.stage_rows) e = make_int4(((t - t_first) * a.R * a.W + w0) * a.C, 0, w0, 0);
-        else e = make_int4(((n * a.H + h0) * a.W + w0) * a.C, h0, w0, 0);
+        e = make_int4(((n * a.H + h0) * a.W + w0) * a.C, h0, w0, 0);
       }
       rowtab[r] = e;
     }
@@ -387,7 +381,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       int2 e = make_int2(0, 0x7FFF7FFF);
       if (k < a.Kg) {
         const int c = k % a.C, rs = k / a.C, ss = rs % a.S, rr = rs / a.S;
-        e = make_int2((rr * a.W + ss) * a.C + c, (a.stage_rows ? 0 : (rr << 16)) | ss);
+        e = make_int2((rr * a.W + ss) * a.C + c, (rr << 16) | ss);
       }
       ktab[k] = e;
     }
@@ -417,27 +411,6 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     const int2* ktab = reinterpret_cast<const int2*>(smem_raw + a.tab_off + BM * 16);
     const uint16_t* xg = reinterpret_cast<const uint16_t*>(a.xg);
     const uint16_t* wg = reinterpret_cast<const uint16_t*>(a.wg);
-    if (a.stage_rows) {
-      // Fill the staging buffer: stage_rows x R input rows of W*C elements,
-      // 4-byte loads (W*C is even when staging is enabled), then a named
-      // barrier over the producer warps only (the MMA warp is not involved).
-      uint32_t* st = reinterpret_cast<uint32_t*>(smem_raw + a.stage_off);
-      const int t_first = (int)m0 / a.Q;
-      const int rowlen = a.W * a.C / 2;   // u32 per input row
-      const int nrows = a.stage_rows * a.R;
-      for (int i = pt; i < nrows * rowlen; i += np) {
-        const int rowi = i / rowlen, e = i - rowi * rowlen;
-        const int lr = rowi / a.R, rr = rowi - lr * a.R;
-        const int t = t_first + lr, n = t / a.P, pp = t - n * a.P;
-        const int h = pp * a.sh - a.ph + rr;
-        uint32_t v = 0;
-        if (n < a.N_ && (unsigned)h < (unsigned)a.H)
-          v = __ldg(reinterpret_cast<const uint32_t*>(xg + ((int64_t)n * a.H + h) * a.W * a.C) + e);
-        st[i] = v;
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(np) : "memory");
-    }
-    const uint16_t* xs = reinterpret_cast<const uint16_t*>(smem_raw + a.stage_off);
     constexpr int CPR = BK / 8;                 // 16-byte chunks per tile row
     constexpr uint32_t SWM = SWZ / 16 - 1;      // swizzle: chunk ^= (offset >> 7) & SWM
     int stage = 0;
@@ -464,18 +437,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int rr = row0 + u * rstep;
-          if (rr < BM && a.stage_rows) {
-            const int4 rt = rowtab[rr];
-#pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-              uint32_t lo = 0, hi = 0;
-              if ((unsigned)(rt.z + (kt[j].y & 0xFFFF)) < (unsigned)a.W && kt[j].y != 0x7FFF7FFF)
-                lo = xs[rt.x + kt[j].x];
-              if ((unsigned)(rt.z + (kt[j + 1].y & 0xFFFF)) < (unsigned)a.W && kt[j + 1].y != 0x7FFF7FFF)
-                hi = xs[rt.x + kt[j + 1].x];
-              v[u][j / 2] = lo | (hi << 16);
-            }
-          } else if (rr < BM) {
+          if (rr < BM) {
             const int4 rt = rowtab[rr];
 #pragma unroll
             for (int j = 0; j < 8; j += 2) {
@@ -810,7 +772,7 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.cblocks = (pb.C + pb.bk - 1) / pb.bk;
   a.kblocks = pb.R * pb.S * a.cblocks;
   a.xg = pb.x; a.wg = pb.w;
-  a.H = pb.H; a.W = pb.W; a.C = pb.C; a.R = pb.R; a.Kg = pb.R * pb.S * pb.C;
+  a.H = pb.H; a.W = pb.W; a.C = pb.C; a.Kg = pb.R * pb.S * pb.C;
   if (pb.gather) a.kblocks = (a.Kg + pb.bk - 1) / pb.bk;
   a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
   a.ws_partial = pb.ws_partial; a.ws_counters = pb.ws_counters;
@@ -843,22 +805,6 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.recv_off = (int)tc_ring_bytes(pb.bm, pb.bn, pb.bk, pb.stages);
   a.tab_off = a.bar_off + 1024;
   plan->smem = (size_t)a.tab_off + (pb.gather ? (size_t)pb.bm * 16 + (size_t)a.kblocks * pb.bk * 8 : 0);
-  // Gathered kind: stage the input rows of the tile in shared memory when
-  // they fit next to the ring (the tile's BM consecutive pixels span at most
-  // ceil((BM - 1) / Q) + 1 output rows, each needing R input rows).
-  a.stage_rows = 0;
-  a.stage_off = 0;
-  a.N_ = pb.N;
-  if (pb.gather && ((int64_t)pb.W * pb.C) % 2 == 0 && !getenv("TP_NO_STAGE")) {
-    const int rows_out = (pb.bm - 1 + pb.Q - 1) / pb.Q + 1;
-    const size_t stage_bytes = (size_t)rows_out * pb.R * pb.W * pb.C * 2;
-    const size_t off = (plan->smem + 15) & ~(size_t)15;
-    if (off + stage_bytes <= 232448) {
-      a.stage_rows = rows_out;
-      a.stage_off = (int)off;
-      plan->smem = off + stage_bytes;
-    }
-  }
   cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
   if (e != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));

@@ -62,10 +62,8 @@ struct TcArgs {
   unsigned long long* trace;   // optional per-CTA timeline (tp_conv2d_trace), nullptr = off
   const void* xg;              // gathered kind: NHWC x and dense [K][R*S*C] weights
   const void* wg;
-  int H, W, C, R, Kg;          // gathered kind: input extent, channels, filter rows, reduction length R*S*C
+  int H, W, C, Kg;             // gathered kind: input extent, channels, reduction length R*S*C
   int tab_off;                 // gathered kind: byte offset of the pixel / k tables
-  int stage_rows, stage_off;   // gathered kind: staged output rows (0 = gather from global) and buffer offset
-  int N_;                      // batch (gathered kind staging)
   int cluster_red;             // 1: split-K reduced through DSMEM in a (1,1,split_k) cluster
   int bar_off;                 // byte offset of the mbarriers in dynamic shared memory
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
