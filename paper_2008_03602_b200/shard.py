@@ -15,7 +15,7 @@ import numpy as np
 
 # Fixed-size record exchanged between ranks (float64 row).
 REC_FIELDS = ("job", "layer", "space_index", "status", "median_us", "min_us", "mean_us", "std_us", "sm_granted",
-              "ctas", "threads_per_cta", "waves", "rank")
+              "ctas", "threads_per_cta", "waves", "rank", "n_per_group", "groups")
 
 
 def shard(cand: list[int] | np.ndarray, rank: int, world: int) -> list[int]:
@@ -35,7 +35,8 @@ def unpack(arr: np.ndarray) -> list[dict]:
     recs = []
     for row in np.asarray(arr).reshape(-1, len(REC_FIELDS)):
         d = dict(zip(REC_FIELDS, row.tolist()))
-        for f in ("job", "layer", "space_index", "status", "sm_granted", "ctas", "threads_per_cta", "waves", "rank"):
+        for f in ("job", "layer", "space_index", "status", "sm_granted", "ctas", "threads_per_cta", "waves", "rank",
+                  "n_per_group", "groups"):
             d[f] = int(d[f])
         recs.append(d)
     return recs
@@ -74,3 +75,21 @@ def merge_best(records: list[dict]) -> dict[tuple[int, int], dict]:
                                                             and r["space_index"] < b["space_index"]):
             best[key] = r
     return best
+
+
+def finalists(records: list[dict], k: int = 3) -> dict[tuple[int, int], list[dict]]:
+    """Top-k OK records per (job, layer) by (median_us, space_index) -- the
+    candidates rank 0 re-times on one device after the gather (SURVEY 8(e):
+    clock/thermal differences between GPUs must not pick the winner)."""
+    by: dict[tuple[int, int], list[dict]] = {}
+    for r in records:
+        if r["status"] == 0:
+            by.setdefault((r["job"], r["layer"]), []).append(r)
+    return {key: sorted(v, key=lambda r: (r["median_us"], r["space_index"]))[:k] for key, v in by.items()}
+
+
+def gpu_busy_us(records: list[dict], warmup: int = 3) -> float:
+    """Kernel time a tuning pass spent on the GPU for these records: per
+    candidate, the gate launch + warm-ups + groups x n timed launches, each
+    at the candidate's median latency (SURVEY 8(d) "GPU-busy fraction")."""
+    return sum((1 + warmup + r["groups"] * r["n_per_group"]) * r["median_us"] for r in records if r["status"] == 0)

@@ -14,7 +14,8 @@ from paper_2008_03602_b200 import shard
 def _fake_records(n, seed):
     rng = random.Random(seed)
     return [dict(space_index=i, status=rng.choice([0, 0, 0, 5]), median_us=rng.choice([1.0, 1.5, 2.0, 2.5]),
-                 min_us=0.9, mean_us=1.0, std_us=0.1, sm_granted=148, ctas=10, threads_per_cta=128, waves=1)
+                 min_us=0.9, mean_us=1.0, std_us=0.1, sm_granted=148, ctas=10, threads_per_cta=128, waves=1,
+                 n_per_group=10, groups=rng.choice([1, 5]))
             for i in range(n)]
 
 
@@ -71,3 +72,22 @@ def test_gloo_gather_world2():
     n, merged_idx, single_idx = q.get(timeout=5)
     assert n == 101
     assert merged_idx == single_idx
+
+
+def test_finalists_top3_sorted_and_ok_only():
+    recs = [dict(r, job=0, layer=r["space_index"] % 2) for r in _fake_records(200, 3)]
+    fin = shard.finalists(recs, 3)
+    for key, top in fin.items():
+        assert len(top) == 3 and all(r["status"] == 0 for r in top)
+        ok = sorted((r for r in recs if (r["job"], r["layer"]) == key and r["status"] == 0),
+                    key=lambda r: (r["median_us"], r["space_index"]))
+        assert [r["space_index"] for r in top] == [r["space_index"] for r in ok[:3]]
+        assert top[0]["space_index"] == shard.merge_best(recs)[key]["space_index"]
+
+
+def test_gpu_busy_counts_gate_warmup_and_groups():
+    recs = [dict(status=0, median_us=2.0, n_per_group=10, groups=5), dict(status=0, median_us=4.0, n_per_group=10,
+                                                                           groups=1),
+            dict(status=5, median_us=1.0, n_per_group=0, groups=0)]
+    # (1 + 3 + 50) * 2 + (1 + 3 + 10) * 4
+    assert shard.gpu_busy_us(recs) == 54 * 2.0 + 14 * 4.0
