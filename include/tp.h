@@ -63,7 +63,14 @@ enum { TP_EPI_BIAS = 1, TP_EPI_RELU = 2 };
  * (fp32, depthwise); IGEMM_TC_GATHER = tcgen05 implicit GEMM whose A/B tiles
  * are gathered into shared memory by CUDA-core warps over the flattened
  * (r, s, c) axis (bf16, g = 1, C % 8 != 0: the C = 3 stems). */
-enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2 };
+enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2, TP_KIND_IGEMM_TC_ROW = 3 };
+/* IGEMM_TC_ROW ("row-halo"): an extra schedule kind appended to the space of
+ * IGEMM_TC layers with 3x3 filters, stride 1, pad 1, C % 64 == 0 and Q >= 56.
+ * A tile is BM pixels of one output row; per (64-channel block, filter row)
+ * one TMA loads the BM+2-pixel input strip once and the MMA reads the three
+ * taps as the strip shifted by 0/1/2 pixels (the im2col A tile is never
+ * re-fetched per tap).  Knobs BM, BN, stages, threads; BK = 64, split_k = 1;
+ * grid = (N*P*ceil(Q/BM), ceil(K/BN), 1). */
 
 /* One conv2d operator ("tuning task", P:947 [src]).  P/Q follow reading C3:
  * P = floor((h + 2 pad_h - dil_h (r-1) - 1) / stride_h) + 1; P < 1 -> TP_EINVAL. */

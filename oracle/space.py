@@ -22,12 +22,14 @@ import math
 KIND_IGEMM_TC = 0
 KIND_DIRECT = 1
 KIND_IGEMM_TC_GATHER = 2
+KIND_IGEMM_TC_ROW = 3
 DTYPE_BF16 = 0
 DTYPE_FP32 = 1
 SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
 
 TC_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("bk", (16, 32, 64, 128)),
             ("stages", (2, 3, 4, 6)), ("threads", (128, 256)), ("split_k", (1, 2, 4, 8)))
+ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)), ("threads", (128, 256)))
 DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
                 ("tile_p", (1, 2, 4, 8)), ("smem_stage", (0, 1)))
 
@@ -105,6 +107,24 @@ def _valid_tc_gather(d: dict, bm, bn, bk, stages, threads, split_k) -> bool:
     return split_k <= nkb
 
 
+def row_eligible(d: dict) -> bool:
+    """Row-halo kind: TMA-kind layers with a 3x3 filter,
+    stride 1, pad 1, C a multiple of 64 and output rows at least 56 wide."""
+    P, Q = out_pq(d)
+    return (layer_kind(d) == KIND_IGEMM_TC and d["r"] == 3 and d["s"] == 3 and d["stride_h"] == 1
+            and d["stride_w"] == 1 and d["pad_h"] == 1 and d["pad_w"] == 1 and d["c"] % 64 == 0 and Q >= 56)
+
+
+def _valid_row(d: dict, bm, bn, stages, threads) -> bool:
+    """Stage = input strip of bm+2 pixels x 128 B (rounded up to 1 KiB) + the
+    three taps' bn x 64-channel weight tiles."""
+    P, Q = out_pq(d)
+    strip = -(-((bm + 2) * 128) // 1024) * 1024
+    if stages * (strip + 3 * bn * 128) + 1024 > SMEM_LIMIT:
+        return False
+    return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))
+
+
 def _valid_direct(d: dict, threads, tile_q, vec_k, tile_p, smem_stage) -> bool:
     P, Q = out_pq(d)
     if tile_q > Q or tile_p > P or vec_k > d["k"]:
@@ -131,13 +151,22 @@ def enumerate_space(d: dict) -> list[dict]:
             s["space_index"] = len(out)
             s.update(geometry(d, s))
             out.append(s)
+    if row_eligible(d):          # appended after every TMA-kind tuple; bk = 64, split_k = 1
+        for combo in itertools.product(*[v for _, v in ROW_KNOBS]):
+            if _valid_row(d, *combo):
+                s = dict(zip([k for k, _ in ROW_KNOBS], combo), bk=64, split_k=1, kind=KIND_IGEMM_TC_ROW,
+                         space_index=len(out))
+                s.update(geometry(d, s))
+                out.append(s)
     return out
 
 
 def geometry(d: dict, s: dict) -> dict:
     """Frozen launch geometry of a schedule (grid, threads per CTA)."""
     P, Q = out_pq(d)
-    if s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER):
+    if s.get("kind") == KIND_IGEMM_TC_ROW:
+        g = (d["n"] * P * _cdiv(Q, s["bm"]), _cdiv(d["k"], s["bn"]), 1)
+    elif s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER):
         M = d["n"] * P * Q
         g = (_cdiv(M, s["bm"]), _cdiv(d["k"], s["bn"]), s["split_k"])
     else:

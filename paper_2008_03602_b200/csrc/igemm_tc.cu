@@ -239,15 +239,25 @@ __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long l
 //   element by element into the same swizzled K-major shared-memory layout the
 //   TMA would produce (the C = 3 stems, where a pixel row is 6 bytes and
 //   neither TMA mode applies).
-template <int BM, int BN, int BK, bool GATHER>
+// MODE = 2 (row-halo, TP_KIND_IGEMM_TC_ROW; BK = 64): the tile is BM pixels of
+//   one output row; a k-block is (64-channel block, filter row r): one tiled
+//   TMA box brings the BM+2-pixel input strip (padding = out-of-bounds zero
+//   fill) and three boxes the taps' weight tiles; the MMA reads tap s as the
+//   strip shifted by s rows of 128 B (descriptor start address + s*128).
+template <int BM, int BN, int BK, int MODE>
 __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+  constexpr bool GATHER = MODE == 1, ROW = MODE == 2;
+  static_assert(!ROW || BK == 64, "row-halo tiles use 64-channel k-blocks");
   // Compile-time tile geometry: one swizzle row holds SUBK channels (32/64/128 B).
   constexpr int SUBK = BK < 64 ? BK : 64;
   constexpr int NSUB = BK / SUBK;
   constexpr uint32_t SWZ = SUBK * 2;
   constexpr uint32_t A_SUB = BM * SUBK * 2, B_SUB = BN * SUBK * 2;
-  constexpr uint32_t A_STAGE = A_SUB * NSUB, B_STAGE = B_SUB * NSUB;
+  // Row-halo stage: input strip (BM+2 rows of 128 B, padded to 1 KiB) + 3 taps' weights.
+  constexpr uint32_t A_STRIP = ((BM + 2) * 128 + 1023) / 1024 * 1024;
+  constexpr uint32_t A_STAGE = ROW ? A_STRIP : A_SUB * NSUB;
+  constexpr uint32_t B_STAGE = ROW ? 3 * B_SUB : B_SUB * NSUB;
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);   // bf16 x bf16 -> f32, K-major A and B
@@ -291,11 +301,22 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   const int nkb = kb1 - kb0;
 
   // Output-pixel origin of this M tile -> im2col base coordinate (lower corner = -pad).
-  const int m0 = m_tile * BM;
-  const int q0 = m0 % a.Q;
-  const int t0 = m0 / a.Q;
-  const int p0 = t0 % a.P;
-  const int n0 = t0 / a.P;
+  // Row-halo: blockIdx.x = (n * P + p) * ceil(Q / BM) + q-block; rows past Q are masked.
+  int m0, q0, p0, n0, mvalid = BM;
+  if constexpr (ROW) {
+    const int qb = m_tile % a.nqb, t = m_tile / a.nqb;
+    q0 = qb * BM;
+    p0 = t % a.P;
+    n0 = t / a.P;
+    m0 = t * a.Q + q0;
+    mvalid = a.Q - q0 < BM ? a.Q - q0 : BM;
+  } else {
+    m0 = m_tile * BM;
+    q0 = m0 % a.Q;
+    const int t0 = m0 / a.Q;
+    p0 = t0 % a.P;
+    n0 = t0 / a.P;
+  }
   const int cw = q0 * a.sw - a.pw, ch = p0 * a.sh - a.ph;
   const int nbase = n_tile * BN;
 
@@ -306,6 +327,19 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   auto produce = [&](uint32_t lead) {
     uint8_t* sa = a_tiles + (size_t)p_stage * A_STAGE;
     uint8_t* sbp = b_tiles + (size_t)p_stage * B_STAGE;
+    if constexpr (ROW) {
+      // k-block = (channel block p_cb, filter row p_r): strip + the three taps.
+      mbar_arrive_expect_tx_p(full + p_stage, (uint32_t)((BM + 2) * 128) + B_STAGE, lead);
+      const int c0 = p_cb * 64;
+      tma_load_tile_4d_p(sa, &tmA, full + p_stage, c0, q0 - 1, p0 + p_r - 1, n0, lead);
+#pragma unroll
+      for (int ss = 0; ss < 3; ++ss)
+        tma_load_tile_4d_p(sbp + ss * B_SUB, &tmB, full + p_stage, c0, ss, p_r, nbase, lead);
+      if (++p_r == 3) { p_r = 0; ++p_cb; }
+      if (++p_stage == stages) { p_stage = 0; p_phase ^= 1u; }
+      ++p_kb;
+      return;
+    }
     mbar_arrive_expect_tx_p(full + p_stage, ((a.dbg & 1) ? 0u : A_STAGE) + ((a.dbg & 2) ? 0u : B_STAGE), lead);
     const int c0 = p_cb * BK;
 #pragma unroll
@@ -345,10 +379,15 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     __syncwarp();
     if constexpr (!GATHER) {
       const uint32_t lead = elect_one();
-      const int rs = kb0 / a.cblocks;
-      p_cb = kb0 - rs * a.cblocks;
-      p_s = rs % a.S;
-      p_r = rs / a.S;
+      if constexpr (ROW) {
+        p_cb = kb0 / 3;
+        p_r = kb0 - p_cb * 3;
+      } else {
+        const int rs = kb0 / a.cblocks;
+        p_cb = kb0 - rs * a.cblocks;
+        p_s = rs % a.S;
+        p_r = rs / a.S;
+      }
       // Wait for the previous grid (PDL), then fill the whole ring before the
       // CTA-wide sync so the first loads overlap the TMEM allocation.
       asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -503,12 +542,26 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       tc_fence_after();
       if (trace && lane == 0 && kb - kb0 < kTraceK) trace[4 + kb - kb0] = gtimer();
       const uint64_t ad = adesc0 + soff_a, bd = bdesc0 + soff_b;
+      if constexpr (ROW) {
+        // Tap s reads the strip from row s: start address + s*128 B.  The
+        // 128-B swizzle is applied on absolute address bits [7:9] (the phase
+        // the TMA wrote), so the descriptor's base-offset field stays 0 --
+        // measured: a base offset of s corrupts every tap s > 0.
 #pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk) {
-        constexpr int kPerSub = SUBK / 16;
-        const uint32_t sb = kk / kPerSub, koff = (kk % kPerSub) * 32;   // compile-time after unroll
-        tc_mma_p(tmem_base, ad + ((sb * A_SUB + koff) >> 4), bd + ((sb * B_SUB + koff) >> 4), IDESC,
-                 (kb > kb0 || kk > 0) ? 1u : 0u, lead);
+        for (int ss = 0; ss < 3; ++ss)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_p(tmem_base, ad + ((uint32_t)(ss * 128 + kk * 32) >> 4),
+                     bd + ((uint32_t)(ss * B_SUB + kk * 32) >> 4), IDESC, (kb > kb0 || ss > 0 || kk > 0) ? 1u : 0u,
+                     lead);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          constexpr int kPerSub = SUBK / 16;
+          const uint32_t sb = kk / kPerSub, koff = (kk % kPerSub) * 32;   // compile-time after unroll
+          tc_mma_p(tmem_base, ad + ((sb * A_SUB + koff) >> 4), bd + ((sb * B_SUB + koff) >> 4), IDESC,
+                   (kb > kb0 || kk > 0) ? 1u : 0u, lead);
+        }
       }
       tc_commit_p(empty + stage, lead);
       if (trace && lane == 0 && kb - kb0 < kTraceK) trace[36 + kb - kb0] = gtimer();
@@ -526,7 +579,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   const int row = (BM == 128) ? quad * 32 + lane : quad * 16 + lane;
   const bool row_ok = (BM == 128 || lane < 16);
   const int64_t m = m0 + row;
-  const bool m_ok = row_ok && m < a.M;
+  const bool m_ok = row_ok && row < mvalid && m < a.M;
   const int64_t tile = (int64_t)m_tile * gridDim.y + n_tile;
   const int64_t n_tiles = (int64_t)gridDim.x * gridDim.y;
 
@@ -690,20 +743,25 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 // ------------------------------------------------------------- host side
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
 
-template <int BM, int BN, bool G>
+template <int BM, int BN, int MODE>
 static KernelFn pick_bk(int bk) {
-  switch (bk) {
-    case 16: return igemm_tc_kernel<BM, BN, 16, G>;
-    case 32: return igemm_tc_kernel<BM, BN, 32, G>;
-    case 64: return igemm_tc_kernel<BM, BN, 64, G>;
-    case 128: return igemm_tc_kernel<BM, BN, 128, G>;
+  if constexpr (MODE == 2) {
+    return bk == 64 ? igemm_tc_kernel<BM, BN, 64, 2> : nullptr;
+  } else {
+    switch (bk) {
+      case 16: return igemm_tc_kernel<BM, BN, 16, MODE>;
+      case 32: return igemm_tc_kernel<BM, BN, 32, MODE>;
+      case 64: return igemm_tc_kernel<BM, BN, 64, MODE>;
+      case 128: return igemm_tc_kernel<BM, BN, 128, MODE>;
+    }
   }
   return nullptr;
 }
 
-static KernelFn pick_tc(int bm, int bn, int bk, bool gather) {
-#define TP_TC_CASE(M_, N_) \
-  if (bm == M_ && bn == N_) return gather ? pick_bk<M_, N_, true>(bk) : pick_bk<M_, N_, false>(bk);
+static KernelFn pick_tc(int bm, int bn, int bk, int mode) {
+#define TP_TC_CASE(M_, N_)                                                                       \
+  if (bm == M_ && bn == N_)                                                                      \
+    return mode == 2 ? pick_bk<M_, N_, 2>(bk) : (mode == 1 ? pick_bk<M_, N_, 1>(bk) : pick_bk<M_, N_, 0>(bk));
   TP_TC_CASE(64, 32) TP_TC_CASE(64, 64) TP_TC_CASE(64, 128) TP_TC_CASE(64, 256)
   TP_TC_CASE(128, 32) TP_TC_CASE(128, 64) TP_TC_CASE(128, 128) TP_TC_CASE(128, 256)
 #undef TP_TC_CASE
@@ -717,9 +775,12 @@ size_t tc_dyn_smem(int bm, int bn, int bk, int stages) {
 // Shared-memory layout: [ring] [split-K receive buffer (cluster path)] [barriers, 1 KiB].
 // The receive buffer must not alias the ring: peers push their slices while
 // this CTA may still be in its mainloop.
-static size_t tc_ring_bytes(int bm, int bn, int bk, int stages) { return (size_t)stages * (bm + bn) * bk * 2; }
-static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red) {
-  size_t off = tc_ring_bytes(bm, bn, bk, stages);
+static size_t tc_ring_bytes(int bm, int bn, int bk, int stages, bool row) {
+  if (row) return (size_t)stages * ((((size_t)(bm + 2) * 128) + 1023) / 1024 * 1024 + 3 * (size_t)bn * 128);
+  return (size_t)stages * (bm + bn) * bk * 2;
+}
+static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red, bool row) {
+  size_t off = tc_ring_bytes(bm, bn, bk, stages, row);
   if (cluster_red) off += (size_t)bm * (bn + 4) * 4;
   return (off + 1023) & ~(size_t)1023;
 }
@@ -735,6 +796,31 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     // Gathered kind: no tensor maps (the kernel never touches tmA / tmB).
     std::memset(&plan->tmA, 0, sizeof(plan->tmA));
     std::memset(&plan->tmB, 0, sizeof(plan->tmB));
+  } else if (pb.row) {
+    // Row-halo kind: A = tiled map over NHWC x, box (64 channels, BM+2 pixels,
+    // 1 row, 1 image), 128-B swizzle; out-of-bounds pixels/rows are zero (pad 1).
+    cuuint64_t dims[4] = {(cuuint64_t)pb.C, (cuuint64_t)pb.W, (cuuint64_t)pb.H, (cuuint64_t)pb.N};
+    cuuint64_t strides[3] = {(cuuint64_t)pb.C * 2, (cuuint64_t)pb.W * pb.C * 2, (cuuint64_t)pb.H * pb.W * pb.C * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)(pb.bm + 2), 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = drv.encodeTiled(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.x), dims,
+                                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (row strip) failed (" + std::to_string((int)r) + ")");
+      return TP_ECUDA;
+    }
+    cuuint64_t b_dims[4] = {(cuuint64_t)pb.C, (cuuint64_t)pb.S, (cuuint64_t)pb.R, (cuuint64_t)pb.K};
+    cuuint64_t b_strides[3] = {(cuuint64_t)pb.C * 2, (cuuint64_t)pb.S * pb.C * 2,
+                               (cuuint64_t)pb.R * pb.S * pb.C * 2};
+    cuuint32_t b_box[4] = {64, 1, 1, (cuuint32_t)pb.bn};
+    r = drv.encodeTiled(&plan->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.w), b_dims, b_strides,
+                        b_box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (row weights) failed (" + std::to_string((int)r) + ")");
+      return TP_ECUDA;
+    }
   } else {
   const CUtensorMapSwizzle swz = sub_k == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
                                              : (sub_k == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
@@ -774,6 +860,11 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.xg = pb.x; a.wg = pb.w;
   a.H = pb.H; a.W = pb.W; a.C = pb.C; a.Kg = pb.R * pb.S * pb.C;
   if (pb.gather) a.kblocks = (a.Kg + pb.bk - 1) / pb.bk;
+  a.nqb = 1;
+  if (pb.row) {
+    a.kblocks = (pb.C / 64) * 3;
+    a.nqb = (pb.Q + pb.bm - 1) / pb.bm;
+  }
   a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
   a.ws_partial = pb.ws_partial; a.ws_counters = pb.ws_counters;
   a.trace = pb.trace;
@@ -781,10 +872,11 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     static const int dbg = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
     a.dbg = dbg;
   }
-  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.gather != 0));
+  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.row ? 2 : (pb.gather ? 1 : 0)));
   if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN x BK"); return TP_EINVALID_CONFIG; }
-  plan->grid = dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn),
-                    (unsigned)pb.split_k);
+  plan->grid = pb.row ? dim3((unsigned)(pb.N * pb.P * a.nqb), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u)
+                      : dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn),
+                             (unsigned)pb.split_k);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
   plan->block = dim3(pb.threads);
   // Split-K reduces through DSMEM inside a (1, 1, split_k) cluster when the
@@ -794,15 +886,15 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   plan->cluster_z = 1;
   if (pb.split_k > 1 && plan->grid.z % (unsigned)pb.split_k == 0 && !getenv("TP_NO_CLUSTER")) {
     const size_t tabs = pb.gather ? (size_t)pb.bm * 16 + (size_t)a.kblocks * pb.bk * 8 : 0;
-    const size_t smem_c = tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, true) + 1024 + tabs;
+    const size_t smem_c = tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, true, pb.row != 0) + 1024 + tabs;
     if (smem_c <= 232448 && ensure_smem_attr(plan->fn, smem_c) == cudaSuccess &&
         cached_max_clusters(plan->fn, plan->block.x, smem_c, pb.split_k) > 0) {
       a.cluster_red = 1;
       plan->cluster_z = pb.split_k;
     }
   }
-  a.bar_off = (int)tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, a.cluster_red != 0);
-  a.recv_off = (int)tc_ring_bytes(pb.bm, pb.bn, pb.bk, pb.stages);
+  a.bar_off = (int)tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, a.cluster_red != 0, pb.row != 0);
+  a.recv_off = (int)tc_ring_bytes(pb.bm, pb.bn, pb.bk, pb.stages, pb.row != 0);
   a.tab_off = a.bar_off + 1024;
   plan->smem = (size_t)a.tab_off + (pb.gather ? (size_t)pb.bm * 16 + (size_t)a.kblocks * pb.bk * 8 : 0);
   cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);

@@ -361,7 +361,7 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     yk = plan->y_nhwc;
     plan->kernels_per_call = 3;
   }
-  if (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) {
+  if (s.kind != TP_KIND_DIRECT) {
     if ((reinterpret_cast<uintptr_t>(xk) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(yk)) & 15) {
       set_error("x, w, y must be 16-byte aligned for the tensor-core path");
       return TP_EINVAL;
@@ -380,6 +380,7 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     pb.ws_counters = s.split_k > 1 ? reinterpret_cast<int*>(wsb + wl.counters) : nullptr;
     pb.ws_partial = s.split_k > 1 ? reinterpret_cast<float*>(wsb + wl.partials) : nullptr;
     pb.gather = s.kind == TP_KIND_IGEMM_TC_GATHER ? 1 : 0;
+    pb.row = s.kind == TP_KIND_IGEMM_TC_ROW ? 1 : 0;
     tp_status st = tc_prepare(pb, &plan->tc);
     if (st != TP_OK) return st;
     plan->ctas_per_sm = tc_occupancy(plan->tc);

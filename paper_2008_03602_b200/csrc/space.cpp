@@ -132,8 +132,34 @@ static bool valid_direct(const Layer& L, int threads, int tq, int vk, int tpp, i
   return true;
 }
 
+// Row-halo kind (3x3, stride 1, pad 1, C % 64 == 0, Q >= 56): an output tile
+// is BM pixels of ONE output row; per (64-channel block, filter row r) the
+// producer loads one input-row strip of BM+2 pixels and the three taps'
+// weight tiles, and the MMA reads the three taps as strips shifted by s.
+bool row_kind_eligible(const Layer& L) {
+  const tp_conv_desc& d = L.d;
+  return L.kind == TP_KIND_IGEMM_TC && d.r == 3 && d.s == 3 && d.stride_h == 1 && d.stride_w == 1 &&
+         d.pad_h == 1 && d.pad_w == 1 && d.c % 64 == 0 && L.Q >= 56;
+}
+int64_t row_stage_bytes(int bm, int bn) {
+  const int64_t strip = (((int64_t)(bm + 2) * 128) + 1023) / 1024 * 1024;
+  return strip + 3 * (int64_t)bn * 128;
+}
+static const int kRowBM[] = {64, 128};
+static const int kRowStages[] = {1, 2, 3};
+
+static bool valid_row(const Layer& L, int bm, int bn, int stages) {
+  if ((int64_t)stages * row_stage_bytes(bm, bn) + 1024 > kSmemLimit) return false;
+  if (bm > np2(L.Q)) return false;
+  return bn <= std::max<int64_t>(32, np2(L.d.k));
+}
+
 void fill_geometry(const Layer& L, tp_schedule* s) {
-  if (s->kind == TP_KIND_IGEMM_TC || s->kind == TP_KIND_IGEMM_TC_GATHER) {
+  if (s->kind == TP_KIND_IGEMM_TC_ROW) {
+    s->grid_x = (int32_t)((int64_t)L.d.n * L.P * cdiv(L.Q, s->bm));
+    s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
+    s->grid_z = 1;
+  } else if (s->kind == TP_KIND_IGEMM_TC || s->kind == TP_KIND_IGEMM_TC_GATHER) {
     s->grid_x = (int32_t)cdiv(L.M, s->bm);
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = s->split_k;
@@ -157,6 +183,16 @@ static void enumerate(const Layer& L, F visit) {
         tp_schedule s; std::memset(&s, 0, sizeof(s));
         s.kind = L.kind; s.bm = bm; s.bn = bn; s.bk = bk; s.stages = st;
         s.threads = th; s.split_k = sk; s.space_index = idx++;
+        if (!visit(s)) return;
+      }
+    // Eligible layers append the row-halo kind after every TMA-kind tuple
+    // (BK is fixed at 64, split_k at 1).
+    if (row_kind_eligible(L))
+      for (int bm : kRowBM) for (int bn : kTcBN) for (int st : kRowStages) for (int th : kTcThreads) {
+        if (!valid_row(L, bm, bn, st)) continue;
+        tp_schedule s; std::memset(&s, 0, sizeof(s));
+        s.kind = TP_KIND_IGEMM_TC_ROW; s.bm = bm; s.bn = bn; s.bk = 64; s.stages = st;
+        s.threads = th; s.split_k = 1; s.space_index = idx++;
         if (!visit(s)) return;
       }
   } else {
@@ -188,6 +224,11 @@ bool space_get(const Layer& L, int64_t idx, tp_schedule* out) {
 }
 
 bool schedule_in_space(const Layer& L, const tp_schedule& s) {
+  auto in_ = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };
+  if (s.kind == TP_KIND_IGEMM_TC_ROW)
+    return row_kind_eligible(L) && in_(s.bm, kRowBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 64 &&
+           in_(s.stages, kRowStages, 3) && in_(s.threads, kTcThreads, 2) && s.split_k == 1 &&
+           valid_row(L, s.bm, s.bn, s.stages);
   if (s.kind != L.kind) return false;
   if (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) {
     auto in = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };

@@ -47,6 +47,9 @@ def mk(n, c, h, w, k, r, s, st=1, pad=0, g=1, dtype=tp.BF16, out=None, epi=3, la
 TC_TINY = [mk(1, 64, 10, 9, 64, 3, 3, 1, 1, out=tp.FP32, epi=1),
            mk(2, 32, 7, 7, 48, 1, 1, 1, 0, out=tp.FP32, epi=1),
            mk(1, 136, 9, 11, 40, 3, 3, 2, 1, out=tp.FP32, epi=1),
+           # row-halo kind appended (3x3 s1 p1, C % 64 == 0, Q >= 56): ragged rows, 2 channel blocks, N = 2
+           mk(1, 64, 6, 60, 40, 3, 3, 1, 1, out=tp.FP32, epi=1),
+           mk(2, 128, 4, 57, 24, 3, 3, 1, 1, out=tp.FP32, epi=1),
            # gathered kind (C % 8 != 0): the ResNet/VGG/MobileNet stems, ragged M tails
            mk(1, 3, 23, 21, 64, 7, 7, 2, 3, out=tp.FP32, epi=1),
            mk(2, 3, 9, 10, 24, 3, 3, 1, 1, out=tp.FP32, epi=1),

@@ -50,11 +50,12 @@ def test_space_counts_and_order():
         stems = [d for d in cat if sp.layer_kind(d) == sp.KIND_IGEMM_TC_GATHER]
         rest = [d for d in cat if sp.layer_kind(d) != sp.KIND_IGEMM_TC_GATHER]
         assert len(stems) == 1 and stems[0]["c"] == 3
-        assert sum(len(sp.enumerate_space(d)) for d in rest) + _direct_count(stems[0]) == total
+        n_rest = sum(1 for d in rest for x in sp.enumerate_space(d) if x["kind"] != sp.KIND_IGEMM_TC_ROW)
+        assert n_rest + _direct_count(stems[0]) == total
     d = wl.catalog("resnet50")[2]
     s = sp.enumerate_space(d)
-    keys = [(x["bm"], x["bn"], x["bk"], x["stages"], x["threads"], x["split_k"]) for x in s]
-    assert keys == sorted(keys)
+    keys = [(x["kind"], x["bm"], x["bn"], x["bk"], x["stages"], x["threads"], x["split_k"]) for x in s]
+    assert keys == sorted(keys)      # kind is the outermost key (row-halo tuples follow the TMA ones)
     assert [x["space_index"] for x in s] == list(range(len(s)))
 
 
@@ -74,6 +75,24 @@ def test_gather_space_hand_count():
     d = wl.catalog("resnet50")[0]
     assert len(sp.enumerate_space(d)) == n
     assert all(s["kind"] == sp.KIND_IGEMM_TC_GATHER for s in sp.enumerate_space(d))
+
+
+def test_row_kind_hand_count_and_order():
+    # VGG conv1_2 (C=64, 224x224, K=64, 3x3 s1 p1): eligible.  BM in {64, 128}
+    # (np2(Q) = 256), BN in {32, 64} (np2(K) = 64), stages {1, 2, 3}, threads {128, 256};
+    # largest stage = 17408 (strip 130 x 128 B -> 1 KiB multiple) + 3 x 64 x 128 = 41984 B,
+    # x 3 stages + 1024 fits, so all 2 x 2 x 3 x 2 = 24 tuples are valid.
+    d = wl.catalog("vgg19_b16")[1]
+    space = sp.enumerate_space(d)
+    row = [x for x in space if x["kind"] == sp.KIND_IGEMM_TC_ROW]
+    assert len(row) == 24
+    first = space.index(row[0])
+    assert all(x["kind"] == sp.KIND_IGEMM_TC for x in space[:first]) and space[first:] == row
+    assert all(x["bk"] == 64 and x["split_k"] == 1 for x in row)
+    assert row[0]["grid_x"] == 16 * 224 * 4 and row[0]["grid_y"] == 2          # BM=64, BN=32
+    # not eligible: stride 2, pad 0, C % 64 != 0, Q < 56
+    r50 = wl.catalog("resnet50")
+    assert [sp.row_eligible(x) for x in r50].count(True) == 1 and sp.row_eligible(r50[2])   # l1.b0.c2 only
 
 
 def test_kind_selection():
@@ -116,7 +135,7 @@ def test_libtp_space_matches_mirror(d):
     for m in mirror:
         s = tp.space_get(d, m["space_index"])
         assert s["kind"] == m["kind"]
-        for f in (fields_dir if m["kind"] == sp.KIND_DIRECT else fields_tc):
+        for f in (fields_dir if m["kind"] == sp.KIND_DIRECT else fields_tc + ("kind",)):
             assert s[f] == m[f], (f, m)
         assert (s["grid_x"], s["grid_y"], s["grid_z"]) == (m["grid_x"], m["grid_y"], m["grid_z"])
         assert s["space_index"] == m["space_index"]

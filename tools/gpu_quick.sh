@@ -1,2 +1,4 @@
-python tools/trace_sched.py resnet50 r50.conv1 64 32 32 3 256 1 2>&1
-python tools/trace_sched.py vgg19_b16 vgg.64.224.0 128 64 16 2 128 1 0.25 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "every_schedule" 2>&1 | tail -2
+KIND=3 python tools/trace_sched.py vgg19_b16 vgg.64.224.1 128 64 64 1 256 1 0.25
+KIND=3 python tools/trace_sched.py vgg19_b16 vgg.64.224.1 128 64 64 1 128 1 0.25
+KIND=3 python tools/trace_sched.py vgg19_b16 vgg.128.112.0 128 128 64 1 256 1 0.25

@@ -11,6 +11,9 @@ ov = dict(zip(("bm", "bn", "bk", "stages", "threads", "split_k"), map(int, sys.a
 part = tp.Partition.get(float(sys.argv[9]) if len(sys.argv) > 9 else 1.0)
 x, w, b = datagen.make_inputs(d, datagen.data_seed(2, li))
 buf = tp.LayerBuffers(d, x, w, b, part=part)
+import os
+if os.environ.get("KIND"):
+    ov["kind"] = int(os.environ["KIND"])
 s = next(tp.space_get(d, i) for i in range(tp.space_size(d)) if all(tp.space_get(d, i)[k] == v for k, v in ov.items()))
 m = tp.conv2d_run(buf, s, part, tp.timing())
 tr = tp.conv2d_trace(buf, s, part).astype(np.int64)
