@@ -118,9 +118,12 @@ typedef struct {
     int32_t flush_l2;         /* 1: write a > L2 buffer before every launch (cold L2) */
     double prune_ratio;       /* tuner only (reading C12b): a candidate whose gate-run time
                                  exceeds prune_ratio x the fastest gate-run time of the same
-                                 tp_tune / tp_tune_subset call is timed with ONE group of n
-                                 launches instead of `groups` (its record says groups = 1);
-                                 0 = every candidate gets `groups`.  Default 2.0.           */
+                                 tp_tune / tp_tune_subset call is "raced": one warm-up and ONE
+                                 group of n = max(min(3, n_min), ceil(target / t_est))
+                                 launches (its record says groups = 1); a raced candidate that
+                                 beats every fully-timed one is re-timed with the full
+                                 protocol.  0 = every candidate gets the full protocol.
+                                 Default 2.0.                                                */
 } tp_timing;
 
 typedef struct tp_partition tp_partition;   /* opaque: green context + stream (or whole device) */

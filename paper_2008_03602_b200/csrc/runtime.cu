@@ -15,7 +15,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -618,17 +620,7 @@ static tp_status gate_check(tp_partition* part, const ConvPlan& plan, Gate* g, t
 
 // ---------------------------------------------------------------- tuner core
 // Enumerate the layer's space once (space_get is O(|space|) per call).
-static std::vector<tp_schedule> space_table(const Layer& L) {
-  std::vector<tp_schedule> t;
-  const int64_t n = space_size(L);
-  t.reserve(n);
-  for (int64_t i = 0; i < n; ++i) {
-    tp_schedule s;
-    space_get(L, i, &s);
-    t.push_back(s);
-  }
-  return t;
-}
+static std::vector<tp_schedule> space_table(const Layer& L) { return space_all(L); }
 
 // Pipelined profiling loop (a10 + a11 for a list of candidates).  No host
 // synchronisation per candidate: phase A enqueues every candidate's gate run
@@ -682,6 +674,9 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       c.m.status = s2;
     }
   } else {
+    // Host-side phase timing (TP_PROFILE=1 prints one line per call to stderr).
+    static const bool prof = getenv("TP_PROFILE") && atoi(getenv("TP_PROFILE")) != 0;
+    const auto tA = std::chrono::steady_clock::now();
     // ---------------- phase A: gate runs, chunked ----------------
     double* d_vals = nullptr;
     TP_CK(cudaMalloc(&d_vals, sizeof(double) * (size_t)std::max(1, ncheck) * kChunk));
@@ -762,6 +757,8 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       return err;
     }
 
+    const auto tB = std::chrono::steady_clock::now();
+    double host_b_us = 0;   // time spent in make/capture/instantiate/enqueue (excl. harvest waits)
     // ---------------- phase B: timing, windowed pipeline ----------------
     // Reading C12b: candidates far slower than the fastest gate run of this
     // call get one timed group (still a warm, graph-timed median of n launches).
@@ -817,10 +814,16 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       }
       c.slot = free_slots.back();
       free_slots.pop_back();
-      c.n = std::min(4096, std::max(std::max(1, tm.n_min), (int)std::ceil(tm.target_group_us / c.t_est)));
-      c.groups = (tm.prune_ratio > 0 && c.t_est > tm.prune_ratio * t_best_est) ? 1 : groups;
+      const auto te0 = std::chrono::steady_clock::now();
+      // C12b: a raced candidate gets one warm-up (the gate launch already ran
+      // it once) and one group of n = max(3, ceil(target / t_est)) launches.
+      const bool raced = tm.prune_ratio > 0 && c.t_est > tm.prune_ratio * t_best_est;
+      const int n_floor = raced ? std::min(3, std::max(1, tm.n_min)) : std::max(1, tm.n_min);
+      c.n = std::min(4096, std::max(n_floor, (int)std::ceil(tm.target_group_us / c.t_est)));
+      c.groups = raced ? 1 : groups;
+      const int warm = raced ? std::min(1, std::max(0, tm.warmup)) : std::max(0, tm.warmup);
       cudaError_t e = cudaSuccess;
-      for (int k = 0; k < std::max(0, tm.warmup) && e == cudaSuccess; ++k) e = launch_plan(c.plan, st);
+      for (int k = 0; k < warm && e == cudaSuccess; ++k) e = launch_plan(c.plan, st);
       if (e == cudaSuccess && tm.use_graph) {
         cudaGraph_t graph = nullptr;
         e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
@@ -858,10 +861,19 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         continue;
       }
       inflight.push_back(i);
+      host_b_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - te0).count();
     }
     for (int32_t i : inflight) {
       tp_status h = harvest(i);
       if (err == TP_OK) err = h;
+    }
+    const auto tC = std::chrono::steady_clock::now();
+    if (prof) {
+      auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::micro>(b - a).count();
+      };
+      fprintf(stderr, "[tp] candidates %d: phase A %.0f us, phase B %.0f us (host enqueue %.0f us)\n", n_cand,
+              us(tA, tB), us(tB, tC), host_b_us);
     }
     // C12b: a raced candidate that beat every fully-timed one is re-timed with
     // the full protocol, so the winner's record is always a full measurement.
@@ -1114,12 +1126,7 @@ tp_status tp_workspace_size_max(const tp_conv_desc* d, size_t* bytes) {
   tp_status st = make_layer(d, &L);
   if (st != TP_OK) return st;
   size_t mx = 0;
-  const int64_t n = space_size(L);
-  for (int64_t i = 0; i < n; ++i) {
-    tp_schedule s;
-    space_get(L, i, &s);
-    mx = std::max(mx, ws_layout(L, s).total);
-  }
+  for (const tp_schedule& s : space_all(L)) mx = std::max(mx, ws_layout(L, s).total);
   *bytes = mx;
   return TP_OK;
 }

@@ -207,6 +207,16 @@ static void enumerate(const Layer& L, F visit) {
   }
 }
 
+std::vector<tp_schedule> space_all(const Layer& L) {
+  std::vector<tp_schedule> out;
+  enumerate(L, [&](const tp_schedule& sc) {
+    out.push_back(sc);
+    fill_geometry(L, &out.back());
+    return true;
+  });
+  return out;
+}
+
 int64_t space_size(const Layer& L) {
   int64_t n = 0;
   enumerate(L, [&](const tp_schedule&) { ++n; return true; });

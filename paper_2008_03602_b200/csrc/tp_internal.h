@@ -3,6 +3,7 @@
 #include <cstdint>
 #include <cstddef>
 #include <string>
+#include <vector>
 #include "../../include/tp.h"
 
 namespace tp {
@@ -28,6 +29,7 @@ int32_t layer_kind(const tp_conv_desc& d);
 // Space (space.cpp).
 int64_t space_size(const Layer& L);
 bool space_get(const Layer& L, int64_t idx, tp_schedule* out);
+std::vector<tp_schedule> space_all(const Layer& L);   // the whole valid space in order, one pass
 void fill_geometry(const Layer& L, tp_schedule* s);
 void direct_lanes(const Layer& L, int threads, int tile_q, int vec_k, int tile_p, int* lanes_k, int* lanes_q);
 int64_t direct_smem_bytes(const Layer& L, int threads, int tile_q, int vec_k, int tile_p);
