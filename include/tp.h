@@ -69,8 +69,10 @@ enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2, TP
  * A tile is BM pixels of one output row; per (64-channel block, filter row)
  * one TMA loads the BM+2-pixel input strip once and the MMA reads the three
  * taps as the strip shifted by 0/1/2 pixels (the im2col A tile is never
- * re-fetched per tap).  Knobs BM, BN, stages, threads; BK = 64, split_k = 1;
- * grid = (N*P*ceil(Q/BM), ceil(K/BN), 1). */
+ * re-fetched per tap).  Knobs BM, BN, stages, threads, tiles_per_cta (a CTA
+ * runs that many consecutive tiles, alternating two TMEM accumulators so one
+ * drains while the other fills; > 1 needs 256 threads); BK = 64, split_k = 1;
+ * grid = (ceil(N*P*ceil(Q/BM) / tiles_per_cta), ceil(K/BN), 1). */
 
 /* One conv2d operator ("tuning task", P:947 [src]).  P/Q follow reading C3:
  * P = floor((h + 2 pad_h - dil_h (r-1) - 1) / stride_h) + 1; P < 1 -> TP_EINVAL. */
@@ -91,7 +93,7 @@ typedef struct {
     int32_t kind;
     int32_t bm, bn, bk, stages, threads, split_k;
     int32_t tile_q, vec_k, tile_p, smem_stage;
-    int32_t reserved;
+    int32_t tiles_per_cta;                     /* IGEMM_TC_ROW: consecutive tiles per CTA (1..16); 0 otherwise */
     int64_t space_index;                       /* rank in the layer's valid space */
     int32_t grid_x, grid_y, grid_z, sm_tuned;  /* frozen geometry; sm_tuned = SMs at tune time */
 } tp_schedule;

@@ -29,7 +29,8 @@ SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
 
 TC_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("bk", (16, 32, 64, 128)),
             ("stages", (2, 3, 4, 6)), ("threads", (128, 256)), ("split_k", (1, 2, 4, 8)))
-ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)), ("threads", (128, 256)))
+ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)), ("threads", (128, 256)),
+             ("tiles_per_cta", (1, 2, 4, 8, 16)))
 DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
                 ("tile_p", (1, 2, 4, 8)), ("smem_stage", (0, 1)))
 
@@ -115,12 +116,15 @@ def row_eligible(d: dict) -> bool:
             and d["stride_w"] == 1 and d["pad_h"] == 1 and d["pad_w"] == 1 and d["c"] % 64 == 0 and Q >= 56)
 
 
-def _valid_row(d: dict, bm, bn, stages, threads) -> bool:
+def _valid_row(d: dict, bm, bn, stages, threads, tiles_per_cta) -> bool:
     """Stage = input strip of bm+2 pixels x 128 B (rounded up to 1 KiB) + the
-    three taps' bn x 64-channel weight tiles."""
+    three taps' bn x 64-channel weight tiles; several tiles per CTA need the
+    256-thread layout (six draining warps)."""
     P, Q = out_pq(d)
     strip = -(-((bm + 2) * 128) // 1024) * 1024
     if stages * (strip + 3 * bn * 128) + 1024 > SMEM_LIMIT:
+        return False
+    if tiles_per_cta > 1 and threads != 256:
         return False
     return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))
 
@@ -165,7 +169,7 @@ def geometry(d: dict, s: dict) -> dict:
     """Frozen launch geometry of a schedule (grid, threads per CTA)."""
     P, Q = out_pq(d)
     if s.get("kind") == KIND_IGEMM_TC_ROW:
-        g = (d["n"] * P * _cdiv(Q, s["bm"]), _cdiv(d["k"], s["bn"]), 1)
+        g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
     elif s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER):
         M = d["n"] * P * Q
         g = (_cdiv(M, s["bm"]), _cdiv(d["k"], s["bn"]), s["split_k"])

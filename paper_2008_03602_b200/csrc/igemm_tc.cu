@@ -239,25 +239,17 @@ __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long l
 //   element by element into the same swizzled K-major shared-memory layout the
 //   TMA would produce (the C = 3 stems, where a pixel row is 6 bytes and
 //   neither TMA mode applies).
-// MODE = 2 (row-halo, TP_KIND_IGEMM_TC_ROW; BK = 64): the tile is BM pixels of
-//   one output row; a k-block is (64-channel block, filter row r): one tiled
-//   TMA box brings the BM+2-pixel input strip (padding = out-of-bounds zero
-//   fill) and three boxes the taps' weight tiles; the MMA reads tap s as the
-//   strip shifted by s rows of 128 B (descriptor start address + s*128).
 template <int BM, int BN, int BK, int MODE>
 __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB, TcArgs a) {
-  constexpr bool GATHER = MODE == 1, ROW = MODE == 2;
-  static_assert(!ROW || BK == 64, "row-halo tiles use 64-channel k-blocks");
+  constexpr bool GATHER = MODE == 1;
+  static_assert(MODE == 0 || MODE == 1, "MODE 2 (row-halo) is igemm_row_kernel");
   // Compile-time tile geometry: one swizzle row holds SUBK channels (32/64/128 B).
   constexpr int SUBK = BK < 64 ? BK : 64;
   constexpr int NSUB = BK / SUBK;
   constexpr uint32_t SWZ = SUBK * 2;
   constexpr uint32_t A_SUB = BM * SUBK * 2, B_SUB = BN * SUBK * 2;
-  // Row-halo stage: input strip (BM+2 rows of 128 B, padded to 1 KiB) + 3 taps' weights.
-  constexpr uint32_t A_STRIP = ((BM + 2) * 128 + 1023) / 1024 * 1024;
-  constexpr uint32_t A_STAGE = ROW ? A_STRIP : A_SUB * NSUB;
-  constexpr uint32_t B_STAGE = ROW ? 3 * B_SUB : B_SUB * NSUB;
+  constexpr uint32_t A_STAGE = A_SUB * NSUB, B_STAGE = B_SUB * NSUB;
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);   // bf16 x bf16 -> f32, K-major A and B
@@ -301,22 +293,11 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   const int nkb = kb1 - kb0;
 
   // Output-pixel origin of this M tile -> im2col base coordinate (lower corner = -pad).
-  // Row-halo: blockIdx.x = (n * P + p) * ceil(Q / BM) + q-block; rows past Q are masked.
-  int m0, q0, p0, n0, mvalid = BM;
-  if constexpr (ROW) {
-    const int qb = m_tile % a.nqb, t = m_tile / a.nqb;
-    q0 = qb * BM;
-    p0 = t % a.P;
-    n0 = t / a.P;
-    m0 = t * a.Q + q0;
-    mvalid = a.Q - q0 < BM ? a.Q - q0 : BM;
-  } else {
-    m0 = m_tile * BM;
-    q0 = m0 % a.Q;
-    const int t0 = m0 / a.Q;
-    p0 = t0 % a.P;
-    n0 = t0 / a.P;
-  }
+  const int m0 = m_tile * BM;
+  const int q0 = m0 % a.Q;
+  const int t0 = m0 / a.Q;
+  const int p0 = t0 % a.P;
+  const int n0 = t0 / a.P;
   const int cw = q0 * a.sw - a.pw, ch = p0 * a.sh - a.ph;
   const int nbase = n_tile * BN;
 
@@ -327,19 +308,6 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   auto produce = [&](uint32_t lead) {
     uint8_t* sa = a_tiles + (size_t)p_stage * A_STAGE;
     uint8_t* sbp = b_tiles + (size_t)p_stage * B_STAGE;
-    if constexpr (ROW) {
-      // k-block = (channel block p_cb, filter row p_r): strip + the three taps.
-      mbar_arrive_expect_tx_p(full + p_stage, (uint32_t)((BM + 2) * 128) + B_STAGE, lead);
-      const int c0 = p_cb * 64;
-      tma_load_tile_4d_p(sa, &tmA, full + p_stage, c0, q0 - 1, p0 + p_r - 1, n0, lead);
-#pragma unroll
-      for (int ss = 0; ss < 3; ++ss)
-        tma_load_tile_4d_p(sbp + ss * B_SUB, &tmB, full + p_stage, c0, ss, p_r, nbase, lead);
-      if (++p_r == 3) { p_r = 0; ++p_cb; }
-      if (++p_stage == stages) { p_stage = 0; p_phase ^= 1u; }
-      ++p_kb;
-      return;
-    }
     mbar_arrive_expect_tx_p(full + p_stage, ((a.dbg & 1) ? 0u : A_STAGE) + ((a.dbg & 2) ? 0u : B_STAGE), lead);
     const int c0 = p_cb * BK;
 #pragma unroll
@@ -379,15 +347,10 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     __syncwarp();
     if constexpr (!GATHER) {
       const uint32_t lead = elect_one();
-      if constexpr (ROW) {
-        p_cb = kb0 / 3;
-        p_r = kb0 - p_cb * 3;
-      } else {
-        const int rs = kb0 / a.cblocks;
-        p_cb = kb0 - rs * a.cblocks;
-        p_s = rs % a.S;
-        p_r = rs / a.S;
-      }
+      const int rs = kb0 / a.cblocks;
+      p_cb = kb0 - rs * a.cblocks;
+      p_s = rs % a.S;
+      p_r = rs / a.S;
       // Wait for the previous grid (PDL), then fill the whole ring before the
       // CTA-wide sync so the first loads overlap the TMEM allocation.
       asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -542,26 +505,12 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       tc_fence_after();
       if (trace && lane == 0 && kb - kb0 < kTraceK) trace[4 + kb - kb0] = gtimer();
       const uint64_t ad = adesc0 + soff_a, bd = bdesc0 + soff_b;
-      if constexpr (ROW) {
-        // Tap s reads the strip from row s: start address + s*128 B.  The
-        // 128-B swizzle is applied on absolute address bits [7:9] (the phase
-        // the TMA wrote), so the descriptor's base-offset field stays 0 --
-        // measured: a base offset of s corrupts every tap s > 0.
 #pragma unroll
-        for (int ss = 0; ss < 3; ++ss)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc_mma_p(tmem_base, ad + ((uint32_t)(ss * 128 + kk * 32) >> 4),
-                     bd + ((uint32_t)(ss * B_SUB + kk * 32) >> 4), IDESC, (kb > kb0 || ss > 0 || kk > 0) ? 1u : 0u,
-                     lead);
-      } else {
-#pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {
-          constexpr int kPerSub = SUBK / 16;
-          const uint32_t sb = kk / kPerSub, koff = (kk % kPerSub) * 32;   // compile-time after unroll
-          tc_mma_p(tmem_base, ad + ((sb * A_SUB + koff) >> 4), bd + ((sb * B_SUB + koff) >> 4), IDESC,
-                   (kb > kb0 || kk > 0) ? 1u : 0u, lead);
-        }
+      for (int kk = 0; kk < BK / 16; ++kk) {
+        constexpr int kPerSub = SUBK / 16;
+        const uint32_t sb = kk / kPerSub, koff = (kk % kPerSub) * 32;   // compile-time after unroll
+        tc_mma_p(tmem_base, ad + ((sb * A_SUB + koff) >> 4), bd + ((sb * B_SUB + koff) >> 4), IDESC,
+                 (kb > kb0 || kk > 0) ? 1u : 0u, lead);
       }
       tc_commit_p(empty + stage, lead);
       if (trace && lane == 0 && kb - kb0 < kTraceK) trace[36 + kb - kb0] = gtimer();
@@ -579,7 +528,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   const int row = (BM == 128) ? quad * 32 + lane : quad * 16 + lane;
   const bool row_ok = (BM == 128 || lane < 16);
   const int64_t m = m0 + row;
-  const bool m_ok = row_ok && row < mvalid && m < a.M;
+  const bool m_ok = row_ok && m < a.M;
   const int64_t tile = (int64_t)m_tile * gridDim.y + n_tile;
   const int64_t n_tiles = (int64_t)gridDim.x * gridDim.y;
 
@@ -740,13 +689,223 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   }
 }
 
+// ------------------------------------------------------------- row-halo kernel
+// TP_KIND_IGEMM_TC_ROW.  A tile is BM pixels of one output row (q0 .. q0+BM-1
+// of row p, image n); a k-block is (64-channel block cb, filter row r): one
+// tiled TMA box brings the input strip of BM+2 pixels (padding = out-of-bounds
+// zero fill) and three boxes bring the taps' BN x 64 weight tiles; the MMA
+// reads tap s as the strip shifted by s rows of 128 B (descriptor start
+// address + s*128; the 128-B swizzle is applied on absolute address bits, so
+// the base-offset field stays 0 -- measured).  Each CTA handles `tpc`
+// consecutive tiles: the producer ring runs across tiles, the MMA alternates
+// between two TMEM accumulators, and (tpc > 1) warps 2..7 drain one
+// accumulator while the MMA fills the other (tmem_full / tmem_empty pairs).
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) igemm_row_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                        const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+  constexpr uint32_t A_STRIP = ((BM + 2) * 128 + 1023) / 1024 * 1024;
+  constexpr uint32_t B_TAP = BN * 128, B_STAGE = 3 * B_TAP;
+  constexpr uint32_t STRIP_BYTES = (BM + 2) * 128;
+  constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(BM >> 4) << 24);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int stages = a.stages;
+  uint8_t* a_tiles = smem_raw;
+  uint8_t* b_tiles = a_tiles + (size_t)stages * A_STRIP;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + a.bar_off);
+  uint64_t* empty = full + stages;
+  uint64_t* tfull = empty + stages;     // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int tpc = a.tpc;
+  const bool split_roles = tpc > 1;     // warps 2..7 drain while warps 0/1 run ahead
+  const int tile0 = blockIdx.x * tpc;
+  const int ntl = a.ntiles - tile0 < tpc ? a.ntiles - tile0 : tpc;
+  const int nbase = blockIdx.y * BN;
+  const int kpt = a.kblocks;            // k-blocks per tile = (C / 64) * 3
+  const uint32_t ncols = (uint32_t)(split_roles ? 2 * BN : BN) <= 32 ? 32u : (uint32_t)(split_roles ? 2 * BN : BN);
+  const int n_epi_warps = split_roles ? 6 : (int)(blockDim.x >> 5);
+  unsigned long long* trace =
+      a.trace ? a.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
+  if (trace && threadIdx.x == 0) {
+    trace[0] = gtimer();
+    unsigned long long g;
+    unsigned sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    trace[63] = g;
+    trace[62] = sm;
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  auto tile_coords = [&](int t, int& q0, int& p0, int& n0, int& mrow0, int& mvalid) {
+    const int qb = t % a.nqb, row = t / a.nqb;
+    q0 = qb * BM;
+    p0 = row % a.P;
+    n0 = row / a.P;
+    mrow0 = row * a.Q + q0;
+    mvalid = a.Q - q0 < BM ? a.Q - q0 : BM;
+  };
+
+  if (warp == 0 && lane == 0) {
+    if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
+    for (int i = 0; i < stages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, (uint32_t)n_epi_warps); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  if (trace && threadIdx.x == 0) trace[1] = gtimer();
+
+  if (warp == 0) {
+    // ---------------- TMA producer: strips + tap weights, ring across tiles ----------------
+    const uint32_t lead = elect_one();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0; i < ntl; ++i) {
+      int q0, p0, n0, mrow0, mvalid;
+      tile_coords(tile0 + i, q0, p0, n0, mrow0, mvalid);
+      int cb = 0, r = 0;
+      for (int kb = 0; kb < kpt; ++kb) {
+        mbar_wait(empty + stage, phase ^ 1u);
+        uint8_t* sa = a_tiles + (size_t)stage * A_STRIP;
+        uint8_t* sb = b_tiles + (size_t)stage * B_STAGE;
+        mbar_arrive_expect_tx_p(full + stage, STRIP_BYTES + B_STAGE, lead);
+        tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
+#pragma unroll
+        for (int ss = 0; ss < 3; ++ss)
+          tma_load_tile_4d_p(sb + ss * B_TAP, &tmB, full + stage, cb * 64, ss, r, nbase, lead);
+        if (++r == 3) { r = 0; ++cb; }
+        if (++stage == stages) { stage = 0; phase ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: two accumulators, alternating per tile ----------------
+    const uint32_t lead = elect_one();
+    const uint64_t adesc0 = make_sdesc(smem_u32(a_tiles), 128);
+    const uint64_t bdesc0 = make_sdesc(smem_u32(b_tiles), 128);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int i = 0; i < ntl; ++i) {
+      const int buf = i & 1;
+      if (i >= 2) {
+        mbar_wait(tempty + buf, (uint32_t)(((i - 2) >> 1) & 1));
+        tc_fence_after();
+      }
+      const uint32_t dcol = tmem_base + (uint32_t)(buf * BN);
+      for (int kb = 0; kb < kpt; ++kb) {
+        mbar_wait(full + stage, phase);
+        tc_fence_after();
+        const uint64_t ad = adesc0 + ((uint32_t)(stage * A_STRIP) >> 4);
+        const uint64_t bd = bdesc0 + ((uint32_t)(stage * B_STAGE) >> 4);
+#pragma unroll
+        for (int ss = 0; ss < 3; ++ss)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_p(dcol, ad + ((uint32_t)(ss * 128 + kk * 32) >> 4), bd + ((uint32_t)(ss * B_TAP + kk * 32) >> 4),
+                     IDESC, (kb > 0 || ss > 0 || kk > 0) ? 1u : 0u, lead);
+        tc_commit_p(empty + stage, lead);
+        if (++stage == stages) { stage = 0; phase ^= 1u; }
+      }
+      tc_commit_p(tfull + buf, lead);
+    }
+  }
+
+  // ---------------- epilogue ----------------
+  if (!split_roles || warp >= 2) {
+    const int quad = warp & 3;
+    int c_begin, c_end;
+    if (split_roles) {               // warps 2..7 -> quadrants 2,3,0,1,2,3
+      const int twin = (quad >= 2) ? 2 : 1;
+      const int half = (warp >= 6) ? 1 : 0;
+      c_begin = half * (BN / twin);
+      c_end = c_begin + BN / twin;
+    } else {
+      const int ngroups = blockDim.x >> 7;
+      c_begin = (warp >> 2) * (BN / ngroups);
+      c_end = c_begin + BN / ngroups;
+    }
+    const int row = (BM == 128) ? quad * 32 + lane : quad * 16 + lane;
+    const bool row_ok = (BM == 128 || lane < 16);
+    for (int i = 0; i < ntl; ++i) {
+      const int buf = i & 1;
+      int q0, p0, n0, mrow0, mvalid;
+      tile_coords(tile0 + i, q0, p0, n0, mrow0, mvalid);
+      float bv[16];
+      const int nb0 = nbase + c_begin;
+#pragma unroll
+      for (int g = 0; g < 16; g += 4) {
+        if (a.has_bias && nb0 + g + 4 <= a.K) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(a.bias + nb0 + g));
+          bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
+        } else {
+          bv[g] = bv[g + 1] = bv[g + 2] = bv[g + 3] = 0.0f;
+        }
+      }
+      __syncwarp();
+      mbar_wait(tfull + buf, (uint32_t)((i >> 1) & 1));
+      tc_fence_after();
+      for (int c = c_begin; c < c_end; c += 16) {
+        uint32_t raw[16];
+        tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + c), raw);
+        const int nb = nbase + c;
+        if (c > c_begin) {
+#pragma unroll
+          for (int g = 0; g < 16; g += 4) {
+            if (a.has_bias && nb + g + 4 <= a.K) {
+              const float4 f = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
+              bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
+            } else {
+              bv[g] = bv[g + 1] = bv[g + 2] = bv[g + 3] = 0.0f;
+            }
+          }
+        }
+        if (row_ok && row < mvalid && nb < a.K) {
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float t = __uint_as_float(raw[j]) + bv[j];
+            v[j] = a.relu ? fmaxf(t, 0.0f) : t;
+          }
+          store16(a.y, (int64_t)mrow0 + row, a.K, nb, v, a.out_f32);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + buf);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (trace && threadIdx.x == 0) trace[3] = gtimer();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols) : "memory");
+  }
+}
+
 // ------------------------------------------------------------- host side
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
 
 template <int BM, int BN, int MODE>
 static KernelFn pick_bk(int bk) {
   if constexpr (MODE == 2) {
-    return bk == 64 ? igemm_tc_kernel<BM, BN, 64, 2> : nullptr;
+    return bk == 64 ? igemm_row_kernel<BM, BN> : nullptr;
   } else {
     switch (bk) {
       case 16: return igemm_tc_kernel<BM, BN, 16, MODE>;
@@ -861,9 +1020,13 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.H = pb.H; a.W = pb.W; a.C = pb.C; a.Kg = pb.R * pb.S * pb.C;
   if (pb.gather) a.kblocks = (a.Kg + pb.bk - 1) / pb.bk;
   a.nqb = 1;
+  a.ntiles = 0;
+  a.tpc = 1;
   if (pb.row) {
     a.kblocks = (pb.C / 64) * 3;
     a.nqb = (pb.Q + pb.bm - 1) / pb.bm;
+    a.ntiles = pb.N * pb.P * a.nqb;
+    a.tpc = pb.tpc > 1 ? pb.tpc : 1;
   }
   a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
   a.ws_partial = pb.ws_partial; a.ws_counters = pb.ws_counters;
@@ -874,7 +1037,7 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   }
   plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.row ? 2 : (pb.gather ? 1 : 0)));
   if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN x BK"); return TP_EINVALID_CONFIG; }
-  plan->grid = pb.row ? dim3((unsigned)(pb.N * pb.P * a.nqb), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u)
+  plan->grid = pb.row ? dim3((unsigned)((a.ntiles + a.tpc - 1) / a.tpc), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u)
                       : dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn),
                              (unsigned)pb.split_k);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);

@@ -383,6 +383,7 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     pb.ws_partial = s.split_k > 1 ? reinterpret_cast<float*>(wsb + wl.partials) : nullptr;
     pb.gather = s.kind == TP_KIND_IGEMM_TC_GATHER ? 1 : 0;
     pb.row = s.kind == TP_KIND_IGEMM_TC_ROW ? 1 : 0;
+    pb.tpc = s.tiles_per_cta;
     tp_status st = tc_prepare(pb, &plan->tc);
     if (st != TP_OK) return st;
     plan->ctas_per_sm = tc_occupancy(plan->tc);

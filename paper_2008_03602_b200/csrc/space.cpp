@@ -147,16 +147,18 @@ int64_t row_stage_bytes(int bm, int bn) {
 }
 static const int kRowBM[] = {64, 128};
 static const int kRowStages[] = {1, 2, 3};
+static const int kRowTpc[] = {1, 2, 4, 8, 16};
 
-static bool valid_row(const Layer& L, int bm, int bn, int stages) {
+static bool valid_row(const Layer& L, int bm, int bn, int stages, int threads, int tpc) {
   if ((int64_t)stages * row_stage_bytes(bm, bn) + 1024 > kSmemLimit) return false;
   if (bm > np2(L.Q)) return false;
+  if (tpc > 1 && threads != 256) return false;   // warps 2..7 drain while warps 0/1 run ahead
   return bn <= std::max<int64_t>(32, np2(L.d.k));
 }
 
 void fill_geometry(const Layer& L, tp_schedule* s) {
   if (s->kind == TP_KIND_IGEMM_TC_ROW) {
-    s->grid_x = (int32_t)((int64_t)L.d.n * L.P * cdiv(L.Q, s->bm));
+    s->grid_x = (int32_t)cdiv((int64_t)L.d.n * L.P * cdiv(L.Q, s->bm), std::max(1, s->tiles_per_cta));
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = 1;
   } else if (s->kind == TP_KIND_IGEMM_TC || s->kind == TP_KIND_IGEMM_TC_GATHER) {
@@ -188,13 +190,14 @@ static void enumerate(const Layer& L, F visit) {
     // Eligible layers append the row-halo kind after every TMA-kind tuple
     // (BK is fixed at 64, split_k at 1).
     if (row_kind_eligible(L))
-      for (int bm : kRowBM) for (int bn : kTcBN) for (int st : kRowStages) for (int th : kTcThreads) {
-        if (!valid_row(L, bm, bn, st)) continue;
-        tp_schedule s; std::memset(&s, 0, sizeof(s));
-        s.kind = TP_KIND_IGEMM_TC_ROW; s.bm = bm; s.bn = bn; s.bk = 64; s.stages = st;
-        s.threads = th; s.split_k = 1; s.space_index = idx++;
-        if (!visit(s)) return;
-      }
+      for (int bm : kRowBM) for (int bn : kTcBN) for (int st : kRowStages) for (int th : kTcThreads)
+        for (int tpc : kRowTpc) {
+          if (!valid_row(L, bm, bn, st, th, tpc)) continue;
+          tp_schedule s; std::memset(&s, 0, sizeof(s));
+          s.kind = TP_KIND_IGEMM_TC_ROW; s.bm = bm; s.bn = bn; s.bk = 64; s.stages = st;
+          s.threads = th; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
+          if (!visit(s)) return;
+        }
   } else {
     for (int th : kDThreads) for (int tq : kDTileQ) for (int vk : kDVecK) for (int tpp : kDTileP)
       for (int sm : kDSmem) {
@@ -238,7 +241,7 @@ bool schedule_in_space(const Layer& L, const tp_schedule& s) {
   if (s.kind == TP_KIND_IGEMM_TC_ROW)
     return row_kind_eligible(L) && in_(s.bm, kRowBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 64 &&
            in_(s.stages, kRowStages, 3) && in_(s.threads, kTcThreads, 2) && s.split_k == 1 &&
-           valid_row(L, s.bm, s.bn, s.stages);
+           in_(s.tiles_per_cta, kRowTpc, 5) && valid_row(L, s.bm, s.bn, s.stages, s.threads, s.tiles_per_cta);
   if (s.kind != L.kind) return false;
   if (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) {
     auto in = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };

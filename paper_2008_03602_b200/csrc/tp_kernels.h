@@ -65,6 +65,7 @@ struct TcArgs {
   int H, W, C, Kg;             // gathered kind: input extent, channels, reduction length R*S*C
   int tab_off;                 // gathered kind: byte offset of the pixel / k tables
   int nqb;                     // row-halo kind: q-blocks per output row, ceil(Q / BM)
+  int ntiles, tpc;             // row-halo kind: N*P*nqb tiles, consecutive tiles per CTA
   int cluster_red;             // 1: split-K reduced through DSMEM in a (1,1,split_k) cluster
   int bar_off;                 // byte offset of the mbarriers in dynamic shared memory
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
@@ -86,6 +87,7 @@ struct TcProblem {
   unsigned long long* trace;
   int gather;      // 1: TP_KIND_IGEMM_TC_GATHER (C % 8 != 0)
   int row;         // 1: TP_KIND_IGEMM_TC_ROW (row-halo strips)
+  int tpc;         // row-halo: tiles per CTA
 };
 
 struct TcPlan {

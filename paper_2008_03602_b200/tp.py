@@ -37,7 +37,7 @@ class ConvDesc(ctypes.Structure):
 
 class Schedule(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int32) for f in ("kind", "bm", "bn", "bk", "stages", "threads", "split_k", "tile_q",
-                                              "vec_k", "tile_p", "smem_stage", "reserved")] + \
+                                              "vec_k", "tile_p", "smem_stage", "tiles_per_cta")] + \
                [("space_index", ctypes.c_int64)] + \
                [(f, ctypes.c_int32) for f in ("grid_x", "grid_y", "grid_z", "sm_tuned")]
 

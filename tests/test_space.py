@@ -79,17 +79,20 @@ def test_gather_space_hand_count():
 
 def test_row_kind_hand_count_and_order():
     # VGG conv1_2 (C=64, 224x224, K=64, 3x3 s1 p1): eligible.  BM in {64, 128}
-    # (np2(Q) = 256), BN in {32, 64} (np2(K) = 64), stages {1, 2, 3}, threads {128, 256};
-    # largest stage = 17408 (strip 130 x 128 B -> 1 KiB multiple) + 3 x 64 x 128 = 41984 B,
-    # x 3 stages + 1024 fits, so all 2 x 2 x 3 x 2 = 24 tuples are valid.
+    # (np2(Q) = 256), BN in {32, 64} (np2(K) = 64), stages {1, 2, 3}, threads x tiles-per-CTA
+    # in {(128, 1), (256, 1), (256, 2), (256, 4), (256, 8), (256, 16)}; largest stage = 17408
+    # (strip 130 x 128 B -> 1 KiB multiple) + 3 x 64 x 128 = 41984 B, x 3 stages + 1024 fits:
+    # 2 x 2 x 3 x 6 = 72.
     d = wl.catalog("vgg19_b16")[1]
     space = sp.enumerate_space(d)
     row = [x for x in space if x["kind"] == sp.KIND_IGEMM_TC_ROW]
-    assert len(row) == 24
+    assert len(row) == 72
     first = space.index(row[0])
     assert all(x["kind"] == sp.KIND_IGEMM_TC for x in space[:first]) and space[first:] == row
     assert all(x["bk"] == 64 and x["split_k"] == 1 for x in row)
-    assert row[0]["grid_x"] == 16 * 224 * 4 and row[0]["grid_y"] == 2          # BM=64, BN=32
+    assert row[0]["grid_x"] == 16 * 224 * 4 and row[0]["grid_y"] == 2          # BM=64, BN=32, 1 tile/CTA
+    r4 = [x for x in row if x["tiles_per_cta"] == 4 and x["bm"] == 128][0]
+    assert r4["grid_x"] == 16 * 224 * 2 // 4 and r4["threads"] == 256
     # not eligible: stride 2, pad 0, C % 64 != 0, Q < 56
     r50 = wl.catalog("resnet50")
     assert [sp.row_eligible(x) for x in r50].count(True) == 1 and sp.row_eligible(r50[2])   # l1.b0.c2 only
@@ -136,6 +139,9 @@ def test_libtp_space_matches_mirror(d):
         s = tp.space_get(d, m["space_index"])
         assert s["kind"] == m["kind"]
         for f in (fields_dir if m["kind"] == sp.KIND_DIRECT else fields_tc + ("kind",)):
+            assert s[f] == m[f], (f, m)
+        if m["kind"] == sp.KIND_IGEMM_TC_ROW:
+            f = "tiles_per_cta"
             assert s[f] == m[f], (f, m)
         assert (s["grid_x"], s["grid_y"], s["grid_z"]) == (m["grid_x"], m["grid_y"], m["grid_z"])
         assert s["space_index"] == m["space_index"]

@@ -1,4 +1,2 @@
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "every_schedule" 2>&1 | tail -2
-KIND=3 python tools/trace_sched.py vgg19_b16 vgg.64.224.1 128 64 64 1 256 1 0.25
-KIND=3 python tools/trace_sched.py vgg19_b16 vgg.64.224.1 128 64 64 1 128 1 0.25
-KIND=3 python tools/trace_sched.py vgg19_b16 vgg.128.112.0 128 128 64 1 256 1 0.25
+FRAC=0.25 timeout 1200 python tools/explore.py vgg19_b16 vgg.64.224.1,vgg.128.112.0,vgg.128.112.1 gpurun_out/ex_row.json 2>&1 | grep "==" | cut -c1-200
