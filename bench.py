@@ -132,6 +132,15 @@ def layer_work(d: dict, P: int, Q: int) -> tuple[float, float]:
 
 
 # ------------------------------------------------------------------ reference arm / CPU baseline (oracle)
+def host_cores() -> int:
+    """Host cores available to this process (torchrun sets OMP_NUM_THREADS=1,
+    so the oracle is given the thread count explicitly)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def oracle_pass(layers, inputs, threads=0):
     """One evaluation of every unique layer with the fp64 oracle (C, OpenMP)."""
     from oracle import conv as oc
@@ -154,13 +163,12 @@ def cpu_inputs(layers):
 
 
 def cpu_baseline(layers, min_s=10.0, max_s=30.0) -> dict:
-    from oracle import conv as oc
     inputs = cpu_inputs(layers)
-    cores = oc.max_threads()
+    cores = host_cores()
     t0 = time.perf_counter()
     passes = 0
     while True:
-        oracle_pass(layers, inputs)
+        oracle_pass(layers, inputs, threads=cores)
         passes += 1
         el = time.perf_counter() - t0
         if el >= min_s or el + el / passes > max_s:
@@ -178,18 +186,17 @@ def run_reference(args):
     from paper_2008_03602_b200 import workloads as wl
     layers = wl.catalog(args.workload)
     inputs = cpu_inputs(layers)
-    from oracle import conv as oc
-    cores = oc.max_threads()
+    cores = host_cores()
     # Each step is a bounded sample: one oracle evaluation of a rotating subset of layers (~5 s).
     probe0 = time.perf_counter()
-    oracle_pass(layers[:1], inputs[:1])
+    oracle_pass(layers[:1], inputs[:1], threads=cores)
     t_one = max(1e-3, time.perf_counter() - probe0)
     per_step = max(1, min(len(layers), int(5.0 / t_one)))
     order = list(range(len(layers)))
 
     def step(k):
         sel = [order[(k * per_step + j) % len(order)] for j in range(per_step)]
-        oracle_pass([layers[i] for i in sel], [inputs[i] for i in sel])
+        oracle_pass([layers[i] for i in sel], [inputs[i] for i in sel], threads=cores)
         return len(sel)
 
     for k in range(args.warmup):
@@ -226,6 +233,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("TP_BENCH_DEVICE") is not None:   # path test: several ranks on one GPU
+        local = int(os.environ["TP_BENCH_DEVICE"])
     if world > 1:
         dist.init_process_group("gloo")
     torch.cuda.set_device(local)
