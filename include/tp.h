@@ -243,6 +243,31 @@ tp_status tp_tune_subset(const tp_conv_desc* d, tp_partition* part, const int64_
                          int32_t n_check, double tol, const tp_timing* timing,
                          tp_measurement* records, int32_t records_cap, int32_t* n_records);
 
+/* Model-guided selection for budgets below |space| (the
+ * paper's tuner ranks configurations with a learned cost model).
+ * Host-only.  Given the schedules measured so far (space indices and median
+ * latencies in us; latency <= 0 or non-finite = failed), returns up to
+ * `batch` unmeasured indices in next_idx[] (*n_next of them): with no
+ * measurements (or fewer than 4 successful ones) the next entries of the
+ * SplitMix64 sample of reading C17; otherwise the (1 - explore) * batch
+ * schedules with the lowest latency predicted by a ridge regression of
+ * log(latency) on a quadratic expansion of standardised schedule features
+ * (tile knobs, CTAs, k-blocks per CTA, waves at sm_granted, padding waste,
+ * kind), plus random unmeasured ones for the rest.  Deterministic.
+ * TP_EINVAL on bad arguments or an index outside the space. */
+tp_status tp_search_next(const tp_conv_desc* d, int32_t sm_granted, const int64_t* measured_idx,
+                         const double* measured_us, int32_t n_measured, int32_t batch, double explore,
+                         uint64_t seed, int64_t* next_idx, int32_t* n_next);
+/* tp_tune with model-guided selection: batches of `batch` candidates chosen by
+ * tp_search_next (explore fraction `explore`), each profiled like
+ * tp_tune_subset, until min(trials, |space|) are measured; records in
+ * measurement order; best / best_m / y as tp_tune. */
+tp_status tp_tune_guided(const tp_conv_desc* d, tp_partition* part, int32_t trials, int32_t batch, double explore,
+                         uint64_t seed, const void* x, const void* w, const void* bias, void* y, void* ws,
+                         size_t ws_bytes, const int64_t* check_idx, const double* check_ref, int32_t n_check,
+                         double tol, const tp_timing* timing, tp_schedule* best, tp_measurement* best_m,
+                         tp_measurement* records, int32_t records_cap, int32_t* n_records);
+
 /* Cross-evaluation: run schedule tuned at p (frozen geometry, reading C15)
  * inside partition `part_q` with the timing protocol (a13). */
 tp_status tp_cross_eval(const tp_conv_desc* d, const tp_schedule* tuned_at_p, tp_partition* part_q,

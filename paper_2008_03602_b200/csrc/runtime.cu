@@ -1274,6 +1274,57 @@ tp_status tp_tune(const tp_conv_desc* d, tp_partition* part, int32_t trials, uin
   return TP_OK;
 }
 
+tp_status tp_tune_guided(const tp_conv_desc* d, tp_partition* part, int32_t trials, int32_t batch, double explore,
+                         uint64_t seed, const void* x, const void* w, const void* bias, void* y, void* ws,
+                         size_t ws_bytes, const int64_t* check_idx, const double* check_ref, int32_t n_check,
+                         double tol, const tp_timing* timing, tp_schedule* best, tp_measurement* best_m,
+                         tp_measurement* records, int32_t cap, int32_t* n_records) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  if (batch < 1 || trials < 0) { set_error("bad guided-tuning arguments"); return TP_EINVAL; }
+  tp_partition* p;
+  st = get_part(part, &p);
+  if (st != TP_OK) return st;
+  const int32_t total = (int32_t)std::min<int64_t>(trials, space_size(L));
+  std::vector<int64_t> idx;
+  std::vector<double> us;
+  std::vector<tp_measurement> recs;
+  std::vector<int64_t> next(batch);
+  std::vector<tp_measurement> brec(batch);
+  while ((int32_t)idx.size() < total) {
+    const int32_t want = std::min<int32_t>(batch, total - (int32_t)idx.size());
+    int32_t nn = 0;
+    st = tp_search_next(d, p->sm_granted, idx.data(), us.data(), (int32_t)idx.size(), want, explore, seed,
+                        next.data(), &nn);
+    if (st != TP_OK) return st;
+    if (nn == 0) break;
+    int32_t nr = 0;
+    st = tp_tune_subset(d, part, next.data(), nn, x, w, bias, y, ws, ws_bytes, check_idx, check_ref, n_check, tol,
+                        timing, brec.data(), batch, &nr);
+    if (st != TP_OK) return st;
+    for (int32_t i = 0; i < nr; ++i) {
+      recs.push_back(brec[i]);
+      idx.push_back(brec[i].space_index);
+      us.push_back(brec[i].status == TP_OK ? brec[i].median_us : -1.0);
+    }
+  }
+  const int32_t nrec = (int32_t)recs.size();
+  if (records) std::memcpy(records, recs.data(), sizeof(tp_measurement) * std::min(cap, nrec));
+  if (n_records) *n_records = records ? std::min(cap, nrec) : nrec;
+  int32_t b = -1;
+  tp_select_best(recs.data(), nrec, &b);
+  if (b < 0) { set_error("no candidate passed the correctness gate"); return TP_EMISMATCH; }
+  if (best_m) *best_m = recs[b];
+  if (best) {
+    space_get(L, recs[b].space_index, best);
+    best->sm_tuned = p->sm_granted;
+    tp_conv2d_run(d, best, part, x, w, bias, y, ws, ws_bytes, nullptr, nullptr);
+    tp_partition_sync(part);
+  }
+  return TP_OK;
+}
+
 tp_status tp_cross_eval(const tp_conv_desc* d, const tp_schedule* tuned_at_p, tp_partition* part_q, const void* x,
                         const void* w, const void* bias, void* y, void* ws, size_t ws_bytes, const tp_timing* timing,
                         tp_measurement* out) {

@@ -95,6 +95,9 @@ _sig("tp_tune", _P(ConvDesc), _vp, _i32, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _P(
      _P(Timing), _P(Schedule), _P(Measurement), _P(Measurement), _i32, _P(_i32))
 _sig("tp_tune_subset", _P(ConvDesc), _vp, _P(_i64), _i32, _vp, _vp, _vp, _vp, _vp, _sz, _P(_i64), _P(_dbl), _i32,
      _dbl, _P(Timing), _P(Measurement), _i32, _P(_i32))
+_sig("tp_search_next", _P(ConvDesc), _i32, _P(_i64), _P(_dbl), _i32, _i32, _dbl, _u64, _P(_i64), _P(_i32))
+_sig("tp_tune_guided", _P(ConvDesc), _vp, _i32, _i32, _dbl, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _P(_i64), _P(_dbl),
+     _i32, _dbl, _P(Timing), _P(Schedule), _P(Measurement), _P(Measurement), _i32, _P(_i32))
 _sig("tp_cross_eval", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(Timing), _P(Measurement))
 _sig("tp_conv2d_trace", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(_u64), _i32, _P(_i32))
 _sig("tp_pack_input", _P(ConvDesc), _vp, _vp, _vp)
@@ -197,6 +200,19 @@ def select_best(records: list[dict]) -> int:
     b = _i32()
     _ck(_lib.tp_select_best(arr, len(records), ctypes.byref(b)), "tp_select_best")
     return b.value
+
+
+def search_next(d: dict, sm_granted: int, measured_idx, measured_us, batch: int, explore: float = 0.25,
+                seed: int = 42) -> list[int]:
+    """Next batch of space indices from the model-guided search (host-only)."""
+    mi = np.ascontiguousarray(measured_idx, dtype=np.int64)
+    mu = np.ascontiguousarray(measured_us, dtype=np.float64)
+    out = (_i64 * max(1, batch))()
+    n = _i32()
+    _ck(_lib.tp_search_next(ctypes.byref(desc(d)), int(sm_granted), mi.ctypes.data_as(_P(_i64)),
+                            mu.ctypes.data_as(_P(_dbl)), int(mi.shape[0]), int(batch), float(explore),
+                            int(seed) & (2**64 - 1), out, ctypes.byref(n)), "tp_search_next")
+    return list(out[:n.value])
 
 
 def workspace_size(d: dict, sched: dict | None = None) -> int:
@@ -401,6 +417,23 @@ def tune(buf: LayerBuffers, part: Partition | None, trials: int, seed: int, chec
                       ctypes.byref(best), ctypes.byref(best_m), recs, cap, ctypes.byref(nrec))
     records = [meas_to_dict(recs[i]) for i in range(nrec.value)]
     _ck(st, "tp_tune")
+    return sched_to_dict(best), meas_to_dict(best_m), records
+
+
+def tune_guided(buf: "LayerBuffers", part: Partition | None, trials: int, batch: int = 16, explore: float = 0.25,
+                seed: int = 42, tol: float = 0.0, timing_cfg: Timing | None = None):
+    """Model-guided tuning (tp_tune_guided): (best schedule, best measurement, records)."""
+    x, w, b, y, ws, wsb = buf.ptrs()
+    cap = max(1, min(trials, space_size(buf.d)))
+    recs = (Measurement * cap)()
+    nrec = _i32()
+    best, best_m = Schedule(), Measurement()
+    st = _lib.tp_tune_guided(ctypes.byref(buf.cd), _h(part), int(trials), int(batch), float(explore),
+                             int(seed) & (2**64 - 1), x, w, b, y, ws, wsb, None, None, 0, float(tol),
+                             ctypes.byref(timing_cfg) if timing_cfg is not None else None, ctypes.byref(best),
+                             ctypes.byref(best_m), recs, cap, ctypes.byref(nrec))
+    records = [meas_to_dict(recs[i]) for i in range(nrec.value)]
+    _ck(st, "tp_tune_guided")
     return sched_to_dict(best), meas_to_dict(best_m), records
 
 

@@ -149,3 +149,16 @@ def test_prune_ratio_times_slow_candidates_with_one_group():
     assert m["groups"] == groups
     _, _, recs0 = tp.tune(buf, None, trials=50, seed=42, timing_cfg=tp.timing(**dict(FAST, prune_ratio=0.0)))
     assert all(r["groups"] == groups for r in recs0)
+
+
+def test_tune_guided_measures_distinct_candidates_and_returns_argmin():
+    d = wl.catalog("resnet50")[16]
+    buf, ref = _layer_with_ref(d)
+    best, m, recs = tp.tune_guided(buf, None, trials=48, batch=16, explore=0.25, seed=5,
+                                   timing_cfg=tp.timing(**FAST))
+    idx = [r["space_index"] for r in recs]
+    assert len(recs) == 48 and len(set(idx)) == 48
+    assert idx[:16] == sp.sample(tp.space_size(d), 16, 5)          # batch 0 = C17 sample prefix
+    assert all(r["status"] == 0 for r in recs)
+    assert recs[sp.argmin(recs)]["space_index"] == best["space_index"] == m["space_index"]
+    assert np.max(np.abs(buf.output() - ref)) / np.max(np.abs(ref)) <= 2e-2
