@@ -162,21 +162,56 @@ def cpu_inputs(layers):
     return out
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(layers, min_s=10.0, max_s=30.0) -> dict:
+    """The fp64 oracle on the host cores (SURVEY 8(d) "oracle timed beside the
+    GPU run"): all-core passes over the unique layers for ~10-30 s, per-layer
+    latency and GFLOP/s from the first pass, and one single-thread pass over the
+    smallest layers for the single-core rate."""
+    from oracle import conv as oc
     inputs = cpu_inputs(layers)
     cores = host_cores()
+    per_layer = []
     t0 = time.perf_counter()
     passes = 0
     while True:
-        oracle_pass(layers, inputs, threads=cores)
+        for d, (x, w, b) in zip(layers, inputs):
+            t1 = time.perf_counter()
+            oc.conv2d_c(d, x, w, b, relu=True, threads=cores)
+            if passes == 0:
+                P, Q = oc.out_dim(d["h"], d["r"], d["stride_h"], d["pad_h"], 1), oc.out_dim(d["w"], d["s"],
+                                                                                           d["stride_w"],
+                                                                                           d["pad_w"], 1)
+                ms = (time.perf_counter() - t1) * 1e3
+                per_layer.append({"layer": d["name"], "ms": round(ms, 2),
+                                  "gflops": round(layer_work(d, P, Q)[0] / (ms * 1e-3) / 1e9, 3)})
         passes += 1
         el = time.perf_counter() - t0
         if el >= min_s or el + el / passes > max_s:
             break
     evals = passes * len(layers)
+    # single thread, on the cheapest layers (about a quarter of the FLOPs)
+    order = sorted(range(len(layers)), key=lambda i: per_layer[i]["ms"])[: max(1, len(layers) // 4)]
+    t1 = time.perf_counter()
+    for i in order:
+        x, w, b = inputs[i]
+        oc.conv2d_c(layers[i], x, w, b, relu=True, threads=1)
+    st = time.perf_counter() - t1
     return {"value": evals / el, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{passes} pass(es) over the {len(layers)} unique layers, one fp64 oracle evaluation per "
-                      f"candidate (a CPU 'candidate' = one run of the layer), {el:.1f}s on {cores} threads"}
+                      f"candidate (a CPU 'candidate' = one run of the layer), {el:.1f}s on {cores} threads",
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "single_thread": {"value": len(order) / st, "unit": UNIT, "layers": len(order), "s": round(st, 2)},
+            "per_layer": per_layer}
 
 
 def run_reference(args):
