@@ -251,7 +251,7 @@ tp_status tp_tune_subset(const tp_conv_desc* d, tp_partition* part, const int64_
  * measurements (or fewer than 4 successful ones) the next entries of the
  * SplitMix64 sample of reading C17; otherwise the (1 - explore) * batch
  * schedules with the lowest latency predicted by a ridge regression of
- * log(latency) on a quadratic expansion of standardised schedule features
+ * log(latency) on standardised schedule features
  * (tile knobs, CTAs, k-blocks per CTA, waves at sm_granted, padding waste,
  * kind), plus random unmeasured ones for the rest.  Deterministic.
  * TP_EINVAL on bad arguments or an index outside the space. */

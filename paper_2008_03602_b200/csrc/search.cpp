@@ -10,8 +10,8 @@
 // by exhaustive scoring:
 //
 //   batch 0      : the first `batch` indices of the SplitMix64 sample (C17);
-//   batch b > 0  : fit a ridge regression of log(latency) on a quadratic
-//                  expansion of standardised schedule features over every
+//   batch b > 0  : fit a ridge regression of log(latency) on the
+//                  standardised schedule features over every
 //                  successful measurement so far, then take the
 //                  (1 - explore) * batch unmeasured schedules with the lowest
 //                  prediction and fill the rest with random unmeasured ones.
@@ -160,7 +160,7 @@ tp_status tp_search_next(const tp_conv_desc* d, int32_t sm_granted, const int64_
     return TP_OK;
   }
 
-  // Standardised features over the whole space, quadratic expansion.
+  // Standardised features over the whole space.
   const int sm = std::max(1, sm_granted);
   std::vector<double> F((size_t)n * kNF);
   for (int64_t i = 0; i < n; ++i) features(L, space[i], sm, &F[(size_t)i * kNF]);
@@ -173,15 +173,14 @@ tp_status tp_search_next(const tp_conv_desc* d, int32_t sm_granted, const int64_
     mu[k] = m;
     sd[k] = v > 1e-12 ? std::sqrt(v / n) : 0.0;
   }
-  const int P = 1 + kNF + kNF * (kNF + 1) / 2;
+  // Linear model on standardised features: measured against the exhaustive
+  // records (profiles/r01_search_regret.json) it ranks better than adding
+  // squares or all pairwise products, which overfit the few points a small
+  // budget provides.
+  const int P = 1 + kNF;
   auto expand = [&](int64_t i, double* z) {
-    double x[kNF];
-    for (int k = 0; k < kNF; ++k) x[k] = sd[k] > 0 ? (F[(size_t)i * kNF + k] - mu[k]) / sd[k] : 0.0;
-    int t = 0;
-    z[t++] = 1.0;
-    for (int k = 0; k < kNF; ++k) z[t++] = x[k];
-    for (int a = 0; a < kNF; ++a)
-      for (int b = a; b < kNF; ++b) z[t++] = x[a] * x[b];
+    z[0] = 1.0;
+    for (int k = 0; k < kNF; ++k) z[k + 1] = sd[k] > 0 ? (F[(size_t)i * kNF + k] - mu[k]) / sd[k] : 0.0;
   };
   std::vector<double> A((size_t)P * P, 0.0), rhs(P, 0.0), z(P);
   for (int32_t r : ok) {
