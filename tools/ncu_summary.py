@@ -3,6 +3,7 @@
   python tools/ncu_summary.py launches <launches.csv> <out.json>
   python tools/ncu_summary.py full <prof.ncu-rep> <out.json>
   python tools/ncu_summary.py dram <dram.csv> <out.json> [catalog]   (one launch per layer, catalog order)
+  python tools/ncu_summary.py fractions <out.json> <ncuf_*.csv ...>   (tuned winner per SM fraction)
 """
 import collections
 import csv
@@ -111,6 +112,42 @@ def dram(path, out, catalog="resnet50"):
                "layers": res}, open(out, "w"), indent=1)
 
 
+def fractions(out, *paths):
+    """Tensor-pipe and DRAM evidence of the tuned winner at each SM fraction.
+    Under a green context ncu's per-SM averages cover the context's SMs only
+    (a 38-SM VGG run reads 64% tensor-pipe active; a 148-SM normalisation
+    would exceed 100% for the 14-SM runs), so the value is reported as is --
+    a percentage of the nominal tensor peak of the partition's SMs."""
+    granted = {"0.1": 14, "0.25": 38, "0.5": 74, "1.0": 148}
+    res = []
+    for path in paths:
+        name = path.split("ncuf_")[1].rsplit(".csv", 1)[0]
+        layer, frac = name.rsplit("_", 1)
+        rows = list(csv.reader(open(path)))
+        hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+        h = rows[hi]
+        mi, vi, ui, ki = (h.index(k) for k in ("Metric Name", "Metric Value", "Metric Unit", "Kernel Name"))
+        m, kern = {}, ""
+        for r in rows[hi + 1:]:
+            m[r[mi]] = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1)
+            kern = r[ki].split("(")[0]
+        g = granted.get(frac, 148)
+        t_us = m.get("gpu__time_duration.sum", 0.0)
+        dram = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+        tp_dev = m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", 0.0)
+        res.append({"layer": layer, "fraction": float(frac), "sm_granted": g, "kernel": kern,
+                    "grid": m.get("launch__grid_size"), "duration_us_cold": t_us,
+                    "tensor_pipe_pct_of_partition": tp_dev,
+                    "dram_bytes": dram, "dram_gbs": dram / (t_us * 1e-6) / 1e9 if t_us else None})
+    res.sort(key=lambda r: (r["layer"], r["fraction"]))
+    json.dump({"note": "ncu --metrics, --clock-control none, caches flushed per replay (cold); "
+                       "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed averages over the "
+                       "green context's SMs (nominal tensor peak)", "runs": res}, open(out, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    fn = {"launches": launches, "full": full, "dram": dram}[sys.argv[1]]
-    fn(*sys.argv[2:])
+    if sys.argv[1] == "fractions":
+        fractions(sys.argv[2], *sys.argv[3:])
+    else:
+        fn = {"launches": launches, "full": full, "dram": dram}[sys.argv[1]]
+        fn(*sys.argv[2:])
