@@ -413,6 +413,9 @@ def main():
     flops_tc = bytes_tc = t_tc = 0.0
     t_direct = 0.0
     per_layer = []
+    pk = peaks()
+    floor_us = part.floor(1, 128)["median_us"]   # measured launch floor of the protocol
+    roof_tc = 0.0                                # sum over tc layers of max(tensor, HBM, floor) time
     for li, d in enumerate(layers):
         b = best.get((0, li))
         if b is None:
@@ -425,11 +428,11 @@ def main():
             flops_tc += f
             bytes_tc += by
             t_tc += b["median_us"]
+            roof_tc += max(f / (pk["bf16_tflops"] * 1e6), by / (pk["hbm_gbs"] * 1e3), floor_us)
         else:
             t_direct += b["median_us"]
         per_layer.append({"layer": d["name"], "best_us": round(b["median_us"], 3), "space_index": b["space_index"],
                           "kind": kind, "ctas": b["ctas"], "waves": b["waves"]})
-    pk = peaks()
     ach_gbs = bytes_tc / (t_tc * 1e-6) / 1e9 if t_tc else 0.0
     ach_tfs = flops_tc / (t_tc * 1e-6) / 1e12 if t_tc else 0.0
     hbm_bound = bytes_tc / pk["hbm_gbs"] > flops_tc / (pk["bf16_tflops"] * 1e3)
@@ -451,7 +454,11 @@ def main():
                                "FLOPs = 2 N K P Q C R S; achieved = sum over the 22 tensor-core layers / "
                                "sum of their tuned median latencies (CUDA events, partition stream, warm L2)",
                  "tensor_frac": round(ach_tfs / pk["bf16_tflops"], 4), "hbm_frac": round(ach_gbs / pk["hbm_gbs"], 4),
-                 "time_share_of_tuned_model": round(t_tc / max(t_tc + t_direct, 1e-9), 3)})
+                 "time_share_of_tuned_model": round(t_tc / max(t_tc + t_direct, 1e-9), 3),
+                 "launch_floor_us": round(floor_us, 3),
+                 "binding_roof_frac": round(roof_tc / max(t_tc, 1e-9), 4),
+                 "binding_roof_note": "sum over the tensor-core layers of max(FLOPs / tensor peak, bytes / HBM "
+                                      "peak, measured empty-kernel launch floor) / sum of their tuned latencies"})
 
     parity = None
     cpu = None
