@@ -187,8 +187,9 @@ tp_status tp_space_sample(const tp_conv_desc* d, int32_t trials, uint64_t seed,
 tp_status tp_select_best(const tp_measurement* records, int32_t n, int32_t* best);
 
 /* ---- running the operator --------------------------------------------- */
-/* Bytes of device workspace a (desc, schedule) needs (split-K partials +
- * counters, NCHW transpose buffers).  The workspace must be zero-filled
+/* Bytes of device workspace a (desc, schedule) needs: split-K arrival counters
+ * (reserved at offset 0 for every schedule of a tensor-core layer), split-K
+ * partials, NCHW transpose buffers.  The workspace must be zero-filled
  * before its first use; libtp leaves it zeroed after each completed call. */
 tp_status tp_workspace_size(const tp_conv_desc* d, const tp_schedule* s, size_t* bytes);
 /* Max workspace over the layer's whole space (for tuning). */

@@ -314,13 +314,16 @@ static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 static WsLayout ws_layout(const Layer& L, const tp_schedule& s) {
   WsLayout w;
   size_t off = 0;
-  if ((s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) && s.split_k > 1) {
-    // The counter region depends on the layer only (sized for the smallest tile,
-    // 64 x 32), so partials of one schedule never land on another schedule's
-    // counters: every counter stays zero between completed launches.
+  // The split-K arrival counters sit at offset 0 for EVERY schedule of a
+  // tensor-core layer (sized for the smallest tile, 64 x 32), so that no other
+  // region of any schedule (partials, NCHW staging) ever overlaps them: every
+  // counter stays zero between completed launches.
+  if (L.kind != TP_KIND_DIRECT) {
     const int64_t max_tiles = cdiv(L.M, 64) * cdiv(L.d.k, 32);
-    const int64_t tiles = cdiv(L.M, s.bm) * cdiv(L.d.k, s.bn);
     w.counters = off; off = align256(off + (size_t)max_tiles * 4);
+  }
+  if ((s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) && s.split_k > 1) {
+    const int64_t tiles = cdiv(L.M, s.bm) * cdiv(L.d.k, s.bn);
     w.partials = off; off = align256(off + (size_t)s.split_k * tiles * s.bm * s.bn * 4);
   }
   if (L.d.in_layout == TP_LAYOUT_NCHW) {

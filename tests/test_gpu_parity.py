@@ -176,3 +176,24 @@ def test_pack_kernels_bit_exact():
     wb = buf.w.view(torch.bfloat16).cpu()
     wwant = torch.tensor(w).permute(0, 2, 3, 1).contiguous().bfloat16().reshape(-1)
     assert torch.equal(wb.view(torch.int16), wwant.view(torch.int16))
+
+
+@pytest.mark.parametrize("d", [TC_TINY[0], TC_TINY[4], TC_TINY[6]], ids=["tc", "row", "gather"])
+def test_every_schedule_bit_exact_global_splitk(d, monkeypatch):
+    """Split-K through the global workspace (the fallback when a context cannot
+    co-schedule the (1,1,split_k) cluster), interleaved with split-1 schedules
+    of every kind in the space, twice: the arrival counters must survive them."""
+    monkeypatch.setenv("TP_NO_CLUSTER", "1")
+    x, w, b = datagen.make_inputs(d, 13, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    bad = []
+    for rep in range(2):
+        for i in range(tp.space_size(d)):
+            s = tp.space_get(d, i)
+            buf.poison()
+            tp.conv2d_run(buf, s)
+            torch.cuda.synchronize()
+            if not np.array_equal(buf.output(), ref):
+                bad.append((rep, i, s["kind"], s["split_k"]))
+    assert not bad, f"{len(bad)} schedule runs differ, first: {bad[:5]}"
