@@ -63,7 +63,14 @@ enum { TP_EPI_BIAS = 1, TP_EPI_RELU = 2 };
  * (fp32, depthwise); IGEMM_TC_GATHER = tcgen05 implicit GEMM whose A/B tiles
  * are gathered into shared memory by CUDA-core warps over the flattened
  * (r, s, c) axis (bf16, g = 1, C % 8 != 0: the C = 3 stems). */
-enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2, TP_KIND_IGEMM_TC_ROW = 3 };
+enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2, TP_KIND_IGEMM_TC_ROW = 3,
+       TP_KIND_IGEMM_TC_MT = 4 };
+/* IGEMM_TC_MT ("multi-tile im2col"): appended last to the space of IGEMM_TC
+ * layers with ceil(M/64)*ceil(K/32) >= 1024.  The IGEMM_TC k-blocks (one TMA
+ * im2col box + one weight box per (channel block, tap), BK = 64) run in the
+ * multi-tile pipeline of the row-halo kernel: tiles_per_cta in {2, 4, 8}
+ * consecutive BM-pixel tiles per CTA, two TMEM accumulators, 256 threads,
+ * split_k = 1; stages in {2, 3, 4}.  grid = (ceil(ceil(M/BM)/tpc), ceil(K/BN), 1). */
 /* IGEMM_TC_ROW ("row-halo"): an extra schedule kind appended to the space of
  * IGEMM_TC layers with 3x3 filters, stride 1, pad 1, C % 64 == 0 and Q >= 56.
  * A tile is BM pixels of one output row; per (64-channel block, filter row)

@@ -23,6 +23,7 @@ KIND_IGEMM_TC = 0
 KIND_DIRECT = 1
 KIND_IGEMM_TC_GATHER = 2
 KIND_IGEMM_TC_ROW = 3
+KIND_IGEMM_TC_MT = 4
 DTYPE_BF16 = 0
 DTYPE_FP32 = 1
 SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
@@ -31,6 +32,7 @@ TC_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("bk", (16, 32, 64, 1
             ("stages", (2, 3, 4, 6)), ("threads", (128, 256)), ("split_k", (1, 2, 4, 8)))
 ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)), ("threads", (128, 256)),
              ("tiles_per_cta", (1, 2, 4, 8, 16)))
+MT_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("tiles_per_cta", (2, 4, 8)))
 DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
                 ("tile_p", (1, 2, 4, 8)), ("smem_stage", (0, 1)))
 
@@ -129,6 +131,20 @@ def _valid_row(d: dict, bm, bn, stages, threads, tiles_per_cta) -> bool:
     return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))
 
 
+def mt_eligible(d: dict) -> bool:
+    """Multi-tile im2col kind: TMA-kind layers with at least 1024 tiles of 64 x 32."""
+    P, Q = out_pq(d)
+    return layer_kind(d) == KIND_IGEMM_TC and _cdiv(d["n"] * P * Q, 64) * _cdiv(d["k"], 32) >= 1024
+
+
+def _valid_mt(d: dict, bm, bn, stages, tiles_per_cta) -> bool:
+    """BK = 64: smem = stages (bm + bn) 64 2 + 1024; tile bounds as the TMA kind."""
+    P, Q = out_pq(d)
+    if stages * (bm + bn) * 64 * 2 + 1024 > SMEM_LIMIT:
+        return False
+    return bn <= max(32, _np2(d["k"])) and bm <= max(64, _np2(d["n"] * P * Q)) and 64 <= max(16, _np2(d["c"]))
+
+
 def _valid_direct(d: dict, threads, tile_q, vec_k, tile_p, smem_stage) -> bool:
     P, Q = out_pq(d)
     if tile_q > Q or tile_p > P or vec_k > d["k"]:
@@ -162,13 +178,22 @@ def enumerate_space(d: dict) -> list[dict]:
                          space_index=len(out))
                 s.update(geometry(d, s))
                 out.append(s)
+    if mt_eligible(d):           # appended last; threads = 256, bk = 64, split_k = 1
+        for combo in itertools.product(*[v for _, v in MT_KNOBS]):
+            if _valid_mt(d, *combo):
+                s = dict(zip([k for k, _ in MT_KNOBS], combo), bk=64, threads=256, split_k=1,
+                         kind=KIND_IGEMM_TC_MT, space_index=len(out))
+                s.update(geometry(d, s))
+                out.append(s)
     return out
 
 
 def geometry(d: dict, s: dict) -> dict:
     """Frozen launch geometry of a schedule (grid, threads per CTA)."""
     P, Q = out_pq(d)
-    if s.get("kind") == KIND_IGEMM_TC_ROW:
+    if s.get("kind") == KIND_IGEMM_TC_MT:
+        g = (_cdiv(_cdiv(d["n"] * P * Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
+    elif s.get("kind") == KIND_IGEMM_TC_ROW:
         g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
     elif s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER):
         M = d["n"] * P * Q

@@ -689,8 +689,9 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   }
 }
 
-// ------------------------------------------------------------- row-halo kernel
-// TP_KIND_IGEMM_TC_ROW.  A tile is BM pixels of one output row (q0 .. q0+BM-1
+// ------------------------------------------------------------- multi-tile kernel
+// TP_KIND_IGEMM_TC_ROW (ROW = true) and TP_KIND_IGEMM_TC_MT (ROW = false).
+// ROW: a tile is BM pixels of one output row (q0 .. q0+BM-1
 // of row p, image n); a k-block is (64-channel block cb, filter row r): one
 // tiled TMA box brings the input strip of BM+2 pixels (padding = out-of-bounds
 // zero fill) and three boxes bring the taps' BN x 64 weight tiles; the MMA
@@ -700,12 +701,22 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 // consecutive tiles: the producer ring runs across tiles, the MMA alternates
 // between two TMEM accumulators, and (tpc > 1) warps 2..7 drain one
 // accumulator while the MMA fills the other (tmem_full / tmem_empty pairs).
-template <int BM, int BN>
-__global__ void __launch_bounds__(256) igemm_row_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                        const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+// MT (ROW = false) runs the same multi-tile pipeline with the im2col k-blocks
+// of the TMA kind: tile = BM consecutive pixels, k-block = (channel block,
+// tap), one im2col box + one weight box per k-block.
+template <int BM, int BN, int BK, bool ROW>
+__global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                       const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+  static_assert(!ROW || BK == 64, "row-halo k-blocks are 64 channels");
+  constexpr int SUBK = BK < 64 ? BK : 64;
+  constexpr int NSUB = BK / SUBK;
+  constexpr uint32_t SWZ = ROW ? 128 : SUBK * 2;
+  constexpr uint32_t A_SUB = BM * SUBK * 2, B_SUB = BN * SUBK * 2;
   constexpr uint32_t A_STRIP = ((BM + 2) * 128 + 1023) / 1024 * 1024;
-  constexpr uint32_t B_TAP = BN * 128, B_STAGE = 3 * B_TAP;
-  constexpr uint32_t STRIP_BYTES = (BM + 2) * 128;
+  constexpr uint32_t B_TAP = BN * 128;
+  constexpr uint32_t A_STAGE = ROW ? A_STRIP : A_SUB * NSUB;
+  constexpr uint32_t B_STAGE = ROW ? 3 * B_TAP : B_SUB * NSUB;
+  constexpr uint32_t A_BYTES = ROW ? (BM + 2) * 128 : A_SUB * NSUB;   // expect_tx of the A part
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
 
@@ -713,7 +724,7 @@ __global__ void __launch_bounds__(256) igemm_row_kernel(const __grid_constant__ 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int stages = a.stages;
   uint8_t* a_tiles = smem_raw;
-  uint8_t* b_tiles = a_tiles + (size_t)stages * A_STRIP;
+  uint8_t* b_tiles = a_tiles + (size_t)stages * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + a.bar_off);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;     // [2]
@@ -741,13 +752,25 @@ __global__ void __launch_bounds__(256) igemm_row_kernel(const __grid_constant__ 
   }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
+  // ROW: tile = BM pixels of one output row (q-block t % nqb of row t / nqb);
+  // im2col: tile = BM consecutive output pixels m0 = t * BM (rows past M masked).
   auto tile_coords = [&](int t, int& q0, int& p0, int& n0, int& mrow0, int& mvalid) {
-    const int qb = t % a.nqb, row = t / a.nqb;
-    q0 = qb * BM;
-    p0 = row % a.P;
-    n0 = row / a.P;
-    mrow0 = row * a.Q + q0;
-    mvalid = a.Q - q0 < BM ? a.Q - q0 : BM;
+    if constexpr (ROW) {
+      const int qb = t % a.nqb, row = t / a.nqb;
+      q0 = qb * BM;
+      p0 = row % a.P;
+      n0 = row / a.P;
+      mrow0 = row * a.Q + q0;
+      mvalid = a.Q - q0 < BM ? a.Q - q0 : BM;
+    } else {
+      const int m0 = t * BM;
+      q0 = m0 % a.Q;
+      const int t0 = m0 / a.Q;
+      p0 = t0 % a.P;
+      n0 = t0 / a.P;
+      mrow0 = m0;
+      mvalid = (int)a.M - m0 < BM ? (int)a.M - m0 : BM;
+    }
   };
 
   if (warp == 0 && lane == 0) {
@@ -779,25 +802,41 @@ __global__ void __launch_bounds__(256) igemm_row_kernel(const __grid_constant__ 
     for (int i = 0; i < ntl; ++i) {
       int q0, p0, n0, mrow0, mvalid;
       tile_coords(tile0 + i, q0, p0, n0, mrow0, mvalid);
-      int cb = 0, r = 0;
+      const int cw = q0 * a.sw - a.pw, chh = p0 * a.sh - a.ph;
+      int cb = 0, r = 0, sx = 0;
       for (int kb = 0; kb < kpt; ++kb) {
         mbar_wait(empty + stage, phase ^ 1u);
-        uint8_t* sa = a_tiles + (size_t)stage * A_STRIP;
+        uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
         uint8_t* sb = b_tiles + (size_t)stage * B_STAGE;
-        mbar_arrive_expect_tx_p(full + stage, STRIP_BYTES + B_STAGE, lead);
-        tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
+        mbar_arrive_expect_tx_p(full + stage, A_BYTES + B_STAGE, lead);
+        if constexpr (ROW) {
+          // (channel block cb, filter row r): the input strip + the three taps
+          tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
 #pragma unroll
-        for (int ss = 0; ss < 3; ++ss)
-          tma_load_tile_4d_p(sb + ss * B_TAP, &tmB, full + stage, cb * 64, ss, r, nbase, lead);
-        if (++r == 3) { r = 0; ++cb; }
+          for (int ss = 0; ss < 3; ++ss)
+            tma_load_tile_4d_p(sb + ss * B_TAP, &tmB, full + stage, cb * 64, ss, r, nbase, lead);
+          if (++r == 3) { r = 0; ++cb; }
+        } else {
+          // (channel block cb, tap (r, sx)): one im2col box + the weight box
+#pragma unroll
+          for (int sb2 = 0; sb2 < NSUB; ++sb2) {
+            tma_load_im2col_4d_p(sa + sb2 * A_SUB, &tmA, full + stage, cb * BK + sb2 * SUBK, cw, chh, n0,
+                                 (uint16_t)sx, (uint16_t)r, lead);
+            tma_load_tile_4d_p(sb + sb2 * B_SUB, &tmB, full + stage, cb * BK + sb2 * SUBK, sx, r, nbase, lead);
+          }
+          if (++cb == a.cblocks) {
+            cb = 0;
+            if (++sx == a.S) { sx = 0; ++r; }
+          }
+        }
         if (++stage == stages) { stage = 0; phase ^= 1u; }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: two accumulators, alternating per tile ----------------
     const uint32_t lead = elect_one();
-    const uint64_t adesc0 = make_sdesc(smem_u32(a_tiles), 128);
-    const uint64_t bdesc0 = make_sdesc(smem_u32(b_tiles), 128);
+    const uint64_t adesc0 = make_sdesc(smem_u32(a_tiles), SWZ);
+    const uint64_t bdesc0 = make_sdesc(smem_u32(b_tiles), SWZ);
     int stage = 0;
     uint32_t phase = 0;
     for (int i = 0; i < ntl; ++i) {
@@ -810,14 +849,25 @@ __global__ void __launch_bounds__(256) igemm_row_kernel(const __grid_constant__ 
       for (int kb = 0; kb < kpt; ++kb) {
         mbar_wait(full + stage, phase);
         tc_fence_after();
-        const uint64_t ad = adesc0 + ((uint32_t)(stage * A_STRIP) >> 4);
+        const uint64_t ad = adesc0 + ((uint32_t)(stage * A_STAGE) >> 4);
         const uint64_t bd = bdesc0 + ((uint32_t)(stage * B_STAGE) >> 4);
+        if constexpr (ROW) {
 #pragma unroll
-        for (int ss = 0; ss < 3; ++ss)
+          for (int ss = 0; ss < 3; ++ss)
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc_mma_p(dcol, ad + ((uint32_t)(ss * 128 + kk * 32) >> 4), bd + ((uint32_t)(ss * B_TAP + kk * 32) >> 4),
-                     IDESC, (kb > 0 || ss > 0 || kk > 0) ? 1u : 0u, lead);
+            for (int kk = 0; kk < 4; ++kk)
+              tc_mma_p(dcol, ad + ((uint32_t)(ss * 128 + kk * 32) >> 4),
+                       bd + ((uint32_t)(ss * B_TAP + kk * 32) >> 4), IDESC, (kb > 0 || ss > 0 || kk > 0) ? 1u : 0u,
+                       lead);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            constexpr int kPerSub = SUBK / 16;
+            const uint32_t sb2 = kk / kPerSub, koff = (kk % kPerSub) * 32;
+            tc_mma_p(dcol, ad + ((sb2 * A_SUB + koff) >> 4), bd + ((sb2 * B_SUB + koff) >> 4), IDESC,
+                     (kb > 0 || kk > 0) ? 1u : 0u, lead);
+          }
+        }
         tc_commit_p(empty + stage, lead);
         if (++stage == stages) { stage = 0; phase ^= 1u; }
       }
@@ -905,7 +955,14 @@ using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
 template <int BM, int BN, int MODE>
 static KernelFn pick_bk(int bk) {
   if constexpr (MODE == 2) {
-    return bk == 64 ? igemm_row_kernel<BM, BN> : nullptr;
+    return bk == 64 ? igemm_mt_kernel<BM, BN, 64, true> : nullptr;
+  } else if constexpr (MODE == 3) {
+    switch (bk) {
+      case 16: return igemm_mt_kernel<BM, BN, 16, false>;
+      case 32: return igemm_mt_kernel<BM, BN, 32, false>;
+      case 64: return igemm_mt_kernel<BM, BN, 64, false>;
+      case 128: return igemm_mt_kernel<BM, BN, 128, false>;
+    }
   } else {
     switch (bk) {
       case 16: return igemm_tc_kernel<BM, BN, 16, MODE>;
@@ -920,7 +977,9 @@ static KernelFn pick_bk(int bk) {
 static KernelFn pick_tc(int bm, int bn, int bk, int mode) {
 #define TP_TC_CASE(M_, N_)                                                                       \
   if (bm == M_ && bn == N_)                                                                      \
-    return mode == 2 ? pick_bk<M_, N_, 2>(bk) : (mode == 1 ? pick_bk<M_, N_, 1>(bk) : pick_bk<M_, N_, 0>(bk));
+    return mode == 3 ? pick_bk<M_, N_, 3>(bk)                                                    \
+                     : (mode == 2 ? pick_bk<M_, N_, 2>(bk)                                       \
+                                  : (mode == 1 ? pick_bk<M_, N_, 1>(bk) : pick_bk<M_, N_, 0>(bk)));
   TP_TC_CASE(64, 32) TP_TC_CASE(64, 64) TP_TC_CASE(64, 128) TP_TC_CASE(64, 256)
   TP_TC_CASE(128, 32) TP_TC_CASE(128, 64) TP_TC_CASE(128, 128) TP_TC_CASE(128, 256)
 #undef TP_TC_CASE
@@ -1022,6 +1081,10 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.nqb = 1;
   a.ntiles = 0;
   a.tpc = 1;
+  if (pb.mt) {
+    a.ntiles = (int)((pb.M + pb.bm - 1) / pb.bm);
+    a.tpc = pb.tpc > 1 ? pb.tpc : 1;
+  }
   if (pb.row) {
     a.kblocks = (pb.C / 64) * 3;
     a.nqb = (pb.Q + pb.bm - 1) / pb.bm;
@@ -1035,9 +1098,10 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     static const int dbg = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
     a.dbg = dbg;
   }
-  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.row ? 2 : (pb.gather ? 1 : 0)));
+  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.mt ? 3 : (pb.row ? 2 : (pb.gather ? 1 : 0))));
   if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN x BK"); return TP_EINVALID_CONFIG; }
-  plan->grid = pb.row ? dim3((unsigned)((a.ntiles + a.tpc - 1) / a.tpc), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u)
+  plan->grid = (pb.row || pb.mt)
+                   ? dim3((unsigned)((a.ntiles + a.tpc - 1) / a.tpc), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u)
                       : dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn),
                              (unsigned)pb.split_k);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);

@@ -145,6 +145,23 @@ int64_t row_stage_bytes(int bm, int bn) {
   const int64_t strip = (((int64_t)(bm + 2) * 128) + 1023) / 1024 * 1024;
   return strip + 3 * (int64_t)bn * 128;
 }
+// Multi-tile im2col kind (TMA-kind layers with >= 1024 tiles of 64 x 32): the
+// TMA kind's k-blocks inside the multi-tile pipeline (two TMEM accumulators,
+// epilogue of one tile overlapping the mainloop of the next), 256 threads,
+// split_k = 1, BK = 64.
+bool mt_kind_eligible(const Layer& L) {
+  return L.kind == TP_KIND_IGEMM_TC && cdiv(L.M, 64) * cdiv(L.d.k, 32) >= 1024;
+}
+static const int kMtStages[] = {2, 3, 4};
+static const int kMtTpc[] = {2, 4, 8};
+
+static bool valid_mt(const Layer& L, int bm, int bn, int stages) {
+  if (tc_smem_bytes(bm, bn, 64, stages) > kSmemLimit) return false;
+  if (bn > std::max<int64_t>(32, np2(L.d.k))) return false;
+  if (bm > std::max<int64_t>(64, np2(L.M))) return false;
+  return 64 <= std::max<int64_t>(16, np2(L.d.c));
+}
+
 static const int kRowBM[] = {64, 128};
 static const int kRowStages[] = {1, 2, 3};
 static const int kRowTpc[] = {1, 2, 4, 8, 16};
@@ -157,7 +174,11 @@ static bool valid_row(const Layer& L, int bm, int bn, int stages, int threads, i
 }
 
 void fill_geometry(const Layer& L, tp_schedule* s) {
-  if (s->kind == TP_KIND_IGEMM_TC_ROW) {
+  if (s->kind == TP_KIND_IGEMM_TC_MT) {
+    s->grid_x = (int32_t)cdiv(cdiv(L.M, s->bm), std::max(1, s->tiles_per_cta));
+    s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
+    s->grid_z = 1;
+  } else if (s->kind == TP_KIND_IGEMM_TC_ROW) {
     s->grid_x = (int32_t)cdiv((int64_t)L.d.n * L.P * cdiv(L.Q, s->bm), std::max(1, s->tiles_per_cta));
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = 1;
@@ -198,6 +219,15 @@ static void enumerate(const Layer& L, F visit) {
           s.threads = th; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
           if (!visit(s)) return;
         }
+    // Layers with many tiles append the multi-tile im2col kind last.
+    if (mt_kind_eligible(L))
+      for (int bm : kTcBM) for (int bn : kTcBN) for (int st : kMtStages) for (int tpc : kMtTpc) {
+        if (!valid_mt(L, bm, bn, st)) continue;
+        tp_schedule s; std::memset(&s, 0, sizeof(s));
+        s.kind = TP_KIND_IGEMM_TC_MT; s.bm = bm; s.bn = bn; s.bk = 64; s.stages = st;
+        s.threads = 256; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
+        if (!visit(s)) return;
+      }
   } else {
     for (int th : kDThreads) for (int tq : kDTileQ) for (int vk : kDVecK) for (int tpp : kDTileP)
       for (int sm : kDSmem) {
@@ -238,6 +268,10 @@ bool space_get(const Layer& L, int64_t idx, tp_schedule* out) {
 
 bool schedule_in_space(const Layer& L, const tp_schedule& s) {
   auto in_ = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };
+  if (s.kind == TP_KIND_IGEMM_TC_MT)
+    return mt_kind_eligible(L) && in_(s.bm, kTcBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 64 &&
+           in_(s.stages, kMtStages, 3) && s.threads == 256 && s.split_k == 1 && in_(s.tiles_per_cta, kMtTpc, 3) &&
+           valid_mt(L, s.bm, s.bn, s.stages);
   if (s.kind == TP_KIND_IGEMM_TC_ROW)
     return row_kind_eligible(L) && in_(s.bm, kRowBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 64 &&
            in_(s.stages, kRowStages, 3) && in_(s.threads, kTcThreads, 2) && s.split_k == 1 &&

@@ -36,6 +36,7 @@ int64_t direct_smem_bytes(const Layer& L, int threads, int tile_q, int vec_k, in
 int64_t tc_smem_bytes(int bm, int bn, int bk, int stages);
 int64_t tcg_table_bytes(const Layer& L, int bm, int bk);   // gather kind: pixel + k tables
 bool row_kind_eligible(const Layer& L);                     // row-halo kind applies
+bool mt_kind_eligible(const Layer& L);                      // multi-tile im2col kind applies
 int64_t row_stage_bytes(int bm, int bn);                    // row-halo kind: one pipeline stage
 bool schedule_in_space(const Layer& L, const tp_schedule& s);
 

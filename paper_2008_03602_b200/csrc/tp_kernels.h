@@ -87,7 +87,8 @@ struct TcProblem {
   unsigned long long* trace;
   int gather;      // 1: TP_KIND_IGEMM_TC_GATHER (C % 8 != 0)
   int row;         // 1: TP_KIND_IGEMM_TC_ROW (row-halo strips)
-  int tpc;         // row-halo: tiles per CTA
+  int tpc;         // row-halo / multi-tile: tiles per CTA
+  int mt;          // 1: TP_KIND_IGEMM_TC_MT (im2col multi-tile)
 };
 
 struct TcPlan {

@@ -197,3 +197,26 @@ def test_every_schedule_bit_exact_global_splitk(d, monkeypatch):
             if not np.array_equal(buf.output(), ref):
                 bad.append((rep, i, s["kind"], s["split_k"]))
     assert not bad, f"{len(bad)} schedule runs differ, first: {bad[:5]}"
+
+
+def test_multitile_kind_every_schedule_bit_exact_integer():
+    """IGEMM_TC_MT (>= 1024 tiles of 64 x 32): every multi-tile schedule, ragged
+    tile counts per CTA (tiles_per_cta 8 over 128 or 256 tiles of 128/64)."""
+    d = mk(1, 64, 128, 128, 128, 3, 3, 1, 1, out=tp.FP32, epi=1)
+    assert sp.mt_eligible(d)
+    x, w, b = datagen.make_inputs(d, 17, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    bad, n = [], 0
+    for i in range(tp.space_size(d)):
+        s = tp.space_get(d, i)
+        if s["kind"] != tp.KIND_IGEMM_TC_MT:
+            continue
+        n += 1
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        if not np.array_equal(buf.output(), ref):
+            bad.append((i, {k: s[k] for k in ("bm", "bn", "stages", "tiles_per_cta")}))
+    # BM {64, 128} x BN {32, 64, 128} (K = 128) x stages {2, 3, 4} x tiles_per_cta {2, 4, 8}
+    assert n == 54 and not bad, f"{len(bad)}/{n} differ, first: {bad[:5]}"

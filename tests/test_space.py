@@ -50,12 +50,13 @@ def test_space_counts_and_order():
         stems = [d for d in cat if sp.layer_kind(d) == sp.KIND_IGEMM_TC_GATHER]
         rest = [d for d in cat if sp.layer_kind(d) != sp.KIND_IGEMM_TC_GATHER]
         assert len(stems) == 1 and stems[0]["c"] == 3
-        n_rest = sum(1 for d in rest for x in sp.enumerate_space(d) if x["kind"] != sp.KIND_IGEMM_TC_ROW)
+        n_rest = sum(1 for d in rest for x in sp.enumerate_space(d)
+                     if x["kind"] not in (sp.KIND_IGEMM_TC_ROW, sp.KIND_IGEMM_TC_MT))
         assert n_rest + _direct_count(stems[0]) == total
     d = wl.catalog("resnet50")[2]
     s = sp.enumerate_space(d)
     keys = [(x["kind"], x["bm"], x["bn"], x["bk"], x["stages"], x["threads"], x["split_k"]) for x in s]
-    assert keys == sorted(keys)      # kind is the outermost key (row-halo tuples follow the TMA ones)
+    assert keys == sorted(keys)      # kind is the outermost key (appended kinds follow the TMA ones)
     assert [x["space_index"] for x in s] == list(range(len(s)))
 
 
@@ -88,7 +89,7 @@ def test_row_kind_hand_count_and_order():
     row = [x for x in space if x["kind"] == sp.KIND_IGEMM_TC_ROW]
     assert len(row) == 72
     first = space.index(row[0])
-    assert all(x["kind"] == sp.KIND_IGEMM_TC for x in space[:first]) and space[first:] == row
+    assert all(x["kind"] == sp.KIND_IGEMM_TC for x in space[:first]) and space[first:first + len(row)] == row
     assert all(x["bk"] == 64 and x["split_k"] == 1 for x in row)
     assert row[0]["grid_x"] == 16 * 224 * 4 and row[0]["grid_y"] == 2          # BM=64, BN=32, 1 tile/CTA
     r4 = [x for x in row if x["tiles_per_cta"] == 4 and x["bm"] == 128][0]
@@ -96,6 +97,19 @@ def test_row_kind_hand_count_and_order():
     # not eligible: stride 2, pad 0, C % 64 != 0, Q < 56
     r50 = wl.catalog("resnet50")
     assert [sp.row_eligible(x) for x in r50].count(True) == 1 and sp.row_eligible(r50[2])   # l1.b0.c2 only
+
+
+def test_mt_kind_hand_count():
+    # VGG conv3_1 (b16, C=128, 56x56, K=256): 784 x 8 >= 1024 64x32 tiles -> eligible.  BM {64, 128},
+    # BN {32..256}, stages {2, 3, 4}, tiles_per_cta {2, 4, 8}; smem = stages (BM+BN) 128 + 1024 fits
+    # for every combination (max 4 x 384 x 128 + 1024 = 197632): 2 x 4 x 3 x 3 = 72, appended last.
+    d = wl.catalog("vgg19_b16")[4]
+    space = sp.enumerate_space(d)
+    mt = [x for x in space if x["kind"] == sp.KIND_IGEMM_TC_MT]
+    assert len(mt) == 72 and space[-72:] == mt and all(x["threads"] == 256 for x in mt)
+    x = [m for m in mt if m["bm"] == 128 and m["bn"] == 128 and m["tiles_per_cta"] == 4][0]
+    assert (x["grid_x"], x["grid_y"], x["grid_z"]) == (-(-(16 * 56 * 56 // 128) // 4), 2, 1)
+    assert not any(sp.mt_eligible(r) for r in wl.catalog("resnet50"))
 
 
 def test_kind_selection():
@@ -140,7 +154,7 @@ def test_libtp_space_matches_mirror(d):
         assert s["kind"] == m["kind"]
         for f in (fields_dir if m["kind"] == sp.KIND_DIRECT else fields_tc + ("kind",)):
             assert s[f] == m[f], (f, m)
-        if m["kind"] == sp.KIND_IGEMM_TC_ROW:
+        if m["kind"] in (sp.KIND_IGEMM_TC_ROW, sp.KIND_IGEMM_TC_MT):
             f = "tiles_per_cta"
             assert s[f] == m[f], (f, m)
         assert (s["grid_x"], s["grid_y"], s["grid_z"]) == (m["grid_x"], m["grid_y"], m["grid_z"])
