@@ -111,6 +111,15 @@ __device__ __forceinline__ void tma_load_tile_4d_p(void* dst, const CUtensorMap*
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(lead)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_tile_2d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                   int32_t c1, uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+      "@q cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(lead)
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_p(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate, uint32_t lead) {
   asm volatile(
@@ -284,10 +293,6 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     trace[61] = ncta;
     trace[60] = (unsigned long long)a.cluster_red;
   }
-  // Let the next kernel in the stream be scheduled now (programmatic dependent
-  // launch); it waits in griddepcontrol.wait before touching memory.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-
   const int kb0 = (split * a.kblocks) / a.split_k;   // 32-bit: M, k-blocks < 2^31 (checked on the host)
   const int kb1 = ((split + 1) * a.kblocks) / a.split_k;
   const int nkb = kb1 - kb0;
@@ -305,27 +310,49 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   // advanced incrementally (no divisions in the loop).
   int p_cb = 0, p_s = 0, p_r = 0, p_stage = 0, p_kb = kb0;
   uint32_t p_phase = 0;
-  auto produce = [&](uint32_t lead) {
+  // Move the producer state `step` k-blocks ahead (step <= stages).
+  auto advance = [&](int step) {
+    for (int t = 0; t < step; ++t) {
+      if (++p_cb == a.cblocks) {
+        p_cb = 0;
+        if (++p_s == a.S) { p_s = 0; ++p_r; }
+      }
+    }
+    p_stage += step;
+    if (p_stage >= stages) { p_stage -= stages; p_phase ^= 1u; }
+    p_kb += step;
+  };
+  // parts: bit0 A (im2col) boxes, bit1 B (weight) boxes, bit2 the stage's expect_tx.
+  // Two producer warps (0 and 3) take alternate k-blocks (step 2): a TMA issue
+  // costs ~90 cycles of the issuing thread (measured, tools/micro/tma_issue.cu)
+  // and independent threads issue in parallel.
+  auto produce = [&](uint32_t lead, int parts, int step) {
     uint8_t* sa = a_tiles + (size_t)p_stage * A_STAGE;
     uint8_t* sbp = b_tiles + (size_t)p_stage * B_STAGE;
-    mbar_arrive_expect_tx_p(full + p_stage, ((a.dbg & 1) ? 0u : A_STAGE) + ((a.dbg & 2) ? 0u : B_STAGE), lead);
+    if (parts & 4)
+      mbar_arrive_expect_tx_p(full + p_stage, ((a.dbg & 1) ? 0u : A_STAGE) + ((a.dbg & 2) ? 0u : B_STAGE), lead);
     const int c0 = p_cb * BK;
 #pragma unroll
     for (int sb = 0; sb < NSUB; ++sb) {
-      if (!(a.dbg & 1))
-        tma_load_im2col_4d_p(sa + sb * A_SUB, &tmA, full + p_stage, c0 + sb * SUBK, cw, ch, n0, (uint16_t)p_s,
-                             (uint16_t)p_r, lead);
-      if (!(a.dbg & 2))
+      if (!(a.dbg & 1) && (parts & 1)) {
+        if (a.a_tiled)   // 1x1 / s1 / p0: A is the plain [M x C] matrix (tiled box, cheaper than im2col)
+          tma_load_tile_2d_p(sa + sb * A_SUB, &tmA, full + p_stage, c0 + sb * SUBK, m0, lead);
+        else
+          tma_load_im2col_4d_p(sa + sb * A_SUB, &tmA, full + p_stage, c0 + sb * SUBK, cw, ch, n0, (uint16_t)p_s,
+                               (uint16_t)p_r, lead);
+      }
+      if (!(a.dbg & 2) && (parts & 2))
         tma_load_tile_4d_p(sbp + sb * B_SUB, &tmB, full + p_stage, c0 + sb * SUBK, p_s, p_r, nbase, lead);
     }
-    if (++p_cb == a.cblocks) {
-      p_cb = 0;
-      if (++p_s == a.S) { p_s = 0; ++p_r; }
-    }
-    if (++p_stage == stages) { p_stage = 0; p_phase ^= 1u; }
-    ++p_kb;
+    advance(step);
   };
 
+  if (!GATHER && (warp == 0 || warp == 3)) {
+    const int rs = kb0 / a.cblocks;
+    p_cb = kb0 - rs * a.cblocks;
+    p_s = rs % a.S;
+    p_r = rs / a.S;
+  }
   if (warp == 0) {
     if (lane == 0) {
       if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // swizzle atoms need 1 KiB alignment
@@ -347,18 +374,16 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     __syncwarp();
     if constexpr (!GATHER) {
       const uint32_t lead = elect_one();
-      const int rs = kb0 / a.cblocks;
-      p_cb = kb0 - rs * a.cblocks;
-      p_s = rs % a.S;
-      p_r = rs / a.S;
-      // Wait for the previous grid (PDL), then fill the whole ring before the
-      // CTA-wide sync so the first loads overlap the TMEM allocation.
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      if (trace && lane == 0) trace[53] = gtimer();
-      const int pre = nkb < stages ? nkb : stages;
-      for (int i = 0; i < pre; ++i) {
-        produce(lead);
-        if (trace && lane == 0 && i < 4) trace[54 + i] = gtimer();
+      // With w_early the weight boxes of the first ring pass go out before the
+      // PDL wait (weights are layer constants; the runtime sets w_early only
+      // when the preceding kernel is a launch of this same plan).  Everything
+      // that depends on the previous grid is issued after the CTA-wide sync, so
+      // the MMA warp waits on stage 0 instead of on the whole ring fill.
+      if (a.w_early) {
+        const int pre = nkb < stages ? nkb : stages;
+        const int s_cb = p_cb, s_s = p_s, s_r = p_r, s_kb = p_kb;
+        for (int i = 0; i < pre; ++i) produce(lead, 6, 1);
+        p_cb = s_cb; p_s = s_s; p_r = s_r; p_kb = s_kb; p_stage = 0; p_phase = 0;
       }
     }
   }
@@ -400,13 +425,19 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   tc_fence_after();
   // Publish the initialised reduction barrier to the cluster; the matching
   // wait sits just before the first remote store, long after every peer arrived.
-  if (a.cluster_red) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  // (relaxed: the mbarrier init is already ordered by fence.mbarrier_init.release.cluster;
+  // a release arrive would also wait for this thread's outstanding memory operations)
+  if (a.cluster_red) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // provably warp-uniform
   if (trace && threadIdx.x == 0) trace[1] = gtimer();
+  // Every warp sleeps in the PDL wait rather than spinning on an mbarrier while
+  // the previous grid may still run on this SM (co-resident CTAs).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (GATHER && warp != 1) {
     // ---------------- gather producers (all warps but the MMA warp) ----------------
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int pt = warp == 0 ? lane : (int)threadIdx.x - 32;
     const int np = (int)blockDim.x - 32;
     const int4* rowtab = reinterpret_cast<const int4*>(smem_raw + a.tab_off);
@@ -485,13 +516,22 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       if (trace && threadIdx.x == 0 && kb - kb0 < kTraceK) trace[20 + kb - kb0] = gtimer();
       if (++stage == stages) { stage = 0; phase ^= 1u; }
     }
-  } else if (!GATHER && warp == 0) {
-    // ---------------- TMA producer (rest of the k-blocks; one elected lane issues) ----------------
+  } else if (!GATHER && (warp == 0 || warp == 3)) {
+    // ---------------- TMA producers: warp 0 even, warp 3 odd k-blocks (one elected lane each) ----------------
     const uint32_t lead = elect_one();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // Every operand this grid reads is now final: the next kernel in the
+    // stream may be scheduled (programmatic dependent launch).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (trace && warp == 0 && lane == 0) trace[53] = gtimer();
+    const int pre = a.w_early ? (nkb < stages ? nkb : stages) : 0;   // weight boxes already in flight
+    if (warp == 3) advance(1);
     while (p_kb < kb1) {
-      mbar_wait(empty + p_stage, p_phase ^ 1u);
-      if (trace && lane == 0 && p_kb - kb0 < kTraceK) trace[20 + p_kb - kb0] = gtimer();
-      produce(lead);
+      const int j = p_kb - kb0;
+      mbar_wait(empty + p_stage, p_phase ^ 1u);   // free on the first ring pass
+      if (trace && warp == 0 && lane == 0 && j < kTraceK) trace[20 + j] = gtimer();
+      produce(lead, j < pre ? 1 : 7, 2);
+      if (trace && warp == 0 && lane == 0 && j < 8) trace[54 + j / 2] = gtimer();
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one elected lane of warp 1) ----------------
@@ -750,7 +790,6 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
     trace[63] = g;
     trace[62] = sm;
   }
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ROW: tile = BM pixels of one output row (q-block t % nqb of row t / nqb);
   // im2col: tile = BM consecutive output pixels m0 = t * BM (rows past M masked).
@@ -796,39 +835,66 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
   if (warp == 0) {
     // ---------------- TMA producer: strips + tap weights, ring across tiles ----------------
     const uint32_t lead = elect_one();
+    // One k-block of a tile: parts bit0 = A box(es), bit1 = weight boxes, bit2 = expect_tx.
+    auto issue = [&](int stage, int cb, int r, int sx, int q0, int p0, int n0, int m0, int parts) {
+      uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
+      uint8_t* sb = b_tiles + (size_t)stage * B_STAGE;
+      if (parts & 4) mbar_arrive_expect_tx_p(full + stage, A_BYTES + B_STAGE, lead);
+      if constexpr (ROW) {
+        // (channel block cb, filter row r): the input strip + the three taps
+        if (parts & 1) tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
+        if (parts & 2) {
+#pragma unroll
+          for (int ss = 0; ss < 3; ++ss)
+            tma_load_tile_4d_p(sb + ss * B_TAP, &tmB, full + stage, cb * 64, ss, r, nbase, lead);
+        }
+      } else {
+        // (channel block cb, tap (r, sx)): one im2col box + the weight box
+        const int cw = q0 * a.sw - a.pw, chh = p0 * a.sh - a.ph;
+#pragma unroll
+        for (int sb2 = 0; sb2 < NSUB; ++sb2) {
+          if (parts & 1) {
+            if (a.a_tiled)
+              tma_load_tile_2d_p(sa + sb2 * A_SUB, &tmA, full + stage, cb * BK + sb2 * SUBK, m0, lead);
+            else
+              tma_load_im2col_4d_p(sa + sb2 * A_SUB, &tmA, full + stage, cb * BK + sb2 * SUBK, cw, chh, n0,
+                                   (uint16_t)sx, (uint16_t)r, lead);
+          }
+          if (parts & 2)
+            tma_load_tile_4d_p(sb + sb2 * B_SUB, &tmB, full + stage, cb * BK + sb2 * SUBK, sx, r, nbase, lead);
+        }
+      }
+    };
+    auto advance = [&](int& cb, int& r, int& sx) {
+      if constexpr (ROW) {
+        if (++r == 3) { r = 0; ++cb; }
+      } else if (++cb == a.cblocks) {
+        cb = 0;
+        if (++sx == a.S) { sx = 0; ++r; }
+      }
+    };
+    // w_early: the weight boxes of the first tile's first ring pass go out
+    // before the PDL wait (weights are layer constants; see TcArgs::w_early).
+    const int npre = (a.w_early && ntl > 0) ? (kpt < stages ? kpt : stages) : 0;
+    {
+      int cb = 0, r = 0, sx = 0;
+      for (int kb = 0; kb < npre; ++kb) {
+        issue(kb, cb, r, sx, 0, 0, 0, 0, 6);
+        advance(cb, r, sx);
+      }
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     int stage = 0;
     uint32_t phase = 0;
     for (int i = 0; i < ntl; ++i) {
       int q0, p0, n0, mrow0, mvalid;
       tile_coords(tile0 + i, q0, p0, n0, mrow0, mvalid);
-      const int cw = q0 * a.sw - a.pw, chh = p0 * a.sh - a.ph;
       int cb = 0, r = 0, sx = 0;
       for (int kb = 0; kb < kpt; ++kb) {
         mbar_wait(empty + stage, phase ^ 1u);
-        uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
-        uint8_t* sb = b_tiles + (size_t)stage * B_STAGE;
-        mbar_arrive_expect_tx_p(full + stage, A_BYTES + B_STAGE, lead);
-        if constexpr (ROW) {
-          // (channel block cb, filter row r): the input strip + the three taps
-          tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
-#pragma unroll
-          for (int ss = 0; ss < 3; ++ss)
-            tma_load_tile_4d_p(sb + ss * B_TAP, &tmB, full + stage, cb * 64, ss, r, nbase, lead);
-          if (++r == 3) { r = 0; ++cb; }
-        } else {
-          // (channel block cb, tap (r, sx)): one im2col box + the weight box
-#pragma unroll
-          for (int sb2 = 0; sb2 < NSUB; ++sb2) {
-            tma_load_im2col_4d_p(sa + sb2 * A_SUB, &tmA, full + stage, cb * BK + sb2 * SUBK, cw, chh, n0,
-                                 (uint16_t)sx, (uint16_t)r, lead);
-            tma_load_tile_4d_p(sb + sb2 * B_SUB, &tmB, full + stage, cb * BK + sb2 * SUBK, sx, r, nbase, lead);
-          }
-          if (++cb == a.cblocks) {
-            cb = 0;
-            if (++sx == a.S) { sx = 0; ++r; }
-          }
-        }
+        issue(stage, cb, r, sx, q0, p0, n0, mrow0, (i == 0 && kb < npre) ? 1 : 7);
+        advance(cb, r, sx);
         if (++stage == stages) { stage = 0; phase ^= 1u; }
       }
     }
@@ -1006,6 +1072,9 @@ static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red, b
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   const DriverApi& drv = driver();
   const int sub_k = pb.bk < 64 ? pb.bk : 64;
+  static const bool no_atile = getenv("TP_NO_ATILE") && atoi(getenv("TP_NO_ATILE")) != 0;
+  const bool a_tiled = !pb.gather && !pb.row && !no_atile && pb.R == 1 && pb.S == 1 && pb.sh == 1 && pb.sw == 1 &&
+                       pb.ph == 0 && pb.pw == 0;
   if (pb.M > INT32_MAX / 2 || (int64_t)pb.N * pb.H * pb.W * pb.C > INT32_MAX) {
     set_error("tensor too large for 32-bit tile indexing");
     return TP_EUNSUPPORTED;
@@ -1042,19 +1111,36 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   } else {
   const CUtensorMapSwizzle swz = sub_k == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
                                              : (sub_k == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  CUresult r;
+  if (a_tiled) {
+    // 1x1 / stride 1 / pad 0: im2col is the identity, A = NHWC x viewed as [M][C]
+    // (a tiled box issues ~3x faster than an im2col box; rows past M are zero fill).
+    cuuint64_t a_dims[2] = {(cuuint64_t)pb.C, (cuuint64_t)pb.M};
+    cuuint64_t a_strides[1] = {(cuuint64_t)pb.C * 2};
+    cuuint32_t a_box[2] = {(cuuint32_t)sub_k, (cuuint32_t)pb.bm};
+    cuuint32_t a_estr[2] = {1, 1};
+    r = drv.encodeTiled(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pb.x), a_dims, a_strides,
+                        a_box, a_estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled (1x1 A) failed (" + std::to_string((int)r) + ")");
+      return TP_ECUDA;
+    }
+  } else {
   // A: im2col over NHWC x, dims (C, W, H, N).
   cuuint64_t a_dims[4] = {(cuuint64_t)pb.C, (cuuint64_t)pb.W, (cuuint64_t)pb.H, (cuuint64_t)pb.N};
   cuuint64_t a_strides[3] = {(cuuint64_t)pb.C * 2, (cuuint64_t)pb.W * pb.C * 2, (cuuint64_t)pb.H * pb.W * pb.C * 2};
   int lower[2] = {-pb.pw, -pb.ph};
   int upper[2] = {pb.pw - (pb.S - 1), pb.ph - (pb.R - 1)};
   cuuint32_t a_estr[4] = {1, (cuuint32_t)pb.sw, (cuuint32_t)pb.sh, 1};
-  CUresult r = drv.encodeIm2col(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.x), a_dims,
-                                a_strides, lower, upper, (cuuint32_t)sub_k, (cuuint32_t)pb.bm, a_estr,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  r = drv.encodeIm2col(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.x), a_dims,
+                       a_strides, lower, upper, (cuuint32_t)sub_k, (cuuint32_t)pb.bm, a_estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")");
     return TP_ECUDA;
+  }
   }
   // B: tiled over KRSC weights, dims (C, S, R, K).
   cuuint64_t b_dims[4] = {(cuuint64_t)pb.C, (cuuint64_t)pb.S, (cuuint64_t)pb.R, (cuuint64_t)pb.K};
@@ -1098,6 +1184,8 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     static const int dbg = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
     a.dbg = dbg;
   }
+  a.w_early = 0;   // set per launch sequence by the runtime (time_plan / tuner phase B)
+  a.a_tiled = a_tiled ? 1 : 0;
   plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.mt ? 3 : (pb.row ? 2 : (pb.gather ? 1 : 0))));
   if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN x BK"); return TP_EINVALID_CONFIG; }
   plan->grid = (pb.row || pb.mt)

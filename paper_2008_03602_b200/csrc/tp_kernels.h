@@ -41,6 +41,9 @@ const DriverApi& driver();
 // Programmatic dependent launch (PDL) for back-to-back kernels in a stream:
 // on unless TP_PDL=0.  Kernels call griddepcontrol.wait before reading memory.
 bool pdl_enabled();
+// Weight prefetch across the PDL wait (TcArgs::w_early) in repeated launches
+// of one plan: on unless TP_W_EARLY=0.
+bool w_early_enabled();
 
 // Per-(function, context) caches of launch-time queries (host-side hot path of
 // the tuner): the max-dynamic-smem attribute and the occupancy calculator.
@@ -70,6 +73,10 @@ struct TcArgs {
   int bar_off;                 // byte offset of the mbarriers in dynamic shared memory
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
   int dbg;                     // TP_DEBUG_TC env (experiments only): bit0 skip A TMA, bit1 skip B TMA
+  int a_tiled;                 // 1: A is a tiled [M][C] map (1x1 / stride 1 / pad 0 layers), not im2col
+  int w_early;                 // 1: weight (B) boxes of the first ring pass are issued before
+                               //    griddepcontrol.wait -- only when the preceding kernel in the
+                               //    stream is a launch of this plan (weights are layer constants)
 };
 
 struct TcProblem {

@@ -220,3 +220,26 @@ def test_multitile_kind_every_schedule_bit_exact_integer():
             bad.append((i, {k: s[k] for k in ("bm", "bn", "stages", "tiles_per_cta")}))
     # BM {64, 128} x BN {32, 64, 128} (K = 128) x stages {2, 3, 4} x tiles_per_cta {2, 4, 8}
     assert n == 54 and not bad, f"{len(bad)}/{n} differ, first: {bad[:5]}"
+
+
+@pytest.mark.parametrize("d", TC_TINY + [mk(1, 64, 128, 128, 128, 3, 3, 1, 1, out=tp.FP32, epi=1)],
+                         ids=lambda d: f"early_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_r{d['r']}s{d['stride_h']}")
+def test_timed_launches_weight_prefetch_bit_exact_integer(d):
+    """Timed runs (time_plan): the first launch waits on the PDL dependency
+    before any load; every later launch issues its first ring pass of weight
+    boxes before griddepcontrol.wait (TcArgs::w_early).  The last launch of a
+    timed run is such a launch, so y after timing must still equal the oracle
+    bit-exactly (O11) for every tensor-core schedule."""
+    x, w, b = datagen.make_inputs(d, 13, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    tm = tp.timing(warmup=1, groups=1, n_min=2, target_group_us=1.0)
+    bad, n = [], tp.space_size(d)
+    for i in range(n):
+        s = tp.space_get(d, i)
+        buf.poison()
+        m = tp.conv2d_run(buf, s, timing_cfg=tm)
+        torch.cuda.synchronize()
+        if m["status"] != 0 or not np.array_equal(buf.output(), ref):
+            bad.append((i, s["kind"], s["bm"], s["bn"], s["bk"], s["stages"], s["split_k"]))
+    assert not bad, f"{len(bad)}/{n} timed schedules differ, first: {bad[:5]}"

@@ -48,6 +48,8 @@ def main():
         rows = []
         for d, r in zip(layers, tuned):
             rows.append({"layer": d["name"], "mult": d["mult"], "best_us": r["best_m"]["median_us"],
+                         "space_index": r["best"]["space_index"],
+                         "sched": {k: r["best"][k] for k in ("bm", "bn", "bk", "stages", "threads", "split_k")},
                          "kind": r["best_m"]["kind"], "candidates": r["candidates"],
                          "roofline": ex.roofline(d, r["best_m"]["median_us"], ctx["sm_granted"], ctx["copy_bw_gbs"],
                                                  ctx["floor_us"], pk, r["best_m"]["kind"])})
