@@ -694,6 +694,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     // Host-side phase timing (TP_PROFILE=1 prints one line per call to stderr).
     static const bool prof = getenv("TP_PROFILE") && atoi(getenv("TP_PROFILE")) != 0;
     const auto tA = std::chrono::steady_clock::now();
+    double host_a_plan_us = 0, host_a_sync_us = 0;
     // ---------------- phase A: gate runs, chunked ----------------
     double* d_vals = nullptr;
     TP_CK(cudaMalloc(&d_vals, sizeof(double) * (size_t)std::max(1, ncheck) * kChunk));
@@ -706,7 +707,9 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       for (int32_t i = c0; i < c1; ++i) {
         Cand& c = cs[i];
         if (cand[i] < 0 || cand[i] >= (int64_t)table.size()) { c.m.status = TP_EINVALID_CONFIG; continue; }
+        const auto tm0 = std::chrono::steady_clock::now();
         tp_status s2 = make_plan(L, table[cand[i]], x, w, bias, y, ws, ws_bytes, &c.plan);
+        if (prof) host_a_plan_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tm0).count();
         if (s2 != TP_OK) { c.m.status = s2; continue; }
         plan_geometry(c.plan, part->sm_granted, &c.m);
         const char* step = "poison";
@@ -731,9 +734,11 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         g_launches += 1;
         c.live = true;
       }
+      const auto ts0 = std::chrono::steady_clock::now();
       cudaError_t e = cudaMemcpyAsync(h_vals.data(), d_vals, sizeof(double) * (size_t)ncheck * (c1 - c0),
                                       cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (prof) host_a_sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts0).count();
       if (e != cudaSuccess) {
         set_error(std::string("gate sync: ") + cudaGetErrorString(e));
         err = TP_ECUDA;
@@ -776,6 +781,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
 
     const auto tB = std::chrono::steady_clock::now();
     double host_b_us = 0;   // time spent in make/capture/instantiate/enqueue (excl. harvest waits)
+    double host_warm_us = 0, host_cap_us = 0, host_inst_us = 0;
     // ---------------- phase B: timing, windowed pipeline ----------------
     // Reading C12b: candidates far slower than the fastest gate run of this
     // call get one timed group (still a warm, graph-timed median of n launches).
@@ -844,6 +850,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       c.plan.tc.args.w_early = w_early_enabled() ? 1 : 0;
       cudaError_t e = cudaSuccess;
       for (int k = 0; k < warm && e == cudaSuccess; ++k) e = launch_plan(c.plan, st);
+      const auto te1 = std::chrono::steady_clock::now();
       if (e == cudaSuccess && tm.use_graph) {
         cudaGraph_t graph = nullptr;
         e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
@@ -854,8 +861,14 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
           g_launches -= (int64_t)c.n * c.plan.kernels_per_call;   // capture does not launch
           e = ce != cudaSuccess ? ce : ee;
         }
+        const auto te2 = std::chrono::steady_clock::now();
         if (e == cudaSuccess) e = cudaGraphInstantiate(&c.exec, graph, 0);
         if (graph) cudaGraphDestroy(graph);
+        if (prof) {
+          host_warm_us += std::chrono::duration<double, std::micro>(te1 - te0).count();
+          host_cap_us += std::chrono::duration<double, std::micro>(te2 - te1).count();
+          host_inst_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - te2).count();
+        }
       }
       cudaEvent_t* ev = pb.ev.data() + (size_t)c.slot * 2 * groups;
       for (int g = 0; g < c.groups && e == cudaSuccess; ++g) {
@@ -892,8 +905,11 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
         return std::chrono::duration<double, std::micro>(b - a).count();
       };
-      fprintf(stderr, "[tp] candidates %d: phase A %.0f us, phase B %.0f us (host enqueue %.0f us)\n", n_cand,
-              us(tA, tB), us(tB, tC), host_b_us);
+      fprintf(stderr,
+              "[tp] candidates %d: phase A %.0f us, phase B %.0f us (host enqueue %.0f us: warm-up %.0f, capture %.0f, "
+              "instantiate %.0f); phase A make_plan %.0f us, chunk sync+D2H %.0f us\n",
+              n_cand, us(tA, tB), us(tB, tC), host_b_us, host_warm_us, host_cap_us, host_inst_us, host_a_plan_us,
+              host_a_sync_us);
     }
     // C12b: a raced candidate that beat every fully-timed one is re-timed with
     // the full protocol, so the winner's record is always a full measurement.
