@@ -24,6 +24,7 @@ KIND_DIRECT = 1
 KIND_IGEMM_TC_GATHER = 2
 KIND_IGEMM_TC_ROW = 3
 KIND_IGEMM_TC_MT = 4
+KIND_IGEMM_TF32X3 = 5
 DTYPE_BF16 = 0
 DTYPE_FP32 = 1
 SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
@@ -33,6 +34,7 @@ TC_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("bk", (16, 32, 64, 1
 ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)), ("threads", (128, 256)),
              ("tiles_per_cta", (1, 2, 4, 8, 16)))
 MT_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("tiles_per_cta", (2, 4, 8)))
+TF32_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)))
 DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
                 ("tile_p", (1, 2, 4, 8)), ("smem_stage", (0, 1)))
 
@@ -156,6 +158,23 @@ def _valid_direct(d: dict, threads, tile_q, vec_k, tile_p, smem_stage) -> bool:
     return True
 
 
+def tf32_eligible(d: dict) -> bool:
+    """3xTF32 tensor-core kind: fp32 dense layers whose NHWC
+    pixel rows are 16-byte multiples (C % 4 == 0) and K % 8 == 0."""
+    return (layer_kind(d) == KIND_DIRECT and d["dtype"] == DTYPE_FP32 and d.get("groups", 1) == 1
+            and d["c"] % 4 == 0 and d["k"] % 8 == 0)
+
+
+def _valid_tf32(d: dict, bm: int, bn: int, stages: int) -> bool:
+    # ring: stages x (A + B) tiles of 32 fp32 channels (128-B rows), hi and lo copies
+    P, Q = out_pq(d)
+    if stages * (bm + bn) * 32 * 4 * 2 + 1024 > SMEM_LIMIT:
+        return False
+    if bn > max(32, _np2(d["k"])):
+        return False
+    return bm <= max(64, _np2(d["n"] * P * Q))
+
+
 def enumerate_space(d: dict) -> list[dict]:
     """Valid schedules in lexicographic knob order (outermost knob first);
     ``space_index`` is the rank among the valid tuples."""
@@ -178,6 +197,13 @@ def enumerate_space(d: dict) -> list[dict]:
                          space_index=len(out))
                 s.update(geometry(d, s))
                 out.append(s)
+    if tf32_eligible(d):         # appended after the direct tuples; bk = 32, threads = 256, split_k = 1
+        for combo in itertools.product(*[v for _, v in TF32_KNOBS]):
+            if _valid_tf32(d, *combo):
+                s = dict(zip([k for k, _ in TF32_KNOBS], combo), bk=32, threads=256, split_k=1,
+                         kind=KIND_IGEMM_TF32X3, space_index=len(out))
+                s.update(geometry(d, s))
+                out.append(s)
     if mt_eligible(d):           # appended last; threads = 256, bk = 64, split_k = 1
         for combo in itertools.product(*[v for _, v in MT_KNOBS]):
             if _valid_mt(d, *combo):
@@ -195,7 +221,7 @@ def geometry(d: dict, s: dict) -> dict:
         g = (_cdiv(_cdiv(d["n"] * P * Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
     elif s.get("kind") == KIND_IGEMM_TC_ROW:
         g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
-    elif s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER):
+    elif s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER, KIND_IGEMM_TF32X3):
         M = d["n"] * P * Q
         g = (_cdiv(M, s["bm"]), _cdiv(d["k"], s["bn"]), s["split_k"])
     else:

@@ -19,13 +19,13 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "-I", os.path.join(ROOT, "include"),
           "--expt-relaxed-constexpr"]
-SOURCES = ["space.cpp", "search.cpp", "runtime.cu", "igemm_tc.cu", "direct_conv.cu", "aux_kernels.cu"]
+SOURCES = ["space.cpp", "search.cpp", "runtime.cu", "igemm_tc.cu", "igemm_tf32.cu", "direct_conv.cu", "aux_kernels.cu"]
 
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
-    deps = [path] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".h")]
+    deps = [path] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     deps.append(os.path.join(ROOT, "include", "tp.h"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj

@@ -28,211 +28,9 @@
 #include <climits>
 
 #include "tp_kernels.h"
+#include "tc_ptx.cuh"
 
 namespace tp {
-
-// ------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "TP_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra TP_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_im2col_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c,
-                                                   int32_t w, int32_t h, int32_t n, uint16_t off_w,
-                                                   uint16_t off_h) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w),
-      "h"(off_h)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_tile_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                                 int32_t c1, int32_t c2, int32_t c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-// Warp-uniform issue: the whole warp executes these (uniform control flow, so
-// descriptors/coordinates stay in uniform registers and no per-instruction
-// ELECT loop is generated); only the lane with lead != 0 issues.
-__device__ __forceinline__ uint32_t elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "selp.u32 %0, 1, 0, e;\n\t}"
-      : "=r"(pred));
-  return pred;
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx_p(uint64_t* bar, uint32_t bytes, uint32_t lead) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
-      "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(bytes), "r"(lead)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_im2col_4d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c,
-                                                     int32_t w, int32_t h, int32_t n, uint16_t off_w, uint16_t off_h,
-                                                     uint32_t lead) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %9, 0;\n\t"
-      "@q cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};\n\t}" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w),
-      "h"(off_h), "r"(lead)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_tile_4d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                                   int32_t c1, int32_t c2, int32_t c3, uint32_t lead) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %7, 0;\n\t"
-      "@q cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];\n\t}" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(lead)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_tile_2d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                                   int32_t c1, uint32_t lead) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
-      "@q cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(lead)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_p(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate, uint32_t lead) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "setp.ne.b32 q, %5, 0;\n\t"
-      "@q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(lead)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit_p(uint64_t* bar, uint32_t lead) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
-      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar)),
-      "r"(lead)
-      : "memory");
-}
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
-  return remote;
-}
-// 16-byte store into a peer CTA's shared memory that completes `bytes` on the
-// peer's mbarrier (both addresses in the shared::cluster window).
-__device__ __forceinline__ void st_async_v4(uint32_t dst, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
-                                            uint32_t bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
-               ::"r"(dst), "r"(a), "r"(b), "r"(c), "r"(d), "r"(bar)
-               : "memory");
-}
-// Store 4 consecutive output channels of row m.
-__device__ __forceinline__ void store4(void* y, int64_t m, int K, int n0, float4 v, int out_f32) {
-  if (out_f32) {
-    *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + m * K + n0) = v;
-  } else {
-    __nv_bfloat162 b0 = __floats2bfloat162_rn(v.x, v.y), b1 = __floats2bfloat162_rn(v.z, v.w);
-    uint2 u;
-    u.x = *reinterpret_cast<uint32_t*>(&b0);
-    u.y = *reinterpret_cast<uint32_t*>(&b1);
-    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(y) + m * K + n0) = u;
-  }
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-      "%14, %15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// Shared-memory matrix descriptor, K-major, swizzled (sm100 format: start>>4
-// [0,14), LBO>>4 [16,30) (unused for swizzled K-major, =1), SBO>>4 [32,46) =
-// 8 rows * row pitch, version 1 at [46,48), layout type at [61,64)).
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t swz_bytes) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1u << 16;
-  d |= (uint64_t)(((8u * swz_bytes) >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1u << 46;
-  const uint64_t layout = swz_bytes == 128 ? 2 : (swz_bytes == 64 ? 4 : 6);
-  d |= layout << 61;
-  return d;
-}
-
-// Store 16 consecutive output channels [n0, n0+16) of row m.
-__device__ __forceinline__ void store16(void* y, int64_t m, int K, int n0, const float (&v)[16], int out_f32) {
-  if (out_f32) {
-    float* p = reinterpret_cast<float*>(y) + m * K + n0;
-#pragma unroll
-    for (int g = 0; g < 16; g += 8) {
-      if (n0 + g + 8 <= K) {
-        reinterpret_cast<float4*>(p + g)[0] = make_float4(v[g], v[g + 1], v[g + 2], v[g + 3]);
-        reinterpret_cast<float4*>(p + g)[1] = make_float4(v[g + 4], v[g + 5], v[g + 6], v[g + 7]);
-      }
-    }
-  } else {
-    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(y) + m * K + n0;
-#pragma unroll
-    for (int g = 0; g < 16; g += 8) {
-      if (n0 + g + 8 <= K) {
-        uint4 u;
-        __nv_bfloat162 b0 = __floats2bfloat162_rn(v[g], v[g + 1]);
-        __nv_bfloat162 b1 = __floats2bfloat162_rn(v[g + 2], v[g + 3]);
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[g + 4], v[g + 5]);
-        __nv_bfloat162 b3 = __floats2bfloat162_rn(v[g + 6], v[g + 7]);
-        u.x = *reinterpret_cast<uint32_t*>(&b0);
-        u.y = *reinterpret_cast<uint32_t*>(&b1);
-        u.z = *reinterpret_cast<uint32_t*>(&b2);
-        u.w = *reinterpret_cast<uint32_t*>(&b3);
-        *reinterpret_cast<uint4*>(p + g) = u;
-      }
-    }
-  }
-}
 
 // Timeline slots per CTA when tracing (SM clock64 cycles): 0 entry, 1 prologue
 // done, 2 epilogue start (tmem_full seen), 3 end, 4.. MMA-thread full-barrier
@@ -1069,12 +867,79 @@ static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red, b
   return (off + 1023) & ~(size_t)1023;
 }
 
+// 3xTF32 kind: fp32 maps (32-channel boxes = 128-B rows, 128-B swizzle), ring of
+// hi tiles + twin ring of lo tiles, barriers (full, ready, empty) after the rings.
+static tp_status tf32_prepare(const TcProblem& pb, bool a_tiled, TcPlan* plan) {
+  const DriverApi& drv = driver();
+  CUresult r;
+  if (a_tiled) {
+    cuuint64_t dims[2] = {(cuuint64_t)pb.C, (cuuint64_t)pb.M};
+    cuuint64_t strides[1] = {(cuuint64_t)pb.C * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)pb.bm};
+    cuuint32_t es[2] = {1, 1};
+    r = drv.encodeTiled(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(pb.x), dims, strides, box,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[4] = {(cuuint64_t)pb.C, (cuuint64_t)pb.W, (cuuint64_t)pb.H, (cuuint64_t)pb.N};
+    cuuint64_t strides[3] = {(cuuint64_t)pb.C * 4, (cuuint64_t)pb.W * pb.C * 4, (cuuint64_t)pb.H * pb.W * pb.C * 4};
+    int lower[2] = {-pb.pw, -pb.ph};
+    int upper[2] = {pb.pw - (pb.S - 1), pb.ph - (pb.R - 1)};
+    cuuint32_t es[4] = {1, (cuuint32_t)pb.sw, (cuuint32_t)pb.sh, 1};
+    r = drv.encodeIm2col(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(pb.x), dims, strides, lower,
+                         upper, 32, (cuuint32_t)pb.bm, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) {
+    set_error("tensor map (tf32 A) failed (" + std::to_string((int)r) + ")");
+    return TP_ECUDA;
+  }
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)pb.C, (cuuint64_t)pb.S, (cuuint64_t)pb.R, (cuuint64_t)pb.K};
+    cuuint64_t strides[3] = {(cuuint64_t)pb.C * 4, (cuuint64_t)pb.S * pb.C * 4, (cuuint64_t)pb.R * pb.S * pb.C * 4};
+    cuuint32_t box[4] = {32, 1, 1, (cuuint32_t)pb.bn};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    r = drv.encodeTiled(&plan->tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(pb.w), dims, strides, box,
+                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("tensor map (tf32 B) failed (" + std::to_string((int)r) + ")");
+      return TP_ECUDA;
+    }
+  }
+  TcArgs& a = plan->args;
+  std::memset(&a, 0, sizeof(a));
+  a.M = pb.M; a.K = pb.K; a.P = pb.P; a.Q = pb.Q; a.S = pb.S;
+  a.sh = pb.sh; a.sw = pb.sw; a.ph = pb.ph; a.pw = pb.pw;
+  a.bk = 32; a.stages = pb.stages; a.split_k = 1;
+  a.cblocks = (pb.C + 31) / 32;
+  a.kblocks = pb.R * pb.S * a.cblocks;
+  a.H = pb.H; a.W = pb.W; a.C = pb.C; a.Kg = pb.R * pb.S * pb.C;
+  a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
+  a.a_tiled = a_tiled ? 1 : 0;
+  a.bar_off = (int)((size_t)pb.stages * (pb.bm + pb.bn) * 256);   // hi + lo rings, 1 KiB multiples
+  plan->fn = pick_tf32(pb.bm, pb.bn);
+  if (!plan->fn) { set_error("no igemm_tf32 instantiation for this BM x BN"); return TP_EINVALID_CONFIG; }
+  plan->grid = dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u);
+  if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
+  plan->block = dim3(256);
+  plan->cluster_z = 1;
+  plan->smem = (size_t)a.bar_off + 1024;
+  cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    return TP_ECUDA;
+  }
+  return TP_OK;
+}
+
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   const DriverApi& drv = driver();
   const int sub_k = pb.bk < 64 ? pb.bk : 64;
   static const bool no_atile = getenv("TP_NO_ATILE") && atoi(getenv("TP_NO_ATILE")) != 0;
   const bool a_tiled = !pb.gather && !pb.row && !no_atile && pb.R == 1 && pb.S == 1 && pb.sh == 1 && pb.sw == 1 &&
                        pb.ph == 0 && pb.pw == 0;
+  if (pb.tf32) return tf32_prepare(pb, a_tiled, plan);
   if (pb.M > INT32_MAX / 2 || (int64_t)pb.N * pb.H * pb.W * pb.C > INT32_MAX) {
     set_error("tensor too large for 32-bit tile indexing");
     return TP_EUNSUPPORTED;

@@ -173,6 +173,22 @@ static bool valid_row(const Layer& L, int bm, int bn, int stages, int threads, i
   return bn <= std::max<int64_t>(32, np2(L.d.k));
 }
 
+// 3xTF32 tensor-core kind for fp32 dense layers: fp32 NHWC x
+// and KRSC w are TMA-loaded (32-channel k-blocks, 128-B rows), split in shared
+// memory into tf32 hi/lo parts, and D += A_hi B_hi + A_hi B_lo + A_lo B_hi on
+// tcgen05 kind::tf32; appended after the direct tuples; 256 threads, split 1.
+bool tf32_kind_eligible(const Layer& L) {
+  const tp_conv_desc& d = L.d;
+  return L.kind == TP_KIND_DIRECT && d.dtype == TP_DTYPE_FP32 && d.groups == 1 && d.c % 4 == 0 && d.k % 8 == 0;
+}
+static const int kTf32Stages[] = {2, 3, 4};
+int64_t tf32_smem_bytes(int bm, int bn, int stages) { return (int64_t)stages * (bm + bn) * 128 * 2 + 1024; }
+static bool valid_tf32(const Layer& L, int bm, int bn, int stages) {
+  if (tf32_smem_bytes(bm, bn, stages) > kSmemLimit) return false;
+  if (bn > std::max<int64_t>(32, np2(L.d.k))) return false;
+  return bm <= std::max<int64_t>(64, np2(L.M));
+}
+
 void fill_geometry(const Layer& L, tp_schedule* s) {
   if (s->kind == TP_KIND_IGEMM_TC_MT) {
     s->grid_x = (int32_t)cdiv(cdiv(L.M, s->bm), std::max(1, s->tiles_per_cta));
@@ -182,7 +198,7 @@ void fill_geometry(const Layer& L, tp_schedule* s) {
     s->grid_x = (int32_t)cdiv((int64_t)L.d.n * L.P * cdiv(L.Q, s->bm), std::max(1, s->tiles_per_cta));
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = 1;
-  } else if (s->kind == TP_KIND_IGEMM_TC || s->kind == TP_KIND_IGEMM_TC_GATHER) {
+  } else if (s->kind == TP_KIND_IGEMM_TC || s->kind == TP_KIND_IGEMM_TC_GATHER || s->kind == TP_KIND_IGEMM_TF32X3) {
     s->grid_x = (int32_t)cdiv(L.M, s->bm);
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = s->split_k;
@@ -237,6 +253,14 @@ static void enumerate(const Layer& L, F visit) {
         s.smem_stage = sm; s.split_k = 1; s.space_index = idx++;
         if (!visit(s)) return;
       }
+    if (tf32_kind_eligible(L))
+      for (int bm : kTcBM) for (int bn : kTcBN) for (int st : kTf32Stages) {
+        if (!valid_tf32(L, bm, bn, st)) continue;
+        tp_schedule s; std::memset(&s, 0, sizeof(s));
+        s.kind = TP_KIND_IGEMM_TF32X3; s.bm = bm; s.bn = bn; s.bk = 32; s.stages = st;
+        s.threads = 256; s.split_k = 1; s.space_index = idx++;
+        if (!visit(s)) return;
+      }
   }
 }
 
@@ -276,6 +300,9 @@ bool schedule_in_space(const Layer& L, const tp_schedule& s) {
     return row_kind_eligible(L) && in_(s.bm, kRowBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 64 &&
            in_(s.stages, kRowStages, 3) && in_(s.threads, kTcThreads, 2) && s.split_k == 1 &&
            in_(s.tiles_per_cta, kRowTpc, 5) && valid_row(L, s.bm, s.bn, s.stages, s.threads, s.tiles_per_cta);
+  if (s.kind == TP_KIND_IGEMM_TF32X3)
+    return tf32_kind_eligible(L) && in_(s.bm, kTcBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 32 &&
+           in_(s.stages, kTf32Stages, 3) && s.threads == 256 && s.split_k == 1 && valid_tf32(L, s.bm, s.bn, s.stages);
   if (s.kind != L.kind) return false;
   if (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) {
     auto in = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };

@@ -96,6 +96,7 @@ struct TcProblem {
   int row;         // 1: TP_KIND_IGEMM_TC_ROW (row-halo strips)
   int tpc;         // row-halo / multi-tile: tiles per CTA
   int mt;          // 1: TP_KIND_IGEMM_TC_MT (im2col multi-tile)
+  int tf32;        // 1: TP_KIND_IGEMM_TF32X3 (fp32 NHWC x, KRSC w; 3xTF32 split)
 };
 
 struct TcPlan {
@@ -108,6 +109,7 @@ struct TcPlan {
 };
 
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan);
+const void* pick_tf32(int bm, int bn);   // igemm_tf32.cu
 cudaError_t tc_launch(const TcPlan& plan, cudaStream_t stream);
 int tc_occupancy(const TcPlan& plan);
 size_t tc_dyn_smem(int bm, int bn, int bk, int stages);

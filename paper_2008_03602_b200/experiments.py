@@ -71,7 +71,9 @@ def roofline(d: dict, t_us: float, sm_granted: int, part_bw_gbs: float, floor_us
     tensor_peak = pk["bf16_tflops"] * 1e12 * share
     alu_peak = pk["fp32_tflops"] * 1e12 * share
     t = t_us * 1e-6
-    compute_peak = alu_peak if kind == tp.KIND_DIRECT else tensor_peak
+    # 3xTF32: dense tf32 runs at half the bf16 rate and every product costs 3 MMAs.
+    compute_peak = alu_peak if kind == tp.KIND_DIRECT else (tensor_peak / 6.0 if kind == tp.KIND_IGEMM_TF32X3
+                                                             else tensor_peak)
     roofs = {"compute_us": f / compute_peak * 1e6, "hbm_us": b / (part_bw_gbs * 1e9) * 1e6, "floor_us": floor_us}
     bound = max(roofs, key=roofs.get)
     return {"flops": f, "bytes": b, "tensor_frac": f / (t * tensor_peak), "alu_frac": f / (t * alu_peak),
@@ -98,6 +100,40 @@ def tune_layers(layers, bufs, part, trials=1000, seed=42, timing_cfg=None) -> li
         res.append({"layer": d["name"], "mult": d.get("mult", 1), "best": best, "best_m": m,
                     "candidates": len(recs), "ok": sum(1 for r in recs if r["status"] == 0), "wall_s": el})
     return res
+
+
+# the "Untuned" column of the paper's T1-T3
+# restated inside this framework -- a fixed, fraction-independent default
+# schedule, the one a user would pick without tuning: the valid schedule of the
+# layer's base kind closest (sum of |log2| distances, ties to the lowest index)
+# to a mid-range target tuple.
+DEFAULT_TC = {"bm": 128, "bn": 128, "bk": 64, "stages": 4, "threads": 128, "split_k": 1}
+DEFAULT_DIRECT = {"threads": 256, "tile_q": 2, "vec_k": 4, "tile_p": 2, "smem_stage": 1}
+
+
+def default_schedule(d: dict) -> dict:
+    """Fixed untuned schedule of layer d (host-only; see DEFAULT_TC / DEFAULT_DIRECT)."""
+    import math
+    kind = tp.layer_kind(d)
+    target = DEFAULT_DIRECT if kind == tp.KIND_DIRECT else DEFAULT_TC
+    best, best_key = None, None
+    for i in range(tp.space_size(d)):
+        s = tp.space_get(d, i)
+        if s["kind"] != kind:
+            continue
+        dist = sum(abs(math.log2(max(s[k], 0.5) / max(v, 0.5))) for k, v in target.items())
+        key = (dist, s["space_index"])
+        if best_key is None or key < best_key:
+            best, best_key = s, key
+    return best
+
+
+def aggregate_5k(model_sum_us: dict, fractions) -> dict:
+    """P:399 / P:472 (T4): 1000 batch-1 images inferred at each run fraction q
+    with the model tuned at p; total in ms = sum_q 1000 * model[p][q] us / 1000."""
+    tot = {str(p): sum(model_sum_us[str(p)][str(q)] for q in fractions) for p in fractions}
+    return {"images_per_fraction": 1000, "total_ms_by_tuned_at": tot,
+            "sweet_spot_tuned_at": min(fractions, key=lambda p: (tot[str(p)], p))}
 
 
 def partition_context(part) -> dict:
@@ -151,6 +187,19 @@ def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3,
                                                       "split_k", "tile_q", "vec_k", "tile_p", "smem_stage", "grid_x",
                                                       "grid_y", "grid_z")} for p in fractions},
                           "diag_roofline": {str(q): diag[q] for q in fractions}})
+    # f2: the untuned default schedule at every run fraction (frozen nothing:
+    # the default's geometry is derived at each q).
+    model_default = {q: 0.0 for q in fractions}
+    for li, d in enumerate(layers):
+        ds = default_schedule(d)
+        row = {}
+        for q in fractions:
+            row[str(q)] = tp.conv2d_run(bufs[li], ds, parts[q], timing_cfg or tp.timing())["median_us"]
+            model_default[q] += d.get("mult", 1) * row[str(q)]
+        per_layer[li]["default_us"] = row
+        per_layer[li]["default_schedule"] = {k: ds[k] for k in ("space_index", "kind", "bm", "bn", "bk", "stages",
+                                                                "threads", "split_k", "tile_q", "vec_k", "tile_p",
+                                                                "smem_stage")}
     # P-D: with exhaustive tuning the diagonal is the column minimum up to noise.
     viol = []
     for row in per_layer:
@@ -162,6 +211,10 @@ def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3,
     return {"fractions": list(fractions), "partitions": {str(f): ctx[f] for f in fractions}, "peaks": pk,
             "tune": {str(p): tune_stats[p] for p in fractions},
             "model_sum_us": {str(p): {str(q): model[p][q] for q in fractions} for p in fractions},
+            "model_sum_default_us": {str(q): model_default[q] for q in fractions},
+            "aggregate_5k": dict(aggregate_5k({str(p): {str(q): model[p][q] for q in fractions} for p in fractions},
+                                              fractions),
+                                 untuned_total_ms=sum(model_default[q] for q in fractions)),
             "diagonal_violations_gt10pct": viol, "layers": per_layer}
 
 

@@ -42,3 +42,29 @@ def test_roofline_fractions_and_binding():
     # the direct kind is measured against the FFMA roof
     r3 = ex.roofline(dd, 3.0, 148, 6000.0, 0.8, pk, 1)
     assert r3["roof_us"]["compute_us"] == pytest.approx(ex.layer_work(dd)[0] / 74e12 * 1e6)
+    # the 3xTF32 kind: tf32 at half the bf16 rate, three MMAs per product
+    r4 = ex.roofline(dd, 3.0, 148, 6000.0, 0.8, pk, 5)
+    assert r4["roof_us"]["compute_us"] == pytest.approx(ex.layer_work(dd)[0] / (1480e12 / 6) * 1e6)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "resnet50", "vgg19_b16", "mobilenetv2"])
+def test_default_schedule_is_valid_base_kind(name):
+    """f2 untuned column: one fixed schedule per layer, in the layer's space, of
+    its base kind, and the closest one to the documented target tuple."""
+    from paper_2008_03602_b200 import tp
+    for d in wl.catalog(name):
+        s = ex.default_schedule(d)
+        assert s is not None and s["kind"] == tp.layer_kind(d)
+        assert tp.space_get(d, s["space_index"]) == s
+        P, Q = tp.output_shape(d)
+        if s["kind"] == tp.KIND_IGEMM_TC and d["c"] >= 64 and d["k"] >= 128 and d["n"] * P * Q >= 128:
+            # the target tuple itself is valid for these layers
+            assert (s["bm"], s["bn"], s["bk"], s["stages"], s["split_k"]) == (128, 128, 64, 4, 1)
+
+
+def test_aggregate_5k_sweet_spot():
+    fr = (0.1, 0.25, 0.5, 1.0)
+    m = {str(p): {str(q): 100.0 * (1 + abs(p - q)) / q for q in fr} for p in fr}
+    a = ex.aggregate_5k(m, fr)
+    assert a["total_ms_by_tuned_at"]["0.25"] == pytest.approx(sum(m["0.25"][str(q)] for q in fr))
+    assert a["sweet_spot_tuned_at"] == min(fr, key=lambda p: sum(m[str(p)][str(q)] for q in fr))

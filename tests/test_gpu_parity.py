@@ -243,3 +243,55 @@ def test_timed_launches_weight_prefetch_bit_exact_integer(d):
         if m["status"] != 0 or not np.array_equal(buf.output(), ref):
             bad.append((i, s["kind"], s["bm"], s["bn"], s["bk"], s["stages"], s["split_k"]))
     assert not bad, f"{len(bad)}/{n} timed schedules differ, first: {bad[:5]}"
+
+
+# ------------------------------------------------------------------ 3xTF32 tensor-core kind
+TF32_TINY = [mk(1, 64, 10, 9, 64, 3, 3, 1, 1, dtype=tp.FP32, epi=1),    # ragged M tail
+             mk(2, 36, 7, 7, 48, 1, 1, 1, 0, dtype=tp.FP32, epi=1),     # 1x1/s1/p0: tiled A; C = 32 + 4
+             mk(1, 4, 9, 11, 40, 3, 3, 2, 1, dtype=tp.FP32, epi=1),     # one partial channel block, stride 2
+             mk(1, 96, 6, 7, 256, 3, 3, 1, 1, dtype=tp.FP32, epi=1)]    # BN up to 256, 3 channel blocks
+
+
+def _tf32_scheds(d):
+    out = [tp.space_get(d, i) for i in range(tp.space_size(d))]
+    out = [s for s in out if s["kind"] == tp.KIND_IGEMM_TF32X3]
+    assert out, "layer has no 3xTF32 schedules"
+    return out
+
+
+@pytest.mark.parametrize("d", TF32_TINY, ids=lambda d: f"tf32_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_r{d['r']}s{d['stride_h']}")
+def test_tf32x3_every_schedule_bit_exact_integer(d):
+    """Integers in {-3..3} are exact tf32 values (lo parts are 0) and every
+    partial sum is an fp32 integer, so every 3xTF32 schedule equals the oracle
+    bit-exactly (O11)."""
+    x, w, b = datagen.make_inputs(d, 21, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    bad = []
+    for s in _tf32_scheds(d):
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        if not np.array_equal(buf.output(), ref):
+            bad.append((s["space_index"], s["bm"], s["bn"], s["stages"]))
+    assert not bad, f"{len(bad)} tf32 schedules differ, first: {bad[:5]}"
+
+
+@pytest.mark.parametrize("d", TF32_TINY + [dict(wl.catalog("cfg1")[0], epilogue=3)],
+                         ids=lambda d: f"tf32r_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_e{d['epilogue']}")
+def test_tf32x3_random_parity_fp32_bar(d):
+    """Random fp32 data: the hi/lo split keeps every schedule within the fp32
+    bar of north_star (1e-5, reading C10/C11), which a single tf32 product
+    (~1e-3) would miss."""
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(1, 5))
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    worst = 0.0
+    for s in _tf32_scheds(d):
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        err = rel_err(buf.output(), ref)
+        worst = max(worst, err)
+        assert err <= 1e-5, (s, err)
+    assert worst > 0.0 or d["c"] <= 4   # random data does round somewhere
