@@ -34,7 +34,7 @@ TC_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("bk", (16, 32, 64, 1
 ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)), ("threads", (128, 256)),
              ("tiles_per_cta", (1, 2, 4, 8, 16)))
 MT_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("tiles_per_cta", (2, 4, 8)))
-TF32_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)))
+TF32_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("split_k", (1, 2, 4, 8)))
 DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
                 ("tile_p", (1, 2, 4, 8)), ("smem_stage", (0, 1)))
 
@@ -165,14 +165,18 @@ def tf32_eligible(d: dict) -> bool:
             and d["c"] % 4 == 0 and d["k"] % 8 == 0)
 
 
-def _valid_tf32(d: dict, bm: int, bn: int, stages: int) -> bool:
-    # ring: stages x (A + B) tiles of 32 fp32 channels (128-B rows), hi and lo copies
+def _valid_tf32(d: dict, bm: int, bn: int, stages: int, split_k: int) -> bool:
+    # ring: stages x (A + B) tiles of 32 fp32 channels (128-B rows), hi and lo copies;
+    # split-K adds the cluster receive buffer of bm rows x (bn + 4) fp32
     P, Q = out_pq(d)
-    if stages * (bm + bn) * 32 * 4 * 2 + 1024 > SMEM_LIMIT:
+    recv = bm * (bn + 4) * 4 if split_k > 1 else 0
+    if stages * (bm + bn) * 32 * 4 * 2 + recv + 1024 > SMEM_LIMIT:
         return False
     if bn > max(32, _np2(d["k"])):
         return False
-    return bm <= max(64, _np2(d["n"] * P * Q))
+    if bm > max(64, _np2(d["n"] * P * Q)):
+        return False
+    return split_k <= d["r"] * d["s"] * _cdiv(d["c"], 32)
 
 
 def enumerate_space(d: dict) -> list[dict]:
@@ -200,7 +204,7 @@ def enumerate_space(d: dict) -> list[dict]:
     if tf32_eligible(d):         # appended after the direct tuples; bk = 32, threads = 256, split_k = 1
         for combo in itertools.product(*[v for _, v in TF32_KNOBS]):
             if _valid_tf32(d, *combo):
-                s = dict(zip([k for k, _ in TF32_KNOBS], combo), bk=32, threads=256, split_k=1,
+                s = dict(zip([k for k, _ in TF32_KNOBS], combo), bk=32, threads=256,
                          kind=KIND_IGEMM_TF32X3, space_index=len(out))
                 s.update(geometry(d, s))
                 out.append(s)

@@ -911,24 +911,36 @@ static tp_status tf32_prepare(const TcProblem& pb, bool a_tiled, TcPlan* plan) {
   std::memset(&a, 0, sizeof(a));
   a.M = pb.M; a.K = pb.K; a.P = pb.P; a.Q = pb.Q; a.S = pb.S;
   a.sh = pb.sh; a.sw = pb.sw; a.ph = pb.ph; a.pw = pb.pw;
-  a.bk = 32; a.stages = pb.stages; a.split_k = 1;
+  a.bk = 32; a.stages = pb.stages; a.split_k = pb.split_k > 1 ? pb.split_k : 1;
   a.cblocks = (pb.C + 31) / 32;
   a.kblocks = pb.R * pb.S * a.cblocks;
   a.H = pb.H; a.W = pb.W; a.C = pb.C; a.Kg = pb.R * pb.S * pb.C;
   a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
   a.a_tiled = a_tiled ? 1 : 0;
-  a.bar_off = (int)((size_t)pb.stages * (pb.bm + pb.bn) * 256);   // hi + lo rings, 1 KiB multiples
+  a.dbg = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
+  // [hi rings][lo rings][split-K receive buffer BM x (BN + 4) fp32][barriers]; all 1 KiB multiples.
+  a.recv_off = (int)((size_t)pb.stages * (pb.bm + pb.bn) * 256);
+  a.bar_off = a.recv_off + (a.split_k > 1 ? pb.bm * (pb.bn + 4) * 4 : 0);
+  a.cluster_red = a.split_k > 1 ? 1 : 0;
   plan->fn = pick_tf32(pb.bm, pb.bn);
   if (!plan->fn) { set_error("no igemm_tf32 instantiation for this BM x BN"); return TP_EINVALID_CONFIG; }
-  plan->grid = dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u);
+  plan->grid = dim3((unsigned)((pb.M + pb.bm - 1) / pb.bm), (unsigned)((pb.K + pb.bn - 1) / pb.bn),
+                    (unsigned)a.split_k);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
   plan->block = dim3(256);
-  plan->cluster_z = 1;
+  plan->cluster_z = a.split_k;
   plan->smem = (size_t)a.bar_off + 1024;
   cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
   if (e != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     return TP_ECUDA;
+  }
+  // Split-K reduces only through DSMEM: the (1, 1, split_k) cluster must be
+  // co-schedulable in the current context (green contexts may not be able to).
+  if (a.split_k > 1 && (plan->grid.z % (unsigned)a.split_k != 0 ||
+                        cached_max_clusters(plan->fn, 256, plan->smem, a.split_k) <= 0)) {
+    set_error("3xTF32 split-K cluster cannot be co-scheduled in this context");
+    return TP_EUNSUPPORTED;
   }
   return TP_OK;
 }

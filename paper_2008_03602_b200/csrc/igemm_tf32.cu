@@ -54,15 +54,18 @@ __global__ void __launch_bounds__(256) igemm_tf32_kernel(const __grid_constant__
   uint64_t* ready = full + stages;
   uint64_t* empty = ready + stages;
   uint64_t* tmem_full = empty + stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* red_bar = tmem_full + 1;   // split-K: every peer's partial rows landed in this CTA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_bar + 1);
 
-  const int m_tile = blockIdx.x, n_tile = blockIdx.y;
+  const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
   const int m0 = m_tile * BM;
   const int q0 = m0 % a.Q, t0 = m0 / a.Q;
   const int p0 = t0 % a.P, n0 = t0 / a.P;
   const int cw = q0 * a.sw - a.pw, ch = p0 * a.sh - a.ph;
   const int nbase = n_tile * BN;
-  const int nkb = a.kblocks;
+  // This split's k-blocks (a k-block = 32-channel block cb of filter tap (r, s), cb fastest).
+  const int kb0 = (split * a.kblocks) / a.split_k, kb1 = ((split + 1) * a.kblocks) / a.split_k;
+  const int rows_per = BM / a.split_k;   // split-K: output rows this CTA owns and reduces
 
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem_raw) & 1023u) != 0) __trap();   // swizzle atoms need 1 KiB alignment
@@ -72,6 +75,8 @@ __global__ void __launch_bounds__(256) igemm_tf32_kernel(const __grid_constant__
       mbar_init(empty + i, 1);
     }
     mbar_init(tmem_full, 1);
+    mbar_init(red_bar, 1);
+    if (a.split_k > 1) mbar_arrive_expect_tx(red_bar, (uint32_t)((a.split_k - 1) * rows_per * BN * 4));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
@@ -85,6 +90,8 @@ __global__ void __launch_bounds__(256) igemm_tf32_kernel(const __grid_constant__
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Publish the reduction barrier to the cluster (waited on before the first remote store).
+  if (a.split_k > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   // Every warp sleeps in the PDL wait (no operand is touched before it).
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -93,9 +100,10 @@ __global__ void __launch_bounds__(256) igemm_tf32_kernel(const __grid_constant__
     // ---------------- TMA producer ----------------
     const uint32_t lead = elect_one();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    int cb = 0, s = 0, r = 0, stage = 0;
+    const int rs = kb0 / a.cblocks;
+    int cb = kb0 - rs * a.cblocks, s = rs % a.S, r = rs / a.S, stage = 0;
     uint32_t phase = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(empty + stage, phase ^ 1u);
       mbar_arrive_expect_tx_p(full + stage, A_T + B_T, lead);
       if (a.a_tiled)
@@ -117,16 +125,18 @@ __global__ void __launch_bounds__(256) igemm_tf32_kernel(const __grid_constant__
     const uint64_t alo0 = make_sdesc(smem_u32(a_lo), 128), blo0 = make_sdesc(smem_u32(b_lo), 128);
     int stage = 0;
     uint32_t phase = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(ready + stage, phase);
       tc_fence_after();
       const uint32_t oa = (uint32_t)(stage * A_T) >> 4, ob = (uint32_t)(stage * B_T) >> 4;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {   // 4 k-steps of 8 tf32 (32 B) per 128-B row
         const uint32_t ko = (uint32_t)(kk * 32) >> 4;
-        tc_mma_tf32_p(tmem_base, ahi0 + oa + ko, bhi0 + ob + ko, IDESC, (kb > 0 || kk > 0) ? 1u : 0u, lead);
-        tc_mma_tf32_p(tmem_base, ahi0 + oa + ko, blo0 + ob + ko, IDESC, 1u, lead);
-        tc_mma_tf32_p(tmem_base, alo0 + oa + ko, bhi0 + ob + ko, IDESC, 1u, lead);
+        tc_mma_tf32_p(tmem_base, ahi0 + oa + ko, bhi0 + ob + ko, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u, lead);
+        if (!(a.dbg & 8)) {   // dbg bit3 (experiments only): 1xTF32
+          tc_mma_tf32_p(tmem_base, ahi0 + oa + ko, blo0 + ob + ko, IDESC, 1u, lead);
+          tc_mma_tf32_p(tmem_base, alo0 + oa + ko, bhi0 + ob + ko, IDESC, 1u, lead);
+        }
       }
       tc_commit_p(empty + stage, lead);
       if (++stage == stages) { stage = 0; phase ^= 1u; }
@@ -135,28 +145,48 @@ __global__ void __launch_bounds__(256) igemm_tf32_kernel(const __grid_constant__
   } else if (warp >= 4) {
     // ---------------- hi/lo split of each landed stage ----------------
     const int t = threadIdx.x - 128;
-    constexpr int kA = (int)(A_T / 16), kB = (int)(B_T / 16);   // 16-byte chunks
     int stage = 0;
     uint32_t phase = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(full + stage, phase);
       uint4* ah = reinterpret_cast<uint4*>(a_hi + (size_t)stage * A_T);
       uint4* al = reinterpret_cast<uint4*>(a_lo + (size_t)stage * A_T);
       uint4* bh = reinterpret_cast<uint4*>(b_hi + (size_t)stage * B_T);
       uint4* bl = reinterpret_cast<uint4*>(b_lo + (size_t)stage * B_T);
-#pragma unroll 4
-      for (int i = t; i < kA + kB; i += 128) {
-        uint4* hp = i < kA ? ah + i : bh + (i - kA);
-        uint4* lp = i < kA ? al + i : bl + (i - kA);
-        const uint4 v = *hp;
-        uint4 h, l;
-        h.x = v.x & 0xFFFFE000u; h.y = v.y & 0xFFFFE000u; h.z = v.z & 0xFFFFE000u; h.w = v.w & 0xFFFFE000u;
-        l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(h.x));
-        l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(h.y));
-        l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(h.z));
-        l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(h.w));
-        *hp = h;
-        *lp = l;
+      // Thread t owns chunks t + 128 J, J < PER; chunk J is in A iff J < BM / 16
+      // (BM * 8 chunks of A, a multiple of 128).  Batches of loads are issued
+      // before any store (the compiler cannot prove hi/lo stores do not alias
+      // the next loads).
+      if (!(a.dbg & 4)) {   // dbg bit2 (experiments only): no split work
+        constexpr int PER = (BM + BN) / 16, BATCH = PER < 8 ? PER : 8;
+#pragma unroll
+        for (int j0 = 0; j0 < PER; j0 += BATCH) {
+          uint4 v[BATCH];
+#pragma unroll
+          for (int j = 0; j < BATCH; ++j) {
+            const int J = j0 + j;
+            if (J < PER) v[j] = J < BM / 16 ? ah[t + J * 128] : bh[t + (J - BM / 16) * 128];
+          }
+#pragma unroll
+          for (int j = 0; j < BATCH; ++j) {
+            const int J = j0 + j;
+            if (J >= PER) break;
+            uint4 h, l;
+            h.x = v[j].x & 0xFFFFE000u; h.y = v[j].y & 0xFFFFE000u;
+            h.z = v[j].z & 0xFFFFE000u; h.w = v[j].w & 0xFFFFE000u;
+            l.x = __float_as_uint(__uint_as_float(v[j].x) - __uint_as_float(h.x));
+            l.y = __float_as_uint(__uint_as_float(v[j].y) - __uint_as_float(h.y));
+            l.z = __float_as_uint(__uint_as_float(v[j].z) - __uint_as_float(h.z));
+            l.w = __float_as_uint(__uint_as_float(v[j].w) - __uint_as_float(h.w));
+            if (J < BM / 16) {
+              ah[t + J * 128] = h;
+              al[t + J * 128] = l;
+            } else {
+              bh[t + (J - BM / 16) * 128] = h;
+              bl[t + (J - BM / 16) * 128] = l;
+            }
+          }
+        }
       }
       // generic-proxy smem writes -> visible to the tensor core (async proxy)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -177,24 +207,79 @@ __global__ void __launch_bounds__(256) igemm_tf32_kernel(const __grid_constant__
   __syncwarp();
   mbar_wait(tmem_full, 0);
   tc_fence_after();
-  for (int c = c_begin; c < c_end; c += 16) {
-    uint32_t raw[16];
-    tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c, raw);
-    const int nb = nbase + c;
-    if (m_ok && nb < a.K) {
-      float v[16];
+  auto bias_relu = [&](int nb, float (&v)[16]) {
 #pragma unroll
-      for (int g = 0; g < 16; g += 4) {
-        float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (a.has_bias && nb + g + 4 <= a.K) bv = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
-        const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
+    for (int g = 0; g < 16; g += 4) {
+      float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a.has_bias && nb + g + 4 <= a.K) bv = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
+      const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float t = __uint_as_float(raw[g + j]) + b4[j];
-          v[g + j] = a.relu ? fmaxf(t, 0.0f) : t;
+      for (int j = 0; j < 4; ++j) {
+        const float t = v[g + j] + b4[j];
+        v[g + j] = a.relu ? fmaxf(t, 0.0f) : t;
+      }
+    }
+  };
+  if (a.split_k == 1) {
+    for (int c = c_begin; c < c_end; c += 16) {
+      uint32_t raw[16];
+      tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c, raw);
+      const int nb = nbase + c;
+      if (m_ok && nb < a.K) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[j]);
+        bias_relu(nb, v);
+        store16(a.y, m, a.K, nb, v, a.out_f32);
+      }
+    }
+  } else {
+    // Split-K through DSMEM (as igemm_tc.cu): every row segment goes to the
+    // CTA of the cluster that owns the row (st.async completing bytes on the
+    // owner's red_bar; a plain shared store for own rows); the owner sums the
+    // split_k slices in split order (deterministic), adds bias, applies ReLU.
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    float* recv = reinterpret_cast<float*>(smem_raw + a.recv_off);
+    for (int c = c_begin; c < c_end; c += 16) {
+      uint32_t raw[16];
+      tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c, raw);
+      if (row_ok) {
+        const int owner = row / rows_per;
+        float* slot = recv + (split * rows_per + (row - owner * rows_per)) * (BN + 4) + c;
+        if (owner == split) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<uint4*>(slot + i) = make_uint4(raw[i], raw[i + 1], raw[i + 2], raw[i + 3]);
+        } else {
+          const uint32_t rdst = mapa_u32(smem_u32(slot), (uint32_t)owner);
+          const uint32_t rbar = mapa_u32(smem_u32(red_bar), (uint32_t)owner);
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) st_async_v4(rdst + i * 4, raw[i], raw[i + 1], raw[i + 2], raw[i + 3], rbar);
         }
       }
-      store16(a.y, m, a.K, nb, v, a.out_f32);
+    }
+    const bool owns = row_ok && (row / rows_per) == split;
+    mbar_wait(red_bar, 0);
+    __syncthreads();   // own-row plain stores of the other warps are visible
+    if (owns && m < a.M) {
+      const float* mine = recv + (row - split * rows_per) * (BN + 4);
+      for (int c = c_begin; c < c_end; c += 16) {
+        const int nb = nbase + c;
+        if (nb >= a.K) continue;
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+        for (int j = 0; j < a.split_k; ++j) {
+          const float* sl = mine + j * rows_per * (BN + 4) + c;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(sl + i);
+            v[i] += t.x; v[i + 1] += t.y; v[i + 2] += t.z; v[i + 3] += t.w;
+          }
+        }
+        bias_relu(nb, v);
+        store16(a.y, m, a.K, nb, v, a.out_f32);
+      }
     }
   }
   tc_fence_before();

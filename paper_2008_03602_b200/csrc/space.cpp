@@ -176,17 +176,23 @@ static bool valid_row(const Layer& L, int bm, int bn, int stages, int threads, i
 // 3xTF32 tensor-core kind for fp32 dense layers: fp32 NHWC x
 // and KRSC w are TMA-loaded (32-channel k-blocks, 128-B rows), split in shared
 // memory into tf32 hi/lo parts, and D += A_hi B_hi + A_hi B_lo + A_lo B_hi on
-// tcgen05 kind::tf32; appended after the direct tuples; 256 threads, split 1.
+// tcgen05 kind::tf32; appended after the direct tuples; 256 threads.  Split-K
+// (1, 2, 4, 8) reduces through DSMEM in a (1, 1, split_k) cluster: the fp32
+// receive buffer (BM x (BN + 4) x 4 B) sits after the rings and counts toward
+// the shared-memory limit; split_k <= k-blocks = R S ceil(C / 32).
 bool tf32_kind_eligible(const Layer& L) {
   const tp_conv_desc& d = L.d;
   return L.kind == TP_KIND_DIRECT && d.dtype == TP_DTYPE_FP32 && d.groups == 1 && d.c % 4 == 0 && d.k % 8 == 0;
 }
 static const int kTf32Stages[] = {2, 3, 4};
-int64_t tf32_smem_bytes(int bm, int bn, int stages) { return (int64_t)stages * (bm + bn) * 128 * 2 + 1024; }
-static bool valid_tf32(const Layer& L, int bm, int bn, int stages) {
-  if (tf32_smem_bytes(bm, bn, stages) > kSmemLimit) return false;
+int64_t tf32_smem_bytes(int bm, int bn, int stages, int split) {
+  return (int64_t)stages * (bm + bn) * 128 * 2 + (split > 1 ? (int64_t)bm * (bn + 4) * 4 : 0) + 1024;
+}
+static bool valid_tf32(const Layer& L, int bm, int bn, int stages, int split) {
+  if (tf32_smem_bytes(bm, bn, stages, split) > kSmemLimit) return false;
   if (bn > std::max<int64_t>(32, np2(L.d.k))) return false;
-  return bm <= std::max<int64_t>(64, np2(L.M));
+  if (bm > std::max<int64_t>(64, np2(L.M))) return false;
+  return split <= (int64_t)L.d.r * L.d.s * cdiv(L.d.c, 32);
 }
 
 void fill_geometry(const Layer& L, tp_schedule* s) {
@@ -254,11 +260,11 @@ static void enumerate(const Layer& L, F visit) {
         if (!visit(s)) return;
       }
     if (tf32_kind_eligible(L))
-      for (int bm : kTcBM) for (int bn : kTcBN) for (int st : kTf32Stages) {
-        if (!valid_tf32(L, bm, bn, st)) continue;
+      for (int bm : kTcBM) for (int bn : kTcBN) for (int st : kTf32Stages) for (int sk : kTcSplit) {
+        if (!valid_tf32(L, bm, bn, st, sk)) continue;
         tp_schedule s; std::memset(&s, 0, sizeof(s));
         s.kind = TP_KIND_IGEMM_TF32X3; s.bm = bm; s.bn = bn; s.bk = 32; s.stages = st;
-        s.threads = 256; s.split_k = 1; s.space_index = idx++;
+        s.threads = 256; s.split_k = sk; s.space_index = idx++;
         if (!visit(s)) return;
       }
   }
@@ -302,7 +308,8 @@ bool schedule_in_space(const Layer& L, const tp_schedule& s) {
            in_(s.tiles_per_cta, kRowTpc, 5) && valid_row(L, s.bm, s.bn, s.stages, s.threads, s.tiles_per_cta);
   if (s.kind == TP_KIND_IGEMM_TF32X3)
     return tf32_kind_eligible(L) && in_(s.bm, kTcBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 32 &&
-           in_(s.stages, kTf32Stages, 3) && s.threads == 256 && s.split_k == 1 && valid_tf32(L, s.bm, s.bn, s.stages);
+           in_(s.stages, kTf32Stages, 3) && s.threads == 256 && in_(s.split_k, kTcSplit, 4) &&
+           valid_tf32(L, s.bm, s.bn, s.stages, s.split_k);
   if (s.kind != L.kind) return false;
   if (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) {
     auto in = [](int v, const int* a, int n) { return std::find(a, a + n, v) != a + n; };

@@ -38,7 +38,7 @@ int64_t tcg_table_bytes(const Layer& L, int bm, int bk);   // gather kind: pixel
 bool row_kind_eligible(const Layer& L);                     // row-halo kind applies
 bool mt_kind_eligible(const Layer& L);                      // multi-tile im2col kind applies
 bool tf32_kind_eligible(const Layer& L);                    // 3xTF32 tensor-core kind applies (fp32 dense)
-int64_t tf32_smem_bytes(int bm, int bn, int stages);
+int64_t tf32_smem_bytes(int bm, int bn, int stages, int split);
 int64_t row_stage_bytes(int bm, int bn);                    // row-halo kind: one pipeline stage
 bool schedule_in_space(const Layer& L, const tp_schedule& s);
 

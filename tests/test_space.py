@@ -114,23 +114,28 @@ def test_mt_kind_hand_count():
 
 def test_tf32_kind_hand_count():
     # cfg1 (fp32, C = K = 64, 56x56, 3x3): eligible (C % 4 == 0, K % 8 == 0, g = 1).  BM {64, 128}
-    # (M = 3136), BN <= max(32, np2(64)) -> {32, 64}, stages {2, 3, 4}; smem = stages (BM+BN) 256 + 1024
-    # fits for all (max 4 x 192 x 256 + 1024 = 197632): 2 x 2 x 3 = 12, appended after the direct tuples.
+    # (M = 3136), BN <= max(32, np2(64)) -> {32, 64}, stages {2, 3, 4}, split_k {1, 2, 4, 8} (<= 9 taps x
+    # 2 channel blocks); smem = stages (BM+BN) 256 + [split > 1] BM (BN+4) 4 + 1024 fits for all (max
+    # 4 x 192 x 256 + 128 x 68 x 4 + 1024 = 232448 = the limit): 2 x 2 x 3 x 4 = 48, after the direct tuples.
     d = wl.catalog("cfg1")[0]
     space = sp.enumerate_space(d)
     tf = [x for x in space if x["kind"] == sp.KIND_IGEMM_TF32X3]
-    assert len(tf) == 12 and space[-12:] == tf
-    assert all(x["bk"] == 32 and x["threads"] == 256 and x["split_k"] == 1 for x in tf)
-    x = [t for t in tf if t["bm"] == 128 and t["bn"] == 64 and t["stages"] == 3][0]
-    assert (x["grid_x"], x["grid_y"], x["grid_z"]) == (-(-3136 // 128), 1, 1)
+    assert len(tf) == 48 and space[-48:] == tf
+    assert all(x["bk"] == 32 and x["threads"] == 256 for x in tf)
+    x = [t for t in tf if t["bm"] == 128 and t["bn"] == 64 and t["stages"] == 3 and t["split_k"] == 4][0]
+    assert (x["grid_x"], x["grid_y"], x["grid_z"]) == (-(-3136 // 128), 1, 4)
     # not eligible: bf16 layers, C % 4 != 0, K % 8 != 0, depthwise
     e = dict(d)
     assert not sp.tf32_eligible(dict(e, c=3)) and not sp.tf32_eligible(dict(e, k=60))
     assert not sp.tf32_eligible(dict(e, groups=64)) and not sp.tf32_eligible(dict(e, dtype=sp.DTYPE_BF16))
-    # BN = 256 at BM = 128 fits only with 2 stages (3 x 384 x 256 + 1024 = 295936 > 232448)
+    # BN = 256 at BM = 128 fits only with 2 stages (3 x 384 x 256 + 1024 = 295936 > 232448), and then
+    # only without the split-K receive buffer (197632 + 128 x 260 x 4 = 330752 > 232448)
     big = dict(e, k=256, h=16, w=16)
     tf2 = [x for x in sp.enumerate_space(big) if x["kind"] == sp.KIND_IGEMM_TF32X3]
-    assert [x["stages"] for x in tf2 if x["bn"] == 256 and x["bm"] == 128] == [2]
+    assert [(x["stages"], x["split_k"]) for x in tf2 if x["bn"] == 256 and x["bm"] == 128] == [(2, 1)]
+    # split_k <= k-blocks: a 1x1 layer with C = 36 has 2 k-blocks
+    one = dict(e, c=36, r=1, s=1, pad_h=0, pad_w=0)
+    assert {x["split_k"] for x in sp.enumerate_space(one) if x["kind"] == sp.KIND_IGEMM_TF32X3} == {1, 2}
 
 
 def test_kind_selection():
