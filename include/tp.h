@@ -159,6 +159,12 @@ tp_status tp_partition_get(int32_t device, double fraction, int32_t flags, tp_pa
  * tuners).  parts[k], granted[k] filled.  Not cached: close each. */
 tp_status tp_partition_split(int32_t device, int32_t k, int32_t sms_each, int32_t flags,
                              tp_partition** parts, int32_t* granted);
+/* k UNPARTITIONED handles on the whole device (the default-MPS
+ * analog -- concurrent tuners with no SM isolation): each has its own
+ * non-blocking stream in the primary context and sm_granted = the device's SM
+ * count; the SMs are shared by whatever runs concurrently.  parts[k] filled.
+ * Not cached: close each with tp_partition_close. */
+tp_status tp_partition_shared(int32_t device, int32_t k, tp_partition** parts);
 tp_status tp_partition_info(tp_partition* part, int32_t* device, int32_t* sm_requested,
                             int32_t* sm_granted, void** cu_stream);
 tp_status tp_partition_sync(tp_partition* part);

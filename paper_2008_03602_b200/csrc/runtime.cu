@@ -1051,6 +1051,25 @@ tp_status tp_partition_split(int32_t device, int32_t k, int32_t sms_each, int32_
   return TP_OK;
 }
 
+tp_status tp_partition_shared(int32_t device, int32_t k, tp_partition** parts) {
+  if (k < 1 || !parts) { set_error("bad shared-partition arguments"); return TP_EINVAL; }
+  DeviceState* ds = nullptr;
+  tp_status st = init_device(device, &ds);
+  if (st != TP_OK) return st;
+  TP_CK(cudaSetDevice(device));
+  for (int i = 0; i < k; ++i) {
+    auto p = std::make_unique<tp_partition>();
+    p->device = device; p->fraction = 1.0; p->flags = 0;
+    p->sm_requested = p->sm_granted = ds->sm_count;
+    p->green = false; p->cached = false; p->ctx = ds->primary;
+    TP_CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->flush_buf = ds->flush_buf;
+    p->flush_bytes = ds->flush_bytes;
+    parts[i] = p.release();
+  }
+  return TP_OK;
+}
+
 tp_status tp_partition_info(tp_partition* part, int32_t* device, int32_t* req, int32_t* gr, void** stream) {
   if (!part) { set_error("null partition"); return TP_EINVAL; }
   if (device) *device = part->device;

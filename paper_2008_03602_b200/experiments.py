@@ -312,3 +312,117 @@ def concurrent_tune(layers, k=4, sms_each=37, trials=1000, config=4, timing_cfg=
     return {"k": k, "sms_each_requested": sms_each, "sms_each_split": asked, "partitions": ctx, "peaks": pk, "wall_s": wall, "candidates": n,
             "candidates_per_s": n / wall, "per_tuner_wall_s": [results[j]["wall_s"] for j in range(k)],
             "assignment": [[layers[i]["name"] for i in a] for a in assign], "layers": layers_out}
+
+
+# ---------------------------------------------------------------------------------------------
+# interference.  The paper keeps concurrent tuners apart with a
+# fixed GPU% per server because "temporally sharing GPU for multiple tuning
+# process will result in wrong latency being reported during profiling ...
+# uncontrolled spatial sharing using default MPS does not provide hardware
+# isolation" (appendix P:1103-1113 [src]).  Three ways to run k
+# tuners on one GPU, each tuning its LPT share of the layers:
+#   isolated    -- k disjoint green contexts (SM isolation; L2/HBM still shared)
+#   shared      -- k streams on the whole device, no partition (default-MPS analog)
+#   time_sliced -- k processes, one CUDA context each, no MPS (the driver time-slices)
+# Each mode's winners are then re-timed alone on the target they were tuned for
+# (a partition of the same size for `isolated`, the whole idle device otherwise):
+# `report_err` = reported / solo latency - 1 (what the tuner believed vs what
+# the schedule does alone), `choice_loss` = solo latency of the mode's winner /
+# solo latency of the winner of a tuner that ran alone - 1.
+
+
+def _tune_share(layer_ids, layers, part, trials, config, seed):
+    out = {}
+    for i in layer_ids:
+        d = layers[i]
+        x, w, b = datagen.make_inputs(d, datagen.data_seed(config, i))
+        buf = tp.LayerBuffers(d, x, w, b, part=part)
+        best, m, recs = tp.tune(buf, part, trials, seed)
+        out[i] = {"space_index": int(best["space_index"]), "reported_us": float(m["median_us"]),
+                  "candidates": len(recs)}
+    return out
+
+
+def _time_sliced_worker(args):
+    layer_ids, cat, trials, config, seed, device = args
+    from . import workloads as wl
+    tp.init(device)
+    layers = wl.catalog(cat)
+    return _tune_share(layer_ids, layers, tp.Partition.get(1.0, device=device), trials, config, seed)
+
+
+def interference(cat: str, k: int = 4, sms_each: int = 36, trials: int = 1000, config: int = 6,
+                 modes=("isolated", "shared", "time_sliced"), device: int = 0, log=print) -> dict:
+    from . import workloads as wl
+    layers = wl.catalog(cat)
+    assign = _lpt(layers, k)
+    seed = datagen.sampler_seed(0)
+    timing = tp.timing()
+
+    def solo_time(part, i, idx):
+        d = layers[i]
+        x, w, b = datagen.make_inputs(d, datagen.data_seed(config, i))
+        buf = tp.LayerBuffers(d, x, w, b, part=part)
+        return tp.conv2d_run(buf, tp.space_get(d, idx), part, timing)["median_us"]
+
+    res = {"catalog": cat, "k": k, "assignment": [[layers[i]["name"] for i in a] for a in assign], "modes": {}}
+    # Ground truth: one tuner alone on each target (a sms_each partition; the whole device).
+    iso_parts = tp.Partition.split(k, sms_each, device=device)
+    whole = tp.Partition.get(1.0, device=device)
+    alone = {"partition": _tune_share(range(len(layers)), layers, iso_parts[0], trials, config, seed),
+             "whole": _tune_share(range(len(layers)), layers, whole, trials, config, seed)}
+    for mode in modes:
+        t0 = time.perf_counter()
+        results = [None] * k
+        if mode == "time_sliced":
+            import multiprocessing as mp
+            with mp.get_context("spawn").Pool(k) as pool:
+                results = pool.map(_time_sliced_worker, [(a, cat, trials, config, seed, device) for a in assign])
+        else:
+            parts = iso_parts if mode == "isolated" else tp.Partition.shared(k, device=device)
+            errs = []
+
+            def worker(j):
+                try:
+                    results[j] = _tune_share(assign[j], layers, parts[j], trials, config, seed)
+                except Exception as e:   # surfaced below
+                    errs.append(repr(e))
+
+            th = [threading.Thread(target=worker, args=(j,)) for j in range(k)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            if mode == "shared":
+                for p in parts:
+                    p.close()
+            if errs:
+                raise RuntimeError("; ".join(errs))
+        wall = time.perf_counter() - t0
+        target = iso_parts[0] if mode == "isolated" else whole
+        ref = alone["partition"] if mode == "isolated" else alone["whole"]
+        rows = []
+        for j in range(k):
+            for i, r in results[j].items():
+                solo = solo_time(target, i, r["space_index"])
+                ref_solo = solo_time(target, i, ref[i]["space_index"])
+                rows.append({"layer": layers[i]["name"], "mult": layers[i].get("mult", 1), "tuner": j,
+                             "space_index": r["space_index"], "reported_us": r["reported_us"], "solo_us": solo,
+                             "alone_winner_solo_us": ref_solo, "report_err": r["reported_us"] / solo - 1.0,
+                             "choice_loss": solo / ref_solo - 1.0})
+        n = sum(r["candidates"] for res_j in results for r in res_j.values())
+        msum = sum(r["mult"] * r["solo_us"] for r in rows)
+        msum_ref = sum(r["mult"] * r["alone_winner_solo_us"] for r in rows)
+        res["modes"][mode] = {
+            "wall_s": wall, "candidates": n, "candidates_per_s": n / wall,
+            "target": f"{sms_each}-SM partition" if mode == "isolated" else "whole device",
+            "mean_abs_report_err": sum(abs(r["report_err"]) for r in rows) / len(rows),
+            "max_abs_report_err": max(abs(r["report_err"]) for r in rows),
+            "changed_winners": sum(1 for r in rows if r["choice_loss"] > 0.02),
+            "model_sum_solo_us": msum, "model_sum_alone_tuned_us": msum_ref,
+            "model_choice_loss": msum / msum_ref - 1.0, "layers": rows}
+        log(f"{mode}: {n} candidates in {wall:.1f}s, mean |report err| "
+            f"{res['modes'][mode]['mean_abs_report_err']:.3f}, model choice loss {msum / msum_ref - 1.0:.3f}")
+    for p in iso_parts:
+        p.close()
+    return res

@@ -76,6 +76,7 @@ _lib.tp_last_error.restype = ctypes.c_char_p
 _lib.tp_launch_count.restype = ctypes.c_int64
 _sig("tp_partition_get", _i32, _dbl, _i32, _P(_vp), _P(_i32), _P(_i32))
 _sig("tp_partition_split", _i32, _i32, _i32, _i32, _P(_vp), _P(_i32))
+_sig("tp_partition_shared", _i32, _i32, _P(_vp))
 _sig("tp_partition_info", _vp, _P(_i32), _P(_i32), _P(_i32), _P(_vp))
 _sig("tp_partition_sync", _vp)
 _sig("tp_partition_close", _vp)
@@ -263,6 +264,13 @@ class Partition:
         hs, gr = (_vp * k)(), (_i32 * k)()
         _ck(_lib.tp_partition_split(device, k, sms_each, flags, hs, gr), "tp_partition_split")
         return [cls(hs[i], device, sms_each, gr[i], sms_each / 148.0, owned=True) for i in range(k)]
+
+    @classmethod
+    def shared(cls, k: int, device: int = 0) -> list["Partition"]:
+        """k unpartitioned whole-device handles, one stream each (f3: no SM isolation)."""
+        hs = (_vp * k)()
+        _ck(_lib.tp_partition_shared(device, k, hs), "tp_partition_shared")
+        return [cls(hs[i], device, 148, 148, 1.0, owned=True) for i in range(k)]
 
     def stream(self) -> int:
         s = _vp()

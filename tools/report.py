@@ -3,6 +3,7 @@
   python tools/report.py crosseval  [--workload resnet50] [--fractions 0.1,0.25,0.5,1.0] out.json
   python tools/report.py concurrent [--workload vgg19_b16] [--k 4] [--sms 37] out.json
   python tools/report.py tune       [--workload mobilenetv2] [--fraction 0.5] out.json
+  python tools/report.py interference [--workload resnet50] [--k 4] [--sms 36] out.json
 """
 import argparse
 import json
@@ -16,7 +17,7 @@ from paper_2008_03602_b200 import experiments as ex, tp, workloads as wl  # noqa
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["crosseval", "concurrent", "tune"])
+    ap.add_argument("mode", choices=["crosseval", "concurrent", "tune", "interference"])
     ap.add_argument("out")
     ap.add_argument("--workload", default=None)
     ap.add_argument("--fractions", default="0.1,0.25,0.5,1.0")
@@ -27,12 +28,19 @@ def main():
     ap.add_argument("--layers", default=None, help="comma-separated subset of layer names")
     a = ap.parse_args()
     tp.init(0)
-    wlname = a.workload or {"crosseval": "resnet50", "concurrent": "vgg19_b16", "tune": "mobilenetv2"}[a.mode]
+    wlname = a.workload or {"crosseval": "resnet50", "concurrent": "vgg19_b16", "tune": "mobilenetv2",
+                            "interference": "resnet50"}[a.mode]
     layers = wl.catalog(wlname)
     if a.layers:
         keep = set(a.layers.split(","))
         layers = [d for d in layers if d["name"] in keep]
     t0 = time.time()
+    if a.mode == "interference":
+        res = ex.interference(a.workload or "resnet50", a.k, a.sms if a.sms != 37 else 36, a.trials)
+        res["workload"] = a.workload or "resnet50"
+        res["elapsed_s"] = time.time() - t0
+        json.dump(res, open(a.out, "w"), indent=1)
+        return
     if a.mode == "crosseval":
         res = ex.cross_eval(layers, tuple(float(f) for f in a.fractions.split(",")), a.trials)
     elif a.mode == "concurrent":
