@@ -79,6 +79,8 @@ class ClockSampler:
         self.lines: list[str] = []
 
     def start(self):
+        if os.environ.get("TP_BENCH_NO_CLOCKS"):   # experiments only: no sampler (never for a reported line)
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],

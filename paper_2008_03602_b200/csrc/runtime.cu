@@ -40,6 +40,7 @@ struct tp_partition {
   cudaStream_t stream = nullptr;
   void* flush_buf = nullptr;   // device-owned L2 flush buffer (cold-L2 timing)
   size_t flush_bytes = 0;
+  void* scratch = nullptr;     // tp::TunerScratch, reused across tuning calls (guarded by mu)
   std::mutex mu;
 };
 
@@ -281,9 +282,15 @@ static tp_status create_green(int device, int requested, int flags, tp_partition
   return TP_OK;
 }
 
+static void delete_scratch(void* s);   // defined with TunerScratch
 static void destroy_partition(tp_partition* p) {
   if (!p) return;
   const DriverApi& drv = driver();
+  if (p->scratch) {
+    CtxGuard g(p);
+    delete_scratch(p->scratch);
+    p->scratch = nullptr;
+  }
   if (p->green) {
     if (p->stream) drv.streamDestroy(reinterpret_cast<CUstream>(p->stream));
     if (p->gctx) drv.greenCtxDestroy(p->gctx);
@@ -451,6 +458,25 @@ struct EventPool {
     return cudaSuccess;
   }
 };
+
+// Per-partition tuner scratch (guarded by the partition lock; created in and
+// destroyed under the partition's context): gate values on the device and
+// their pinned host copies (two chunks), gate and timing event pools.
+struct TunerScratch {
+  double* d = nullptr;
+  double* h = nullptr;
+  size_t cap = 0;
+  EventPool pa, pb;
+  ~TunerScratch() {
+    if (d) cudaFree(d);
+    if (h) cudaFreeHost(h);
+  }
+};
+static void delete_scratch(void* s) { delete static_cast<TunerScratch*>(s); }
+static TunerScratch& scratch_of(tp_partition* p) {
+  if (!p->scratch) p->scratch = new TunerScratch();
+  return *static_cast<TunerScratch*>(p->scratch);
+}
 
 // Caller holds the partition lock and has its context current.
 // `launch(st)` enqueues one call (kpc kernels) on st.
@@ -695,16 +721,37 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     // Host-side phase timing (TP_PROFILE=1 prints one line per call to stderr).
     static const bool prof = getenv("TP_PROFILE") && atoi(getenv("TP_PROFILE")) != 0;
     const auto tA = std::chrono::steady_clock::now();
-    double host_a_plan_us = 0, host_a_sync_us = 0;
-    // ---------------- phase A: gate runs, chunked ----------------
-    double* d_vals = nullptr;
-    TP_CK(cudaMalloc(&d_vals, sizeof(double) * (size_t)std::max(1, ncheck) * kChunk));
-    std::vector<double> h_vals((size_t)std::max(1, ncheck) * kChunk);
-    EventPool pa;
-    TP_CK(pa.ensure(2 * kChunk));
-    tp_status err = TP_OK;
-    for (int32_t c0 = 0; c0 < n_cand && err == TP_OK; c0 += kChunk) {
-      const int32_t c1 = std::min(n_cand, c0 + kChunk);
+    double host_a_plan_us = 0, host_a_sync_us = 0, host_a_us = 0;
+    double host_b_us = 0;   // time spent in make/capture/instantiate/enqueue (excl. harvest waits)
+    double host_warm_us = 0, host_cap_us = 0, host_inst_us = 0;
+    // Gate chunks (phase A) and timing (phase B) are interleaved on the one
+    // stream: gate chunk c+1 is enqueued before the timing work of chunk c, so
+    // the host evaluates a chunk's gate values and enqueues the next chunk's
+    // gate runs while the GPU is still timing the previous chunk.  Two chunks'
+    // gate values are in flight (double-buffered device / pinned host arrays).
+    const size_t vpc = (size_t)std::max(1, ncheck) * kChunk;
+    // Scratch lives in the partition (the caller holds its lock) and is reused
+    // across calls: no allocation, page-locking or event creation per call.
+    TunerScratch& vb = scratch_of(part);
+    if (vb.cap < vpc * 2) {
+      if (vb.d) cudaFree(vb.d);
+      if (vb.h) cudaFreeHost(vb.h);
+      vb.d = nullptr; vb.h = nullptr; vb.cap = 0;
+      TP_CK(cudaMalloc(&vb.d, sizeof(double) * vpc * 2));
+      TP_CK(cudaMallocHost(&vb.h, sizeof(double) * vpc * 2));
+      vb.cap = vpc * 2;
+    }
+    EventPool& pa = vb.pa;   // per buffer: 2 * kChunk gate events + 1 "values copied" event
+    TP_CK(pa.ensure(2 * (2 * kChunk + 1)));
+    const int nchunks = (n_cand + kChunk - 1) / kChunk;
+    double t_best_est = 1e30;   // C12b reference: fastest gate run evaluated so far
+
+    auto enqueue_gate = [&](int chunk) -> tp_status {
+      const auto t0 = std::chrono::steady_clock::now();
+      const int buf = chunk & 1;
+      const int32_t c0 = chunk * kChunk, c1 = std::min(n_cand, c0 + kChunk);
+      cudaEvent_t* ev = pa.ev.data() + (size_t)buf * (2 * kChunk + 1);
+      double* dv = vb.d + (size_t)buf * vpc;
       for (int32_t i = c0; i < c1; ++i) {
         Cand& c = cs[i];
         if (cand[i] < 0 || cand[i] >= (int64_t)table.size()) { c.m.status = TP_EINVALID_CONFIG; continue; }
@@ -715,13 +762,13 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         plan_geometry(c.plan, part->sm_granted, &c.m);
         const char* step = "poison";
         cudaError_t e = cudaMemsetAsync(y, 0xFF, ybytes, st);   // NaN in bf16 and fp32
-        if (e == cudaSuccess) { step = "event"; e = cudaEventRecord(pa.ev[2 * (i - c0)], st); }
+        if (e == cudaSuccess) { step = "event"; e = cudaEventRecord(ev[2 * (i - c0)], st); }
         if (e == cudaSuccess) { step = "conv"; e = launch_plan(c.plan, st); }
-        if (e == cudaSuccess) { step = "event"; e = cudaEventRecord(pa.ev[2 * (i - c0) + 1], st); }
+        if (e == cudaSuccess) { step = "event"; e = cudaEventRecord(ev[2 * (i - c0) + 1], st); }
         if (e == cudaSuccess) {
           step = "gather";
           e = launch_gather(y, L.d.in_layout == TP_LAYOUT_NHWC, L.d.out_dtype == TP_DTYPE_FP32, L.d.n, L.d.k, L.P,
-                            L.Q, gate->d_idx, ncheck, d_vals + (size_t)(i - c0) * ncheck, st);
+                            L.Q, gate->d_idx, ncheck, dv + (size_t)(i - c0) * ncheck, st);
         }
         if (e != cudaSuccess) {
           cudaGetLastError();   // a failed launch must not poison the next candidate's error check
@@ -735,23 +782,35 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         g_launches += 1;
         c.live = true;
       }
-      const auto ts0 = std::chrono::steady_clock::now();
-      cudaError_t e = cudaMemcpyAsync(h_vals.data(), d_vals, sizeof(double) * (size_t)ncheck * (c1 - c0),
+      cudaError_t e = cudaMemcpyAsync(vb.h + (size_t)buf * vpc, dv, sizeof(double) * (size_t)ncheck * (c1 - c0),
                                       cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = cudaEventRecord(ev[2 * kChunk], st);
+      if (prof) host_a_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+      if (e != cudaSuccess) {
+        set_error(std::string("gate copy: ") + cudaGetErrorString(e));
+        return TP_ECUDA;
+      }
+      return TP_OK;
+    };
+    auto eval_gate = [&](int chunk) -> tp_status {
+      const int buf = chunk & 1;
+      const int32_t c0 = chunk * kChunk, c1 = std::min(n_cand, c0 + kChunk);
+      cudaEvent_t* ev = pa.ev.data() + (size_t)buf * (2 * kChunk + 1);
+      const auto ts0 = std::chrono::steady_clock::now();
+      cudaError_t e = cudaEventSynchronize(ev[2 * kChunk]);
       if (prof) host_a_sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts0).count();
       if (e != cudaSuccess) {
         set_error(std::string("gate sync: ") + cudaGetErrorString(e));
-        err = TP_ECUDA;
-        break;
+        return TP_ECUDA;
       }
+      const double* hv = vb.h + (size_t)buf * vpc;
       for (int32_t i = c0; i < c1; ++i) {
         Cand& c = cs[i];
         if (!c.live) continue;
         float ms = 0;
-        cudaEventElapsedTime(&ms, pa.ev[2 * (i - c0)], pa.ev[2 * (i - c0) + 1]);
+        cudaEventElapsedTime(&ms, ev[2 * (i - c0)], ev[2 * (i - c0) + 1]);
         c.t_est = std::max(1e-3, ms * 1000.0);
-        const double* v = h_vals.data() + (size_t)(i - c0) * ncheck;
+        const double* v = hv + (size_t)(i - c0) * ncheck;
         bool finite = true;
         for (int j = 0; j < ncheck; ++j) finite = finite && std::isfinite(v[j]);
         if (!gate->have_ref && finite) {
@@ -769,27 +828,17 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         if (!finite || !(e2 <= gate->tol * std::max(mref, 1e-30))) {
           c.m.status = TP_EMISMATCH;
           c.live = false;
+        } else {
+          t_best_est = std::min(t_best_est, c.t_est);
         }
       }
-    }
-    cudaFree(d_vals);
-    if (err != TP_OK) {
-      for (int32_t i = 0; i < n_cand; ++i)
-        if (i < cap) records[i] = cs[i].m;
-      *n_records = std::min(cap, n_cand);
-      return err;
-    }
+      return TP_OK;
+    };
 
-    const auto tB = std::chrono::steady_clock::now();
-    double host_b_us = 0;   // time spent in make/capture/instantiate/enqueue (excl. harvest waits)
-    double host_warm_us = 0, host_cap_us = 0, host_inst_us = 0;
     // ---------------- phase B: timing, windowed pipeline ----------------
-    // Reading C12b: candidates far slower than the fastest gate run of this
-    // call get one timed group (still a warm, graph-timed median of n launches).
-    double t_best_est = 1e30;
-    for (int32_t i = 0; i < n_cand; ++i)
-      if (cs[i].live) t_best_est = std::min(t_best_est, cs[i].t_est);
-    EventPool pb;
+    // Reading C12b: candidates far slower than the fastest gate run evaluated
+    // so far get one timed group (still a warm, graph-timed median of n launches).
+    EventPool& pb = vb.pb;
     TP_CK(pb.ensure((size_t)kWindow * 2 * groups));
     std::vector<int> free_slots;
     for (int i = kWindow - 1; i >= 0; --i) free_slots.push_back(i);
@@ -828,13 +877,12 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       c.m.status = TP_OK;
       return TP_OK;
     };
-    for (int32_t i = 0; i < n_cand && err == TP_OK; ++i) {
+    auto enqueue_timing = [&](int32_t i) -> tp_status {
       Cand& c = cs[i];
-      if (!c.live) continue;
       if (free_slots.empty()) {
-        err = harvest(inflight.front());
+        tp_status h = harvest(inflight.front());
         inflight.erase(inflight.begin());
-        if (err != TP_OK) break;
+        if (h != TP_OK) return h;
       }
       c.slot = free_slots.back();
       free_slots.pop_back();
@@ -846,8 +894,9 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       c.n = std::min(4096, std::max(n_floor, (int)std::ceil(tm.target_group_us / c.t_est)));
       c.groups = raced ? 1 : groups;
       const int warm = raced ? std::min(1, std::max(0, tm.warmup)) : std::max(0, tm.warmup);
-      // Phase A synchronised after every operand write, so each launch here
-      // follows a kernel that never writes the weights (TcArgs::w_early).
+      // The gate run of this candidate synchronised after every operand write
+      // (the weights are written before the call), so each launch here follows
+      // a kernel that never writes the weights (TcArgs::w_early).
       c.plan.tc.args.w_early = w_early_enabled() ? 1 : 0;
       cudaError_t e = cudaSuccess;
       for (int k = 0; k < warm && e == cudaSuccess; ++k) e = launch_plan(c.plan, st);
@@ -891,12 +940,23 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         c.exec = nullptr;
         free_slots.push_back(c.slot);
         cudaGetLastError();
-        if (cudaStreamSynchronize(st) != cudaSuccess) err = TP_ECUDA;
-        continue;
+        if (cudaStreamSynchronize(st) != cudaSuccess) return TP_ECUDA;
+        return TP_OK;
       }
       inflight.push_back(i);
       host_b_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - te0).count();
+      return TP_OK;
+    };
+
+    tp_status err = nchunks > 0 ? enqueue_gate(0) : TP_OK;
+    for (int ch = 0; ch < nchunks && err == TP_OK; ++ch) {
+      err = eval_gate(ch);
+      if (err == TP_OK && ch + 1 < nchunks) err = enqueue_gate(ch + 1);
+      const int32_t c0 = ch * kChunk, c1 = std::min(n_cand, c0 + kChunk);
+      for (int32_t i = c0; i < c1 && err == TP_OK; ++i)
+        if (cs[i].live) err = enqueue_timing(i);
     }
+    const auto tB = tA;   // phases are interleaved; see the host_* counters
     for (int32_t i : inflight) {
       tp_status h = harvest(i);
       if (err == TP_OK) err = h;
@@ -909,7 +969,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       fprintf(stderr,
               "[tp] candidates %d: phase A %.0f us, phase B %.0f us (host enqueue %.0f us: warm-up %.0f, capture %.0f, "
               "instantiate %.0f); phase A make_plan %.0f us, chunk sync+D2H %.0f us\n",
-              n_cand, us(tA, tB), us(tB, tC), host_b_us, host_warm_us, host_cap_us, host_inst_us, host_a_plan_us,
+              n_cand, host_a_us, us(tB, tC), host_b_us, host_warm_us, host_cap_us, host_inst_us, host_a_plan_us,
               host_a_sync_us);
     }
     // C12b: a raced candidate that beat every fully-timed one is re-timed with
