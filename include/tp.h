@@ -64,7 +64,7 @@ enum { TP_EPI_BIAS = 1, TP_EPI_RELU = 2 };
  * are gathered into shared memory by CUDA-core warps over the flattened
  * (r, s, c) axis (bf16, g = 1, C % 8 != 0: the C = 3 stems). */
 enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2, TP_KIND_IGEMM_TC_ROW = 3,
-       TP_KIND_IGEMM_TC_MT = 4, TP_KIND_IGEMM_TF32X3 = 5 };
+       TP_KIND_IGEMM_TC_MT = 4, TP_KIND_IGEMM_TF32X3 = 5, TP_KIND_IGEMM_TC_STEM = 6 };
 /* IGEMM_TC_MT ("multi-tile im2col"): appended last to the space of IGEMM_TC
  * layers with ceil(M/64)*ceil(K/32) >= 1024.  The IGEMM_TC k-blocks (one TMA
  * im2col box + one weight box per (channel block, tap), BK = 64) run in the

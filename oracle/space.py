@@ -25,6 +25,7 @@ KIND_IGEMM_TC_GATHER = 2
 KIND_IGEMM_TC_ROW = 3
 KIND_IGEMM_TC_MT = 4
 KIND_IGEMM_TF32X3 = 5
+KIND_IGEMM_TC_STEM = 6
 DTYPE_BF16 = 0
 DTYPE_FP32 = 1
 SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
@@ -34,6 +35,7 @@ TC_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("bk", (16, 32, 64, 1
 ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)), ("threads", (128, 256)),
              ("tiles_per_cta", (1, 2, 4, 8, 16)))
 MT_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("tiles_per_cta", (2, 4, 8)))
+STEM_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128)), ("tiles_per_cta", (2, 4, 8, 16)))
 TF32_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("split_k", (1, 2, 4, 8)))
 DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
                 ("tile_p", (1, 2, 4, 8)), ("smem_stage", (0, 1)))
@@ -158,6 +160,30 @@ def _valid_direct(d: dict, threads, tile_q, vec_k, tile_p, smem_stage) -> bool:
     return True
 
 
+def stem_eligible(d: dict) -> bool:
+    """Stem kind: gathered (C % 8 != 0) tensor-core layers with C <= 8, R S C <= 256
+    and output rows at least 64 wide."""
+    P, Q = out_pq(d)
+    return (layer_kind(d) == KIND_IGEMM_TC_GATHER and d["c"] <= 8 and d["r"] * d["s"] * d["c"] <= 256
+            and Q >= 64)
+
+
+def stem_kp(d: dict) -> int:
+    return _cdiv(d["r"] * d["s"] * d["c"], 64) * 64
+
+
+def _valid_stem(d: dict, bm: int, bn: int, tiles_per_cta: int) -> bool:
+    # resident weights bn x KP, two im2col tiles bm x KP (bf16), the input patch
+    # R x ((bm-1) s_w + S) x C bf16 rounded up to 1 KiB, the KP-entry k table, barriers
+    P, Q = out_pq(d)
+    kp = stem_kp(d)
+    cols = (bm - 1) * d["stride_w"] + d["s"]
+    patch = _cdiv(d["r"] * cols * d["c"] * 2, 1024) * 1024
+    if bn * kp * 2 + 2 * bm * kp * 2 + patch + kp * 4 + 1024 > SMEM_LIMIT:
+        return False
+    return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))
+
+
 def tf32_eligible(d: dict) -> bool:
     """3xTF32 tensor-core kind: fp32 dense layers whose NHWC
     pixel rows are 16-byte multiples (C % 4 == 0) and K % 8 == 0."""
@@ -208,6 +234,13 @@ def enumerate_space(d: dict) -> list[dict]:
                          kind=KIND_IGEMM_TF32X3, space_index=len(out))
                 s.update(geometry(d, s))
                 out.append(s)
+    if stem_eligible(d):         # after the gathered tuples; bk = KP, stages = 2, threads = 256, split_k = 1
+        for combo in itertools.product(*[v for _, v in STEM_KNOBS]):
+            if _valid_stem(d, *combo):
+                s = dict(zip([k for k, _ in STEM_KNOBS], combo), bk=stem_kp(d), stages=2, threads=256, split_k=1,
+                         kind=KIND_IGEMM_TC_STEM, space_index=len(out))
+                s.update(geometry(d, s))
+                out.append(s)
     if mt_eligible(d):           # appended last; threads = 256, bk = 64, split_k = 1
         for combo in itertools.product(*[v for _, v in MT_KNOBS]):
             if _valid_mt(d, *combo):
@@ -223,6 +256,8 @@ def geometry(d: dict, s: dict) -> dict:
     P, Q = out_pq(d)
     if s.get("kind") == KIND_IGEMM_TC_MT:
         g = (_cdiv(_cdiv(d["n"] * P * Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
+    elif s.get("kind") == KIND_IGEMM_TC_STEM:
+        g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
     elif s.get("kind") == KIND_IGEMM_TC_ROW:
         g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
     elif s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER, KIND_IGEMM_TF32X3):

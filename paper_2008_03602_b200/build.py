@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "-I", os.path.join(ROOT, "include"),
           "--expt-relaxed-constexpr"]
-SOURCES = ["space.cpp", "search.cpp", "runtime.cu", "igemm_tc.cu", "igemm_tf32.cu", "direct_conv.cu", "aux_kernels.cu"]
+SOURCES = ["space.cpp", "search.cpp", "runtime.cu", "igemm_tc.cu", "igemm_tf32.cu", "igemm_stem.cu", "direct_conv.cu", "aux_kernels.cu"]
 
 
 def _compile(src: str, verbose: bool) -> str:

@@ -1,0 +1,235 @@
+// igemm_stem.cu -- tensor-core conv2d for the small-channel stems (C < 8:
+// ResNet-50 conv1, VGG-19 conv1_1, MobileNetV2 conv0), kind TP_KIND_IGEMM_TC_STEM.
+//
+// What it computes: the same operator as igemm_tc.cu (bias +
+// ReLU of P:388), D[M x K] = A_im2col[M x K_g] W[K x K_g]^T with the reduction
+// axis k = (r, s, c) flattened (c fastest, KRSC weights), K_g = R S C <= 256
+// padded with zeros to KP = 64 ceil(K_g / 64).
+//
+// Why a separate kind: a C = 3 pixel row is 6 bytes, so neither TMA mode can
+// feed it, and gathering the im2col tile element by element from global memory
+// (the gathered kind) is bound by the L1 wavefront rate of scattered 2-byte
+// loads (~2 elements / cycle / SM measured, ~4000 cycles per 128-pixel VGG
+// tile).  Here a tile is BM output pixels of ONE output row, whose input patch
+// (R rows x ((BM-1) s_w + S) pixels x C channels) is a set of R contiguous
+// global segments: three producer warps copy it into shared memory with
+// coalesced loads, then expand it into the 128-B-swizzled K-major im2col tile
+// with shared-memory reads (a k table maps k -> patch offset).  The BN x KP
+// weight tile is staged once per CTA and stays resident for tiles_per_cta
+// tiles; two TMEM accumulators let the epilogue of tile i overlap the MMAs of
+// tile i+1.
+//
+// Warp roles (256 threads): warps 0-2 producers (patch + im2col tile, named
+// barrier 1), warp 3 MMA issuer (one elected lane), warps 4-7 epilogue (TMEM
+// lane quadrant = warp % 4), warp 2 also allocates TMEM.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "tp_kernels.h"
+#include "tc_ptx.cuh"
+
+namespace tp {
+
+template <int BM, int BN>
+__global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                                                         TcArgs a) {   // (no tensor maps: same launch signature as igemm_tc)
+  constexpr uint32_t A_SUB = BM * 128, B_SUB = BN * 128;   // one 64-element (128-B) k column block
+  constexpr uint32_t kTmemCols = 2 * BN;                   // two accumulators
+  constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(BM >> 4) << 24);   // bf16 x bf16 -> f32, K-major A and B
+  constexpr int kProd = 96;                                 // producer threads (warps 0-2)
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KP = a.bk, NSUB = KP >> 6, CH = KP >> 3;        // 16-byte chunks per row
+  uint8_t* b_s = smem_raw;
+  uint8_t* a_s = smem_raw + (size_t)NSUB * B_SUB;
+  uint16_t* patch = reinterpret_cast<uint16_t*>(smem_raw + a.patch_off);
+  int* ktab = reinterpret_cast<int*>(smem_raw + a.tab_off);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + a.bar_off);
+  uint64_t* b_full = bars;        // weights staged (3 producer warps)
+  uint64_t* a_full = bars + 1;    // [2] im2col tile ready (3 producer warps)
+  uint64_t* a_empty = bars + 3;   // [2] MMAs of the tile done (commit)
+  uint64_t* t_full = bars + 5;    // [2] accumulator ready (commit)
+  uint64_t* t_empty = bars + 7;   // [2] accumulator drained (4 epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int tile0 = blockIdx.x * a.tpc;
+  const int ntl = a.ntiles - tile0 < a.tpc ? a.ntiles - tile0 : a.tpc;
+  const int nbase = blockIdx.y * BN;
+  const int C = a.C, cols = a.pcols, rowlen = cols * C;     // patch row: cols pixels x C channels
+
+  if (warp == 0 && lane == 0) {
+    if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
+    mbar_init(b_full, 3);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(a_full + i, 3);
+      mbar_init(a_empty + i, 1);
+      mbar_init(t_full + i, 1);
+      mbar_init(t_empty + i, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // k table: k = (r, s, c) -> offset of x[r][s + m s_w][c] in the patch for pixel m = 0; -1 = padding.
+  for (int k = threadIdx.x; k < KP; k += blockDim.x) {
+    int v = -1;
+    if (k < a.Kg) {
+      const int c = k % C, rs = k / C, s = rs % a.S, r = rs / a.S;
+      v = r * rowlen + s * C + c;
+    }
+    ktab[k] = v;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp < 3) {
+    // ---------------- producers ----------------
+    const int pt = threadIdx.x;
+    if (warp == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint16_t* xg = reinterpret_cast<const uint16_t*>(a.xg);
+    const uint16_t* wg = reinterpret_cast<const uint16_t*>(a.wg);
+    // Weights once per CTA: row n of B = W[nbase + n][0..KP) (zero past K_g / K).
+    for (int idx = pt; idx < BN * CH; idx += kProd) {
+      const int n = idx % BN, ch = idx / BN, k0 = ch * 8, kn = nbase + n;
+      uint32_t v[4];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        uint32_t lo = 0, hi = 0;
+        if (kn < a.K && k0 + j < a.Kg) lo = __ldg(wg + (int64_t)kn * a.Kg + k0 + j);
+        if (kn < a.K && k0 + j + 1 < a.Kg) hi = __ldg(wg + (int64_t)kn * a.Kg + k0 + j + 1);
+        v[j / 2] = lo | (hi << 16);
+      }
+      const uint32_t off = (uint32_t)n * 128 + ((uint32_t)(((k0 & 63) >> 3) ^ (n & 7)) << 4);
+      *reinterpret_cast<uint4*>(b_s + (size_t)(k0 >> 6) * B_SUB + off) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(b_full);
+
+    const int WC = a.W * C;
+    for (int i = 0; i < ntl; ++i) {
+      const int t = tile0 + i, b = i & 1;
+      const int qb = t % a.nqb, prow = t / a.nqb, p = prow % a.P, n = prow / a.P;
+      const int q0 = qb * BM;
+      // Input patch: R contiguous segments of the NHWC input (zero outside the image).
+      const int e0 = (q0 * a.sw - a.pw) * C;   // element offset of the patch start in an input row
+      for (int r = 0; r < a.R; ++r) {
+        const int h = p * a.sh - a.ph + r;
+        const bool hv = (unsigned)h < (unsigned)a.H;
+        const uint16_t* xr = xg + ((int64_t)n * a.H + (hv ? h : 0)) * WC;
+        uint16_t* pr = patch + r * rowlen;
+        for (int e = pt; e < rowlen; e += kProd) {
+          const int gi = e0 + e;
+          pr[e] = (hv && (unsigned)gi < (unsigned)WC) ? __ldg(xr + gi) : (uint16_t)0;
+        }
+      }
+      asm volatile("bar.sync 1, 96;" ::: "memory");
+      // Expand into the swizzled im2col tile b (after the MMAs of tile i-2 released it).
+      mbar_wait(a_empty + b, ((uint32_t)(i >> 1) & 1u) ^ 1u);
+      uint8_t* at = a_s + (size_t)b * NSUB * A_SUB;
+      const int mstep = a.sw * C;
+      for (int idx = pt; idx < BM * CH; idx += kProd) {
+        const int m = idx % BM, ch = idx / BM, k0 = ch * 8;
+        const int mo = m * mstep;
+        uint32_t v[4];
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const int o0 = ktab[k0 + j], o1 = ktab[k0 + j + 1];
+          const uint32_t lo = o0 >= 0 ? patch[o0 + mo] : 0u, hi = o1 >= 0 ? patch[o1 + mo] : 0u;
+          v[j / 2] = lo | (hi << 16);
+        }
+        const uint32_t off = (uint32_t)m * 128 + ((uint32_t)(((k0 & 63) >> 3) ^ (m & 7)) << 4);
+        *reinterpret_cast<uint4*>(at + (size_t)(k0 >> 6) * A_SUB + off) = make_uint4(v[0], v[1], v[2], v[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + b);
+      asm volatile("bar.sync 1, 96;" ::: "memory");   // the patch is reused for the next tile
+    }
+  } else if (warp == 3) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t lead = elect_one();
+    mbar_wait(b_full, 0);
+    const uint64_t bdesc0 = make_sdesc(smem_u32(b_s), 128);
+    for (int i = 0; i < ntl; ++i) {
+      const int b = i & 1;
+      mbar_wait(a_full + b, (uint32_t)(i >> 1) & 1u);
+      if (i >= 2) mbar_wait(t_empty + b, (uint32_t)((i - 2) >> 1) & 1u);
+      tc_fence_after();
+      const uint64_t adesc0 = make_sdesc(smem_u32(a_s + (size_t)b * NSUB * A_SUB), 128);
+      const uint32_t d = tmem_base + (uint32_t)(b * BN);
+      for (int kk = 0; kk < KP / 16; ++kk) {
+        const uint32_t sb = (uint32_t)(kk >> 2), ko = (uint32_t)((kk & 3) * 32);
+        tc_mma_p(d, adesc0 + ((sb * A_SUB + ko) >> 4), bdesc0 + ((sb * B_SUB + ko) >> 4), IDESC, kk > 0 ? 1u : 0u,
+                 lead);
+      }
+      tc_commit_p(a_empty + b, lead);
+      tc_commit_p(t_full + b, lead);
+    }
+  } else {
+    // ---------------- epilogue (warps 4-7) ----------------
+    const int quad = warp & 3;
+    const int row = (BM == 128) ? quad * 32 + lane : quad * 16 + lane;
+    const bool row_ok = (BM == 128 || lane < 16);
+    for (int i = 0; i < ntl; ++i) {
+      const int t = tile0 + i, b = i & 1;
+      const int qb = t % a.nqb, prow = t / a.nqb;
+      const int q = qb * BM + row;
+      __syncwarp();
+      mbar_wait(t_full + b, (uint32_t)(i >> 1) & 1u);
+      tc_fence_after();
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t raw[16];
+        tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * BN + c), raw);
+        const int nb = nbase + c;
+        if (row_ok && q < a.Q && nb < a.K) {
+          float v[16];
+#pragma unroll
+          for (int g = 0; g < 16; g += 4) {
+            float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (a.has_bias && nb + g + 4 <= a.K) bv = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
+            const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float s = __uint_as_float(raw[g + j]) + b4[j];
+              v[g + j] = a.relu ? fmaxf(s, 0.0f) : s;
+            }
+          }
+          store16(a.y, (int64_t)prow * a.Q + q, a.K, nb, v, a.out_f32);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t_empty + b);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+const void* pick_stem(int bm, int bn) {
+#define TP_STEM_CASE(M_, N_) \
+  if (bm == M_ && bn == N_) return reinterpret_cast<const void*>(igemm_stem_kernel<M_, N_>);
+  TP_STEM_CASE(64, 32) TP_STEM_CASE(64, 64) TP_STEM_CASE(64, 128)
+  TP_STEM_CASE(128, 32) TP_STEM_CASE(128, 64) TP_STEM_CASE(128, 128)
+#undef TP_STEM_CASE
+  return nullptr;
+}
+
+}  // namespace tp

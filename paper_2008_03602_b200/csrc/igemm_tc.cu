@@ -945,8 +945,46 @@ static tp_status tf32_prepare(const TcProblem& pb, bool a_tiled, TcPlan* plan) {
   return TP_OK;
 }
 
+// Stem kind: no tensor maps; smem = [weights NSUB x BN x 128 B][2 im2col tiles NSUB x BM x 128 B]
+// [input patch, 1 KiB multiple][k table KP x 4 B][barriers] (matches space.cpp stem_smem_bytes).
+static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
+  std::memset(&plan->tmA, 0, sizeof(plan->tmA));
+  std::memset(&plan->tmB, 0, sizeof(plan->tmB));
+  TcArgs& a = plan->args;
+  std::memset(&a, 0, sizeof(a));
+  const int kg = pb.R * pb.S * pb.C;
+  const int kp = (kg + 63) / 64 * 64;
+  a.M = pb.M; a.K = pb.K; a.P = pb.P; a.Q = pb.Q; a.S = pb.S; a.R = pb.R;
+  a.sh = pb.sh; a.sw = pb.sw; a.ph = pb.ph; a.pw = pb.pw;
+  a.H = pb.H; a.W = pb.W; a.C = pb.C; a.Kg = kg; a.bk = kp; a.stages = 2; a.split_k = 1;
+  a.xg = pb.x; a.wg = pb.w;
+  a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
+  a.pcols = (pb.bm - 1) * pb.sw + pb.S;
+  a.nqb = (pb.Q + pb.bm - 1) / pb.bm;
+  a.ntiles = pb.N * pb.P * a.nqb;
+  a.tpc = pb.tpc > 1 ? pb.tpc : 1;
+  const size_t patch = ((size_t)pb.R * a.pcols * pb.C * 2 + 1023) / 1024 * 1024;
+  a.patch_off = (int)((size_t)pb.bn * kp * 2 + 2 * (size_t)pb.bm * kp * 2);
+  a.tab_off = a.patch_off + (int)patch;
+  a.bar_off = a.tab_off + kp * 4;
+  plan->fn = pick_stem(pb.bm, pb.bn);
+  if (!plan->fn) { set_error("no igemm_stem instantiation for this BM x BN"); return TP_EINVALID_CONFIG; }
+  plan->grid = dim3((unsigned)((a.ntiles + a.tpc - 1) / a.tpc), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u);
+  if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
+  plan->block = dim3(256);
+  plan->cluster_z = 1;
+  plan->smem = (size_t)a.bar_off + 128;
+  cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    return TP_ECUDA;
+  }
+  return TP_OK;
+}
+
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   const DriverApi& drv = driver();
+  if (pb.stem) return stem_prepare(pb, plan);
   const int sub_k = pb.bk < 64 ? pb.bk : 64;
   static const bool no_atile = getenv("TP_NO_ATILE") && atoi(getenv("TP_NO_ATILE")) != 0;
   const bool a_tiled = !pb.gather && !pb.row && !no_atile && pb.R == 1 && pb.S == 1 && pb.sh == 1 && pb.sw == 1 &&

@@ -400,6 +400,7 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     pb.tpc = s.tiles_per_cta;
     pb.mt = s.kind == TP_KIND_IGEMM_TC_MT ? 1 : 0;
     pb.tf32 = s.kind == TP_KIND_IGEMM_TF32X3 ? 1 : 0;
+    pb.stem = s.kind == TP_KIND_IGEMM_TC_STEM ? 1 : 0;
     tp_status st = tc_prepare(pb, &plan->tc);
     if (st != TP_OK) return st;
     plan->ctas_per_sm = tc_occupancy(plan->tc);

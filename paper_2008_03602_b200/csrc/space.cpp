@@ -195,7 +195,42 @@ static bool valid_tf32(const Layer& L, int bm, int bn, int stages, int split) {
   return split <= (int64_t)L.d.r * L.d.s * cdiv(L.d.c, 32);
 }
 
+// Stem kind for the C < 8 gathered layers (ResNet-50 conv1, VGG-19 conv1_1,
+// MobileNetV2 conv0): a tile is BM output pixels of one output row; three
+// producer warps stage the tile's input patch (R rows x ((BM-1) s_w + S) pixels
+// x C channels, coalesced) in shared memory and expand it into the swizzled
+// im2col tile (k = (r, s, c) flattened, padded to KP = 64 ceil(R S C / 64));
+// the BN x KP weight tile stays resident for tiles_per_cta tiles; two TMEM
+// accumulators overlap the epilogue of one tile with the next tile's MMAs.
+bool stem_kind_eligible(const Layer& L) {
+  const tp_conv_desc& d = L.d;
+  return L.kind == TP_KIND_IGEMM_TC_GATHER && d.c <= 8 && (int64_t)d.r * d.s * d.c <= 256 && L.Q >= 64;
+}
+static const int kStemBM[] = {64, 128};
+static const int kStemBN[] = {32, 64, 128};
+static const int kStemTpc[] = {2, 4, 8, 16};
+int64_t stem_kp(const Layer& L) { return cdiv((int64_t)L.d.r * L.d.s * L.d.c, 64) * 64; }
+int64_t stem_patch_bytes(const Layer& L, int bm) {
+  const int64_t cols = (int64_t)(bm - 1) * L.d.stride_w + L.d.s;
+  return cdiv((int64_t)L.d.r * cols * L.d.c * 2, 1024) * 1024;
+}
+int64_t stem_smem_bytes(const Layer& L, int bm, int bn) {
+  const int64_t kp = stem_kp(L);
+  return (int64_t)bn * kp * 2 + 2 * (int64_t)bm * kp * 2 + stem_patch_bytes(L, bm) + kp * 4 + 1024;
+}
+static bool valid_stem(const Layer& L, int bm, int bn) {
+  if (stem_smem_bytes(L, bm, bn) > kSmemLimit) return false;
+  if (bm > np2(L.Q)) return false;
+  return bn <= std::max<int64_t>(32, np2(L.d.k));
+}
+
 void fill_geometry(const Layer& L, tp_schedule* s) {
+  if (s->kind == TP_KIND_IGEMM_TC_STEM) {
+    s->grid_x = (int32_t)cdiv((int64_t)L.d.n * L.P * cdiv(L.Q, s->bm), std::max(1, s->tiles_per_cta));
+    s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
+    s->grid_z = 1;
+    return;
+  }
   if (s->kind == TP_KIND_IGEMM_TC_MT) {
     s->grid_x = (int32_t)cdiv(cdiv(L.M, s->bm), std::max(1, s->tiles_per_cta));
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
@@ -241,6 +276,15 @@ static void enumerate(const Layer& L, F visit) {
           s.threads = th; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
           if (!visit(s)) return;
         }
+    // Gathered stems append the stem kind (after every gathered tuple).
+    if (stem_kind_eligible(L))
+      for (int bm : kStemBM) for (int bn : kStemBN) for (int tpc : kStemTpc) {
+        if (!valid_stem(L, bm, bn)) continue;
+        tp_schedule s; std::memset(&s, 0, sizeof(s));
+        s.kind = TP_KIND_IGEMM_TC_STEM; s.bm = bm; s.bn = bn; s.bk = (int32_t)stem_kp(L); s.stages = 2;
+        s.threads = 256; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
+        if (!visit(s)) return;
+      }
     // Layers with many tiles append the multi-tile im2col kind last.
     if (mt_kind_eligible(L))
       for (int bm : kTcBM) for (int bn : kTcBN) for (int st : kMtStages) for (int tpc : kMtTpc) {
@@ -306,6 +350,10 @@ bool schedule_in_space(const Layer& L, const tp_schedule& s) {
     return row_kind_eligible(L) && in_(s.bm, kRowBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 64 &&
            in_(s.stages, kRowStages, 3) && in_(s.threads, kTcThreads, 2) && s.split_k == 1 &&
            in_(s.tiles_per_cta, kRowTpc, 5) && valid_row(L, s.bm, s.bn, s.stages, s.threads, s.tiles_per_cta);
+  if (s.kind == TP_KIND_IGEMM_TC_STEM)
+    return stem_kind_eligible(L) && in_(s.bm, kStemBM, 2) && in_(s.bn, kStemBN, 3) && s.bk == stem_kp(L) &&
+           s.stages == 2 && s.threads == 256 && s.split_k == 1 && in_(s.tiles_per_cta, kStemTpc, 4) &&
+           valid_stem(L, s.bm, s.bn);
   if (s.kind == TP_KIND_IGEMM_TF32X3)
     return tf32_kind_eligible(L) && in_(s.bm, kTcBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 32 &&
            in_(s.stages, kTf32Stages, 3) && s.threads == 256 && in_(s.split_k, kTcSplit, 4) &&

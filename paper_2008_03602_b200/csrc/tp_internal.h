@@ -37,7 +37,10 @@ int64_t tc_smem_bytes(int bm, int bn, int bk, int stages);
 int64_t tcg_table_bytes(const Layer& L, int bm, int bk);   // gather kind: pixel + k tables
 bool row_kind_eligible(const Layer& L);                     // row-halo kind applies
 bool mt_kind_eligible(const Layer& L);                      // multi-tile im2col kind applies
-bool tf32_kind_eligible(const Layer& L);                    // 3xTF32 tensor-core kind applies (fp32 dense)
+bool tf32_kind_eligible(const Layer& L);
+bool stem_kind_eligible(const Layer& L);                    // stem kind applies (C < 8 gathered layers)
+int64_t stem_kp(const Layer& L);                            // stem kind: reduction padded to 64 (R S C)
+int64_t stem_patch_bytes(const Layer& L, int bm);                    // 3xTF32 tensor-core kind applies (fp32 dense)
 int64_t tf32_smem_bytes(int bm, int bn, int stages, int split);
 int64_t row_stage_bytes(int bm, int bn);                    // row-halo kind: one pipeline stage
 bool schedule_in_space(const Layer& L, const tp_schedule& s);

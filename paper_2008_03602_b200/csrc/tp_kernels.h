@@ -74,6 +74,7 @@ struct TcArgs {
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
   int dbg;                     // TP_DEBUG_TC env (experiments only): bit0 skip A TMA, bit1 skip B TMA
   int a_tiled;                 // 1: A is a tiled [M][C] map (1x1 / stride 1 / pad 0 layers), not im2col
+  int R, pcols, patch_off;     // stem kind: filter rows, patch pixels per row, patch offset in smem
   int w_early;                 // 1: weight (B) boxes of the first ring pass are issued before
                                //    griddepcontrol.wait -- only when the preceding kernel in the
                                //    stream is a launch of this plan (weights are layer constants)
@@ -97,6 +98,7 @@ struct TcProblem {
   int tpc;         // row-halo / multi-tile: tiles per CTA
   int mt;          // 1: TP_KIND_IGEMM_TC_MT (im2col multi-tile)
   int tf32;        // 1: TP_KIND_IGEMM_TF32X3 (fp32 NHWC x, KRSC w; 3xTF32 split)
+  int stem;        // 1: TP_KIND_IGEMM_TC_STEM (C < 8 stems: staged input patch, resident weights)
 };
 
 struct TcPlan {
@@ -110,6 +112,7 @@ struct TcPlan {
 
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan);
 const void* pick_tf32(int bm, int bn);   // igemm_tf32.cu
+const void* pick_stem(int bm, int bn);   // igemm_stem.cu
 cudaError_t tc_launch(const TcPlan& plan, cudaStream_t stream);
 int tc_occupancy(const TcPlan& plan);
 size_t tc_dyn_smem(int bm, int bn, int bk, int stages);

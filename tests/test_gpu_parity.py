@@ -295,3 +295,62 @@ def test_tf32x3_random_parity_fp32_bar(d):
         worst = max(worst, err)
         assert err <= 1e-5, (s, err)
     assert worst > 0.0 or d["c"] <= 4   # random data does round somewhere
+
+
+# ------------------------------------------------------------------ stem kind (C < 8: staged patch)
+STEM_TINY = [mk(2, 3, 10, 70, 64, 3, 3, 1, 1, out=tp.FP32, epi=1),     # VGG conv1_1-like, 2 images, Q = 70
+             mk(1, 3, 23, 140, 64, 7, 7, 2, 3, out=tp.FP32, epi=1),    # R50 conv1-like (7x7 s2 p3), Q = 70
+             mk(1, 3, 9, 132, 32, 3, 3, 2, 1, out=tp.FP32, epi=1),     # MobileNetV2 conv0-like (3x3 s2)
+             mk(1, 5, 6, 80, 40, 3, 3, 1, 1, out=tp.FP32, epi=1)]      # C = 5, K = 40 (ragged N tile)
+
+
+def _stem_scheds(d):
+    out = [tp.space_get(d, i) for i in range(tp.space_size(d))]
+    out = [s for s in out if s["kind"] == tp.KIND_IGEMM_TC_STEM]
+    assert out, "layer has no stem schedules"
+    return out
+
+
+@pytest.mark.parametrize("d", STEM_TINY, ids=lambda d: f"stem_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_r{d['r']}s{d['stride_h']}")
+def test_stem_every_schedule_bit_exact_integer(d):
+    """O11 for the stem kind: ragged last tile of every output row, zero-padded
+    patch borders, several images, every tiles_per_cta (partial last CTA)."""
+    x, w, b = datagen.make_inputs(d, 23, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    bad = []
+    for s in _stem_scheds(d):
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        if not np.array_equal(buf.output(), ref):
+            bad.append((s["space_index"], s["bm"], s["bn"], s["tiles_per_cta"]))
+    assert not bad, f"{len(bad)} stem schedules differ, first: {bad[:5]}"
+
+
+STEM_FULL = [wl.catalog("resnet50")[0], wl.catalog("mobilenetv2")[0]]
+
+
+@pytest.mark.parametrize("d", STEM_FULL, ids=lambda d: d["name"])
+def test_stem_full_size_random_parity(d):
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(2, 0))
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    for s in _stem_scheds(d):
+        buf.poison()
+        tp.conv2d_run(buf, s, timing_cfg=tp.timing(warmup=1, groups=1, n_min=2, target_group_us=1.0))
+        torch.cuda.synchronize()
+        assert rel_err(buf.output(), ref) <= 2e-2, s
+
+
+def test_stem_vgg_conv1_1_sampled_points():
+    d = wl.catalog("vgg19_b16")[0]
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(4, 0))
+    buf = tp.LayerBuffers(d, x, w, b)
+    P, Q = tp.output_shape(d)
+    idx = datagen.sample_points(d["n"] * d["k"] * P * Q, 4096, 5)
+    ref = oc.conv2d_points_c(d, bf16_round(x), bf16_round(w), b, True, idx)
+    for s in _stem_scheds(d)[::3]:
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        assert rel_err(buf.gather(idx), ref) <= 2e-2, s

@@ -74,8 +74,29 @@ def test_gather_space_hand_count():
                         continue
                     n += 2 * sum(1 for sk in (1, 2, 4, 8) if sk <= nkb)
     d = wl.catalog("resnet50")[0]
-    assert len(sp.enumerate_space(d)) == n
-    assert all(s["kind"] == sp.KIND_IGEMM_TC_GATHER for s in sp.enumerate_space(d))
+    g = [s for s in sp.enumerate_space(d) if s["kind"] == sp.KIND_IGEMM_TC_GATHER]
+    assert len(g) == n and sp.enumerate_space(d)[:n] == g
+
+
+def test_stem_kind_hand_count():
+    # R50 conv1 (C=3, 7x7 s2 p3, Q=112): KP = 64 ceil(147/64) = 192; BM {64, 128} (<= np2(112));
+    # BN <= max(32, np2(64)) -> {32, 64}; tiles_per_cta {2, 4, 8, 16}; the largest smem
+    # (BM=128, BN=64) = 64*192*2 + 2*128*192*2 + ceil(7*261*3*2/1024) KiB + 192*4 + 1024
+    # = 24576 + 98304 + 11264 + 768 + 1024 = 135936 fits: 2 x 2 x 4 = 16, appended after the gathered tuples.
+    d = wl.catalog("resnet50")[0]
+    sps = sp.enumerate_space(d)
+    st = [s for s in sps if s["kind"] == sp.KIND_IGEMM_TC_STEM]
+    assert len(st) == 16 and sps[-16:] == st and all(s["bk"] == 192 for s in st)
+    x = [s for s in st if s["bm"] == 64 and s["bn"] == 32 and s["tiles_per_cta"] == 8][0]
+    assert (x["grid_x"], x["grid_y"], x["grid_z"]) == (-(-(112 * 2) // 8), 2, 1)
+    # VGG conv1_1 (C=3, 3x3 s1, Q=224, b16): KP = 64; eligible; MobileNetV2 conv0 (3x3 s2, Q=112): eligible
+    v = wl.catalog("vgg19_b16")[0]
+    assert sp.stem_eligible(v) and sp.stem_kp(v) == 64
+    assert sp.stem_eligible(wl.catalog("mobilenetv2")[0])
+    # not eligible: C % 8 == 0 layers, narrow outputs, R S C > 256
+    assert not sp.stem_eligible(wl.catalog("resnet50")[1])
+    assert not sp.stem_eligible(dict(v, h=32, w=32))
+    assert not sp.stem_eligible(dict(v, c=6, r=7, s=7))
 
 
 def test_row_kind_hand_count_and_order():

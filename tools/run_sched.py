@@ -18,6 +18,10 @@ reps = int(sys.argv[9]) if len(sys.argv) > 9 else 3
 part = tp.Partition.get(float(os.environ.get("FRAC", "1.0")))
 x, w, b = datagen.make_inputs(d, datagen.data_seed(2, li))
 buf = tp.LayerBuffers(d, x, w, b, part=part)
+if os.environ.get("KIND"):
+    ov["kind"] = int(os.environ["KIND"])
+if os.environ.get("TPC"):
+    ov["tiles_per_cta"] = int(os.environ["TPC"])
 s = next(tp.space_get(d, i) for i in range(tp.space_size(d)) if all(tp.space_get(d, i)[k] == v for k, v in ov.items()))
 for _ in range(reps):
     tp.conv2d_run(buf, s, part)
