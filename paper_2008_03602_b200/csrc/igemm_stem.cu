@@ -34,7 +34,7 @@ namespace tp {
 
 template <int BM, int BN>
 __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
-                                                         TcArgs a) {   // (no tensor maps: same launch signature as igemm_tc)
+                                                         const __grid_constant__ CUtensorMap, TcArgs a) {   // (no tensor maps: same launch signature as igemm_tc)
   constexpr uint32_t A_SUB = BM * 128, B_SUB = BN * 128;   // one 64-element (128-B) k column block
   constexpr uint32_t kTmemCols = 2 * BN;                   // two accumulators
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |

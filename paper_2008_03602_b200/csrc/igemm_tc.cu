@@ -48,7 +48,8 @@ __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long l
 //   neither TMA mode applies).
 template <int BM, int BN, int BK, int MODE>
 __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                       const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+                                                       const __grid_constant__ CUtensorMap tmB,
+                                                       const __grid_constant__ CUtensorMap tmY, TcArgs a) {
   constexpr bool GATHER = MODE == 1;
   static_assert(MODE == 0 || MODE == 1, "MODE 2 (row-halo) is igemm_row_kernel");
   // Compile-time tile geometry: one swizzle row holds SUBK channels (32/64/128 B).
@@ -402,7 +403,48 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 #pragma unroll
     for (int i = 0; i < 16; ++i) bv[i] = bias_next[i];
     if (c + 16 < c_end) load_bias16(nb + 16, bias_next);
-    if (a.split_k == 1) {
+    if (a.split_k == 1 && a.y_tma) {
+      // Stage the tile in the (now idle) ring in the swizzled layout of the y
+      // tensor map's box (IB-byte rows, BN / (IB / EB) boxes side by side); rows
+      // past M and columns past K are clipped by the TMA store.
+      if (row_ok) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float t = __uint_as_float(raw[i]) + bv[i];
+          v[i] = a.relu ? fmaxf(t, 0.0f) : t;
+        }
+        const uint32_t EB = a.out_f32 ? 4u : 2u;
+        const uint32_t IB = BN * EB < 128u ? BN * EB : 128u;
+        const uint32_t cb = (uint32_t)c * EB, j = cb / IB, cin = cb % IB;
+        uint8_t* sub = smem_raw + (size_t)j * BM * IB;
+        const uint32_t swm = IB / 16 - 1;
+        if (a.out_f32) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t off = (uint32_t)row * IB + cin + q * 16;
+            off ^= ((off >> 7) & swm) << 4;
+            *reinterpret_cast<float4*>(sub + off) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint32_t off = (uint32_t)row * IB + cin + q * 16;
+            off ^= ((off >> 7) & swm) << 4;
+            uint4 u;
+            __nv_bfloat162 b0 = __floats2bfloat162_rn(v[8 * q], v[8 * q + 1]);
+            __nv_bfloat162 b1 = __floats2bfloat162_rn(v[8 * q + 2], v[8 * q + 3]);
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * q + 4], v[8 * q + 5]);
+            __nv_bfloat162 b3 = __floats2bfloat162_rn(v[8 * q + 6], v[8 * q + 7]);
+            u.x = *reinterpret_cast<uint32_t*>(&b0);
+            u.y = *reinterpret_cast<uint32_t*>(&b1);
+            u.z = *reinterpret_cast<uint32_t*>(&b2);
+            u.w = *reinterpret_cast<uint32_t*>(&b3);
+            *reinterpret_cast<uint4*>(sub + off) = u;
+          }
+        }
+      }
+    } else if (a.split_k == 1) {
       if (m_ok && nb < a.K) {
         float v[16];
 #pragma unroll
@@ -443,6 +485,18 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     }
   }
 
+  if (a.split_k == 1 && a.y_tma) {
+    // generic-proxy smem writes -> visible to the TMA engine; one thread stores.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int EB = a.out_f32 ? 4 : 2;
+      const int IB = BN * EB < 128 ? BN * EB : 128;
+      for (int j = 0; j < BN * EB / IB; ++j)
+        tma_store_2d(&tmY, smem_raw + (size_t)j * BM * IB, nbase + j * (IB / EB), m0);
+      tma_store_commit_wait();
+    }
+  }
   if (a.split_k > 1 && a.cluster_red) {
     // Owner side: the threads whose row this CTA owns wait for the other
     // splits' slices, sum all split_k slices in split order (deterministic),
@@ -544,7 +598,8 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 // tap), one im2col box + one weight box per k-block.
 template <int BM, int BN, int BK, bool ROW>
 __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                       const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+                                                       const __grid_constant__ CUtensorMap tmB,
+                                                       const __grid_constant__ CUtensorMap, TcArgs a) {
   static_assert(!ROW || BK == 64, "row-halo k-blocks are 64 channels");
   constexpr int SUBK = BK < 64 ? BK : 64;
   constexpr int NSUB = BK / SUBK;
@@ -814,7 +869,7 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
 }
 
 // ------------------------------------------------------------- host side
-using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, TcArgs);
+using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, TcArgs);
 
 template <int BM, int BN, int MODE>
 static KernelFn pick_bk(int bk) {
@@ -1070,6 +1125,31 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     return TP_ECUDA;
   }
   }
+  // TMA-store epilogue (igemm_tc_kernel, split 1): y viewed as [M][K], box
+  // (IB / EB columns, BM rows) with the swizzle of IB-byte rows; the tile is
+  // staged in the ring, so it must fit there.
+  int y_tma = 0;
+  {
+    static const bool no_ytma = getenv("TP_NO_YTMA") && atoi(getenv("TP_NO_YTMA")) != 0;
+    const int eb = pb.out_f32 ? 4 : 2;
+    const int ib = pb.bn * eb < 128 ? pb.bn * eb : 128;
+    const size_t ring = (size_t)pb.stages * (pb.bm + pb.bn) * pb.bk * 2;
+    if (!no_ytma && !pb.row && !pb.mt && pb.split_k == 1 && (size_t)pb.bm * pb.bn * eb <= ring &&
+        ((size_t)pb.K * eb) % 16 == 0) {
+      cuuint64_t dims[2] = {(cuuint64_t)pb.K, (cuuint64_t)pb.M};
+      cuuint64_t strides[1] = {(cuuint64_t)pb.K * eb};
+      cuuint32_t box[2] = {(cuuint32_t)(ib / eb), (cuuint32_t)pb.bm};
+      cuuint32_t es[2] = {1, 1};
+      const CUtensorMapSwizzle sw = ib == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                              : (ib == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+      CUresult ry = drv.encodeTiled(&plan->tmY, pb.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                           : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                    2, pb.y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      y_tma = ry == CUDA_SUCCESS ? 1 : 0;
+    }
+    if (!y_tma) std::memset(&plan->tmY, 0, sizeof(plan->tmY));
+  }
   TcArgs& a = plan->args;
   a.M = pb.M; a.K = pb.K; a.P = pb.P; a.Q = pb.Q; a.S = pb.S;
   a.sh = pb.sh; a.sw = pb.sw; a.ph = pb.ph; a.pw = pb.pw;
@@ -1101,6 +1181,7 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   }
   a.w_early = 0;   // set per launch sequence by the runtime (time_plan / tuner phase B)
   a.a_tiled = a_tiled ? 1 : 0;
+  a.y_tma = y_tma;
   plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.mt ? 3 : (pb.row ? 2 : (pb.gather ? 1 : 0))));
   if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN x BK"); return TP_EINVALID_CONFIG; }
   plan->grid = (pb.row || pb.mt)
@@ -1158,7 +1239,7 @@ cudaError_t tc_launch(const TcPlan& plan, cudaStream_t stream) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, fn, plan.tmA, plan.tmB, plan.args);
+  return cudaLaunchKernelEx(&cfg, fn, plan.tmA, plan.tmB, plan.tmY, plan.args);
 }
 
 int tc_occupancy(const TcPlan& plan) {

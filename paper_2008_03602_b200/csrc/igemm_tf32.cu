@@ -35,7 +35,8 @@ namespace tp {
 
 template <int BM, int BN>
 __global__ void __launch_bounds__(256) igemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                         const __grid_constant__ CUtensorMap tmB, TcArgs a) {
+                                                         const __grid_constant__ CUtensorMap tmB,
+                                                         const __grid_constant__ CUtensorMap, TcArgs a) {
   constexpr uint32_t A_T = BM * 128, B_T = BN * 128;   // one k-block tile: rows x 32 fp32 channels
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
   // kind::tf32: D = F32 (bit 4), A = B = TF32 (format 2 at bits 7 and 10), K-major A and B.

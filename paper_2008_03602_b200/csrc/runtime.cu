@@ -346,8 +346,12 @@ static WsLayout ws_layout(const Layer& L, const tp_schedule& s) {
   return w;
 }
 
+// sm_count: SMs of the partition the plan runs in (the TMA-store epilogue is
+// kept only when the grid has more CTAs than that: a single wave is latency-
+// bound and plain 16-byte stores retire sooner; several waves are store-
+// throughput-bound and the staged TMA store writes whole lines).
 static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* x, const void* w,
-                           const void* bias, void* y, void* ws, size_t ws_bytes, ConvPlan* plan) {
+                           const void* bias, void* y, void* ws, size_t ws_bytes, ConvPlan* plan, int sm_count) {
   tp_schedule s = s_in;
   if (!schedule_in_space(L, s)) {
     set_error("schedule is not in this layer's v0 space");
@@ -404,6 +408,8 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     tp_status st = tc_prepare(pb, &plan->tc);
     if (st != TP_OK) return st;
     plan->ctas_per_sm = tc_occupancy(plan->tc);
+    const int64_t ctas = (int64_t)plan->tc.grid.x * plan->tc.grid.y * plan->tc.grid.z;
+    if (plan->tc.args.y_tma && ctas <= (int64_t)sm_count) plan->tc.args.y_tma = 0;
   } else {
     tp_status st = direct_prepare(L, s, xk, w, reinterpret_cast<const float*>(bias), yk, &plan->dp);
     if (st != TP_OK) return st;
@@ -710,7 +716,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     for (int32_t i = 0; i < n_cand; ++i) {
       Cand& c = cs[i];
       if (cand[i] < 0 || cand[i] >= (int64_t)table.size()) { c.m.status = TP_EINVALID_CONFIG; continue; }
-      tp_status s2 = make_plan(L, table[cand[i]], x, w, bias, y, ws, ws_bytes, &c.plan);
+      tp_status s2 = make_plan(L, table[cand[i]], x, w, bias, y, ws, ws_bytes, &c.plan, part->sm_granted);
       if (s2 == TP_OK) {
         plan_geometry(c.plan, part->sm_granted, &c.m);
         s2 = gate_check(part, c.plan, gate, &c.m);
@@ -757,7 +763,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         Cand& c = cs[i];
         if (cand[i] < 0 || cand[i] >= (int64_t)table.size()) { c.m.status = TP_EINVALID_CONFIG; continue; }
         const auto tm0 = std::chrono::steady_clock::now();
-        tp_status s2 = make_plan(L, table[cand[i]], x, w, bias, y, ws, ws_bytes, &c.plan);
+        tp_status s2 = make_plan(L, table[cand[i]], x, w, bias, y, ws, ws_bytes, &c.plan, part->sm_granted);
         if (prof) host_a_plan_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tm0).count();
         if (s2 != TP_OK) { c.m.status = s2; continue; }
         plan_geometry(c.plan, part->sm_granted, &c.m);
@@ -1261,7 +1267,7 @@ tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partitio
   std::lock_guard<std::mutex> lk(p->mu);
   CtxGuard g(p);
   ConvPlan plan;
-  st = make_plan(L, *s, x, w, bias, y, ws, ws_bytes, &plan);
+  st = make_plan(L, *s, x, w, bias, y, ws, ws_bytes, &plan, p->sm_granted);
   if (st != TP_OK) return st;
   if (!timing && !out) {
     TP_CK(launch_plan(plan, p->stream));
@@ -1295,7 +1301,7 @@ tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partit
   ConvPlan plan;
   {
     CtxGuard g(p);
-    st = make_plan(L, *s, x, w, bias, y, ws, ws_bytes, &plan);
+    st = make_plan(L, *s, x, w, bias, y, ws, ws_bytes, &plan, p->sm_granted);
   }
   if (st != TP_OK) return st;
   const int64_t ctas = (int64_t)plan.tc.grid.x * plan.tc.grid.y * plan.tc.grid.z;

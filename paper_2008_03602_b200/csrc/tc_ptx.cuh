@@ -118,6 +118,19 @@ static __device__ __forceinline__ void tc_mma_tf32_p(uint32_t tmem_d, uint64_t a
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(lead)
       : "memory");
 }
+// TMA 2-D tile store shared -> global (bulk group), commit and wait until the
+// shared-memory source has been read (the global writes complete with the grid,
+// before any dependent grid's griddepcontrol.wait returns).
+static __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+static __device__ __forceinline__ void tma_store_commit_wait() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 static __device__ __forceinline__ void tc_commit_p(uint64_t* bar, uint32_t lead) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"

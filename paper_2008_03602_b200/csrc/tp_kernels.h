@@ -74,6 +74,7 @@ struct TcArgs {
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
   int dbg;                     // TP_DEBUG_TC env (experiments only): bit0 skip A TMA, bit1 skip B TMA
   int a_tiled;                 // 1: A is a tiled [M][C] map (1x1 / stride 1 / pad 0 layers), not im2col
+  int y_tma;                   // igemm_tc split 1: epilogue staged in the ring smem, TMA 2-D store of y
   int R, pcols, patch_off;     // stem kind: filter rows, patch pixels per row, patch offset in smem
   int w_early;                 // 1: weight (B) boxes of the first ring pass are issued before
                                //    griddepcontrol.wait -- only when the preceding kernel in the
@@ -103,6 +104,7 @@ struct TcProblem {
 
 struct TcPlan {
   CUtensorMap tmA, tmB;
+  CUtensorMap tmY;   // output [M][K] tiled map for the TMA-store epilogue (TcArgs::y_tma)
   TcArgs args;
   const void* fn = nullptr;
   dim3 grid, block;

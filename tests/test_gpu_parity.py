@@ -354,3 +354,30 @@ def test_stem_vgg_conv1_1_sampled_points():
         tp.conv2d_run(buf, s)
         torch.cuda.synchronize()
         assert rel_err(buf.gather(idx), ref) <= 2e-2, s
+
+
+@pytest.mark.parametrize("d", TC_TINY[:3] + [mk(1, 64, 128, 128, 128, 3, 3, 1, 1, out=tp.FP32, epi=1),
+                                             mk(1, 64, 40, 40, 96, 1, 1, 1, 0, epi=3)],
+                         ids=lambda d: f"ytma_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_r{d['r']}_o{d['out_dtype']}")
+def test_tma_store_epilogue_bit_exact_small_partition(d):
+    """In a 14-SM partition most split-1 grids have more CTAs than SMs, so the
+    staged TMA-store epilogue (TcArgs::y_tma) writes y: every tensor-core
+    schedule must still match the oracle (bit-exactly on integers; the bf16
+    output case within one bf16 rounding)."""
+    part = tp.Partition.get(0.1)
+    x, w, b = datagen.make_inputs(d, 29, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b, part=part)
+    bad = []
+    for i in range(tp.space_size(d)):
+        s = tp.space_get(d, i)
+        if s["kind"] not in (tp.KIND_IGEMM_TC, tp.KIND_IGEMM_TC_GATHER) or s["split_k"] != 1:
+            continue
+        buf.poison()
+        tp.conv2d_run(buf, s, part)
+        part.sync()
+        y = buf.output()
+        ok = np.array_equal(y, ref) if d["out_dtype"] == tp.FP32 else rel_err(y, ref) <= 2 ** -8
+        if not ok:
+            bad.append((i, s["bm"], s["bn"], s["bk"], s["stages"]))
+    assert not bad, f"{len(bad)} schedules differ, first: {bad[:5]}"
