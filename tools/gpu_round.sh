@@ -13,3 +13,4 @@ timeout 1800 python tools/report.py concurrent gpurun_out/r01_concurrent_vgg19.j
 timeout 900 python tools/report.py tune gpurun_out/r01_tune_mbv2_50.json > gpurun_out/mbv2.log 2>&1
 ls -la gpurun_out | tail -20
 timeout 600 python tools/report.py tune --workload cfg1 --fraction 1.0 gpurun_out/r01_tune_cfg1_100.json > gpurun_out/cfg1.log 2>&1
+timeout 1200 python tools/report.py interference gpurun_out/r01_interference_r50.json > gpurun_out/interference.log 2>&1
