@@ -173,12 +173,13 @@ def stem_kp(d: dict) -> int:
 
 
 def _valid_stem(d: dict, bm: int, bn: int, tiles_per_cta: int) -> bool:
-    # resident weights bn x KP, two im2col tiles bm x KP (bf16), the input patch
-    # R x ((bm-1) s_w + S) x C bf16 rounded up to 1 KiB, the KP-entry k table, barriers
+    # resident weights bn x KP, two im2col tiles bm x KP (bf16), two input patches of
+    # R rows x ((bm-1) s_w + S) C + 2 bf16 each rounded up to 1 KiB, the KP-entry k table, barriers
     P, Q = out_pq(d)
     kp = stem_kp(d)
     cols = (bm - 1) * d["stride_w"] + d["s"]
-    patch = _cdiv(d["r"] * cols * d["c"] * 2, 1024) * 1024
+    prow = (cols * d["c"] + 3) // 2 * 2          # even row pitch >= cols C + 1 (a row starts on a word)
+    patch = 2 * _cdiv(d["r"] * prow * 2, 1024) * 1024   # two buffers
     if bn * kp * 2 + 2 * bm * kp * 2 + patch + kp * 4 + 1024 > SMEM_LIMIT:
         return False
     return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))

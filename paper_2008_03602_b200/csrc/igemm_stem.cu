@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   const int KP = a.bk, NSUB = KP >> 6, CH = KP >> 3;        // 16-byte chunks per row
   uint8_t* b_s = smem_raw;
   uint8_t* a_s = smem_raw + (size_t)NSUB * B_SUB;
-  uint16_t* patch = reinterpret_cast<uint16_t*>(smem_raw + a.patch_off);
+  uint16_t* patch0 = reinterpret_cast<uint16_t*>(smem_raw + a.patch_off);   // two buffers of a.pbuf bytes
   int* ktab = reinterpret_cast<int*>(smem_raw + a.tab_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + a.bar_off);
   uint64_t* b_full = bars;        // weights staged (3 producer warps)
@@ -59,7 +59,10 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   const int tile0 = blockIdx.x * a.tpc;
   const int ntl = a.ntiles - tile0 < a.tpc ? a.ntiles - tile0 : a.tpc;
   const int nbase = blockIdx.y * BN;
-  const int C = a.C, cols = a.pcols, rowlen = cols * C;     // patch row: cols pixels x C channels
+  // Patch row r of a tile holds input elements e0 - sh1 .. e0 - sh1 + prow - 1 of
+  // input row h0 + r (e0 = (q0 s_w - p_w) C; sh1 = (p_w C) & 1 makes the row
+  // start on a 4-byte word, since q0 s_w C is even).
+  const int C = a.C, prow = a.prow, sh1 = (a.pw * C) & 1;
 
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     int v = -1;
     if (k < a.Kg) {
       const int c = k % C, rs = k / C, s = rs % a.S, r = rs / a.S;
-      v = r * rowlen + s * C + c;
+      v = r * prow + sh1 + s * C + c;
     }
     ktab[k] = v;
   }
@@ -118,21 +121,48 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     if (lane == 0) mbar_arrive(b_full);
 
     const int WC = a.W * C;
-    for (int i = 0; i < ntl; ++i) {
-      const int t = tile0 + i, b = i & 1;
-      const int qb = t % a.nqb, prow = t / a.nqb, p = prow % a.P, n = prow / a.P;
-      const int q0 = qb * BM;
-      // Input patch: R contiguous segments of the NHWC input (zero outside the image).
-      const int e0 = (q0 * a.sw - a.pw) * C;   // element offset of the patch start in an input row
+    const int nw = prow >> 1;   // 4-byte words per patch row
+    // Stream tile t's patch into buffer pb: with cp.async (4-byte words, zero
+    // fill outside the image) when the input rows are whole words, else by
+    // plain loads.
+    auto stage_patch = [&](int t, int pbi) {
+      const int qb = t % a.nqb, prw = t / a.nqb, p = prw % a.P, n = prw / a.P;
+      const int e0 = (qb * BM * a.sw - a.pw) * C - sh1;
+      const int h0 = p * a.sh - a.ph;
+      uint16_t* pbase = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(patch0) + (size_t)pbi * a.pbuf);
+      const uint16_t* ximg = xg + (int64_t)n * a.H * WC;
       for (int r = 0; r < a.R; ++r) {
-        const int h = p * a.sh - a.ph + r;
+        const int h = h0 + r;
         const bool hv = (unsigned)h < (unsigned)a.H;
-        const uint16_t* xr = xg + ((int64_t)n * a.H + (hv ? h : 0)) * WC;
-        uint16_t* pr = patch + r * rowlen;
-        for (int e = pt; e < rowlen; e += kProd) {
-          const int gi = e0 + e;
-          pr[e] = (hv && (unsigned)gi < (unsigned)WC) ? __ldg(xr + gi) : (uint16_t)0;
+        const uint16_t* xr = ximg + (int64_t)(hv ? h : 0) * WC;
+        uint16_t* pr = pbase + r * prow;
+        if (a.pc_async) {
+          for (int wi = pt; wi < nw; wi += kProd) {
+            const int g = e0 + 2 * wi;
+            const bool ok = hv && g >= 0 && g < WC;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(pr + 2 * wi)),
+                         "l"(ok ? xr + g : xr), "r"(ok ? 4 : 0)
+                         : "memory");
+          }
+        } else {
+          for (int e = pt; e < prow; e += kProd) {
+            const int g = e0 + e;
+            pr[e] = (hv && (unsigned)g < (unsigned)WC) ? __ldg(xr + g) : (uint16_t)0;
+          }
         }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (ntl > 0) stage_patch(tile0, 0);
+    for (int i = 0; i < ntl; ++i) {
+      const int b = i & 1;
+      const uint16_t* patch =
+          reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(patch0) + (size_t)b * a.pbuf);
+      if (i + 1 < ntl) {
+        stage_patch(tile0 + i + 1, b ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       asm volatile("bar.sync 1, 96;" ::: "memory");
       // Expand into the swizzled im2col tile b (after the MMAs of tile i-2 released it).
@@ -155,7 +185,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full + b);
-      asm volatile("bar.sync 1, 96;" ::: "memory");   // the patch is reused for the next tile
+      asm volatile("bar.sync 1, 96;" ::: "memory");   // buffer b is refilled for tile i + 2
     }
   } else if (warp == 3) {
     // ---------------- MMA issuer ----------------

@@ -1018,7 +1018,11 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   a.nqb = (pb.Q + pb.bm - 1) / pb.bm;
   a.ntiles = pb.N * pb.P * a.nqb;
   a.tpc = pb.tpc > 1 ? pb.tpc : 1;
-  const size_t patch = ((size_t)pb.R * a.pcols * pb.C * 2 + 1023) / 1024 * 1024;
+  // Two patch buffers of R rows x prow elements (prow = pcols C + 2: a row starts on a 4-byte word).
+  a.prow = (a.pcols * pb.C + 3) & ~1;   // even pitch >= pcols C + 1 (row shifted by (pw C) & 1)
+  a.pbuf = (int)(((size_t)pb.R * a.prow * 2 + 1023) / 1024 * 1024);
+  a.pc_async = ((pb.W * pb.C) % 2 == 0) ? 1 : 0;   // cp.async 4-byte words need even rows
+  const size_t patch = 2 * (size_t)a.pbuf;
   a.patch_off = (int)((size_t)pb.bn * kp * 2 + 2 * (size_t)pb.bm * kp * 2);
   a.tab_off = a.patch_off + (int)patch;
   a.bar_off = a.tab_off + kp * 4;

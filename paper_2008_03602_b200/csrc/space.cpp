@@ -210,9 +210,12 @@ static const int kStemBM[] = {64, 128};
 static const int kStemBN[] = {32, 64, 128};
 static const int kStemTpc[] = {2, 4, 8, 16};
 int64_t stem_kp(const Layer& L) { return cdiv((int64_t)L.d.r * L.d.s * L.d.c, 64) * 64; }
+// Two patch buffers (the next tile's patch streams in while this tile's im2col
+// tile is built), rows padded by 2 elements (a row starts on a 4-byte word).
 int64_t stem_patch_bytes(const Layer& L, int bm) {
   const int64_t cols = (int64_t)(bm - 1) * L.d.stride_w + L.d.s;
-  return cdiv((int64_t)L.d.r * cols * L.d.c * 2, 1024) * 1024;
+  const int64_t prow = (cols * L.d.c + 3) & ~(int64_t)1;   // even row pitch >= cols C + 1
+  return 2 * cdiv((int64_t)L.d.r * prow * 2, 1024) * 1024;
 }
 int64_t stem_smem_bytes(const Layer& L, int bm, int bn) {
   const int64_t kp = stem_kp(L);

@@ -76,6 +76,7 @@ struct TcArgs {
   int a_tiled;                 // 1: A is a tiled [M][C] map (1x1 / stride 1 / pad 0 layers), not im2col
   int y_tma;                   // igemm_tc split 1: epilogue staged in the ring smem, TMA 2-D store of y
   int R, pcols, patch_off;     // stem kind: filter rows, patch pixels per row, patch offset in smem
+  int prow, pbuf, pc_async;    // stem kind: patch row pitch (elements), bytes per patch buffer, cp.async path
   int w_early;                 // 1: weight (B) boxes of the first ring pass are issued before
                                //    griddepcontrol.wait -- only when the preceding kernel in the
                                //    stream is a launch of this plan (weights are layer constants)
