@@ -180,7 +180,8 @@ def _valid_stem(d: dict, bm: int, bn: int, tiles_per_cta: int) -> bool:
     cols = (bm - 1) * d["stride_w"] + d["s"]
     prow = (cols * d["c"] + 3) // 2 * 2          # even row pitch >= cols C + 1 (a row starts on a word)
     patch = 2 * _cdiv(d["r"] * prow * 2, 1024) * 1024   # two buffers
-    if bn * kp * 2 + 2 * bm * kp * 2 + patch + kp * 4 + 1024 > SMEM_LIMIT:
+    stage = bm * bn * 4                          # output staging of the TMA-store epilogue (fp32 size)
+    if bn * kp * 2 + 2 * bm * kp * 2 + patch + _cdiv(kp * 4, 1024) * 1024 + stage + 1024 > SMEM_LIMIT:
         return False
     return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))
 

@@ -34,7 +34,7 @@ namespace tp {
 
 template <int BM, int BN>
 __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
-                                                         const __grid_constant__ CUtensorMap, TcArgs a) {   // (no tensor maps: same launch signature as igemm_tc)
+                                                         const __grid_constant__ CUtensorMap tmY, TcArgs a) {   // (no tensor maps: same launch signature as igemm_tc)
   constexpr uint32_t A_SUB = BM * 128, B_SUB = BN * 128;   // one 64-element (128-B) k column block
   constexpr uint32_t kTmemCols = 2 * BN;                   // two accumulators
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -209,40 +209,88 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     }
   } else {
     // ---------------- epilogue (warps 4-7) ----------------
+    // y_tma: the tile is staged in its own buffer in the swizzled box layout of
+    // a 3-D [N P][Q][K] map (q >= Q clipped by the store) and written by one
+    // 2-D-per-column-block TMA store; else 16-byte row stores.
     const int quad = warp & 3;
     const int row = (BM == 128) ? quad * 32 + lane : quad * 16 + lane;
     const bool row_ok = (BM == 128 || lane < 16);
+    uint8_t* stg = smem_raw + a.recv_off;
+    const uint32_t EB = a.out_f32 ? 4u : 2u;
+    const uint32_t IB = BN * EB < 128u ? BN * EB : 128u;
     for (int i = 0; i < ntl; ++i) {
       const int t = tile0 + i, b = i & 1;
-      const int qb = t % a.nqb, prow = t / a.nqb;
+      const int qb = t % a.nqb, prw = t / a.nqb;
       const int q = qb * BM + row;
       __syncwarp();
       mbar_wait(t_full + b, (uint32_t)(i >> 1) & 1u);
       tc_fence_after();
+      if (a.y_tma) {
+        // the previous tile's store must have read the staging buffer
+        if (threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+      }
       for (int c = 0; c < BN; c += 16) {
         uint32_t raw[16];
         tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * BN + c), raw);
         const int nb = nbase + c;
-        if (row_ok && q < a.Q && nb < a.K) {
-          float v[16];
+        float v[16];
 #pragma unroll
-          for (int g = 0; g < 16; g += 4) {
-            float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (a.has_bias && nb + g + 4 <= a.K) bv = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
-            const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
+        for (int g = 0; g < 16; g += 4) {
+          float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (a.has_bias && nb + g + 4 <= a.K) bv = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
+          const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float s = __uint_as_float(raw[g + j]) + b4[j];
-              v[g + j] = a.relu ? fmaxf(s, 0.0f) : s;
+          for (int j = 0; j < 4; ++j) {
+            const float sv = __uint_as_float(raw[g + j]) + b4[j];
+            v[g + j] = a.relu ? fmaxf(sv, 0.0f) : sv;
+          }
+        }
+        if (a.y_tma) {
+          if (row_ok) {
+            const uint32_t cb = (uint32_t)c * EB, j = cb / IB, cin = cb % IB;
+            uint8_t* sub = stg + (size_t)j * BM * IB;
+            const uint32_t swm = IB / 16 - 1;
+            for (uint32_t qq = 0; qq < 16 * EB / 16; ++qq) {
+              uint32_t off = (uint32_t)row * IB + cin + qq * 16;
+              off ^= ((off >> 7) & swm) << 4;
+              uint4 u;
+              if (a.out_f32) {
+                u = make_uint4(__float_as_uint(v[4 * qq]), __float_as_uint(v[4 * qq + 1]),
+                               __float_as_uint(v[4 * qq + 2]), __float_as_uint(v[4 * qq + 3]));
+              } else {
+                __nv_bfloat162 b0 = __floats2bfloat162_rn(v[8 * qq], v[8 * qq + 1]);
+                __nv_bfloat162 b1 = __floats2bfloat162_rn(v[8 * qq + 2], v[8 * qq + 3]);
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * qq + 4], v[8 * qq + 5]);
+                __nv_bfloat162 b3 = __floats2bfloat162_rn(v[8 * qq + 6], v[8 * qq + 7]);
+                u = make_uint4(*reinterpret_cast<uint32_t*>(&b0), *reinterpret_cast<uint32_t*>(&b1),
+                               *reinterpret_cast<uint32_t*>(&b2), *reinterpret_cast<uint32_t*>(&b3));
+              }
+              *reinterpret_cast<uint4*>(sub + off) = u;
             }
           }
-          store16(a.y, (int64_t)prow * a.Q + q, a.K, nb, v, a.out_f32);
+        } else if (row_ok && q < a.Q && nb < a.K) {
+          store16(a.y, (int64_t)prw * a.Q + q, a.K, nb, v, a.out_f32);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(t_empty + b);
+      if (a.y_tma) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (threadIdx.x == 128) {
+          for (uint32_t j = 0; j < BN * EB / IB; ++j)
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tmY)),
+                         "r"(smem_u32(stg + (size_t)j * BM * IB)), "r"((int)(nbase + j * (IB / EB))),
+                         "r"(qb * BM), "r"(prw)
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
     }
+    if (a.y_tma && threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();

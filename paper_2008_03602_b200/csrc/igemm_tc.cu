@@ -1005,6 +1005,7 @@ static tp_status tf32_prepare(const TcProblem& pb, bool a_tiled, TcPlan* plan) {
 static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   std::memset(&plan->tmA, 0, sizeof(plan->tmA));
   std::memset(&plan->tmB, 0, sizeof(plan->tmB));
+  std::memset(&plan->tmY, 0, sizeof(plan->tmY));
   TcArgs& a = plan->args;
   std::memset(&a, 0, sizeof(a));
   const int kg = pb.R * pb.S * pb.C;
@@ -1025,7 +1026,26 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   const size_t patch = 2 * (size_t)a.pbuf;
   a.patch_off = (int)((size_t)pb.bn * kp * 2 + 2 * (size_t)pb.bm * kp * 2);
   a.tab_off = a.patch_off + (int)patch;
-  a.bar_off = a.tab_off + kp * 4;
+  // Output staging for the TMA-store epilogue (reserved at fp32 size: the space's budget).
+  a.recv_off = (a.tab_off + kp * 4 + 1023) / 1024 * 1024;
+  a.bar_off = a.recv_off + pb.bm * pb.bn * 4;
+  {
+    static const bool no_ytma = getenv("TP_NO_YTMA") && atoi(getenv("TP_NO_YTMA")) != 0;
+    const int eb = pb.out_f32 ? 4 : 2;
+    const int ib = pb.bn * eb < 128 ? pb.bn * eb : 128;
+    cuuint64_t dims[3] = {(cuuint64_t)pb.K, (cuuint64_t)pb.Q, (cuuint64_t)pb.N * pb.P};
+    cuuint64_t strides[2] = {(cuuint64_t)pb.K * eb, (cuuint64_t)pb.Q * pb.K * eb};
+    cuuint32_t box[3] = {(cuuint32_t)(ib / eb), (cuuint32_t)pb.bm, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUtensorMapSwizzle sw = ib == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                            : (ib == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    a.y_tma = 0;
+    if (!no_ytma && ((size_t)pb.K * eb) % 16 == 0 &&
+        driver().encodeTiled(&plan->tmY, pb.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                             3, pb.y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      a.y_tma = 1;
+  }
   plan->fn = pick_stem(pb.bm, pb.bn);
   if (!plan->fn) { set_error("no igemm_stem instantiation for this BM x BN"); return TP_EINVALID_CONFIG; }
   plan->grid = dim3((unsigned)((a.ntiles + a.tpc - 1) / a.tpc), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u);

@@ -219,7 +219,9 @@ int64_t stem_patch_bytes(const Layer& L, int bm) {
 }
 int64_t stem_smem_bytes(const Layer& L, int bm, int bn) {
   const int64_t kp = stem_kp(L);
-  return (int64_t)bn * kp * 2 + 2 * (int64_t)bm * kp * 2 + stem_patch_bytes(L, bm) + kp * 4 + 1024;
+  // + the output staging of the TMA-store epilogue (BM x BN at fp32 size, 1 KiB aligned)
+  return (int64_t)bn * kp * 2 + 2 * (int64_t)bm * kp * 2 + stem_patch_bytes(L, bm) + cdiv(kp * 4, 1024) * 1024 +
+         (int64_t)bm * bn * 4 + 1024;
 }
 static bool valid_stem(const Layer& L, int bm, int bn) {
   if (stem_smem_bytes(L, bm, bn) > kSmemLimit) return false;

@@ -81,8 +81,9 @@ def test_gather_space_hand_count():
 def test_stem_kind_hand_count():
     # R50 conv1 (C=3, 7x7 s2 p3, Q=112): KP = 64 ceil(147/64) = 192; BM {64, 128} (<= np2(112));
     # BN <= max(32, np2(64)) -> {32, 64}; tiles_per_cta {2, 4, 8, 16}; the largest smem
-    # (BM=128, BN=64) = 64*192*2 + 2*128*192*2 + 2 ceil(7*786*2/1024) KiB + 192*4 + 1024
-    # = 24576 + 98304 + 22528 + 768 + 1024 = 147200 fits: 2 x 2 x 4 = 16, appended after the gathered tuples.
+    # (BM=128, BN=64) = 64*192*2 + 2*128*192*2 + 2 ceil(7*786*2/1024) KiB + 1 KiB (k table) + 128*64*4
+    # (output staging) + 1024 = 24576 + 98304 + 22528 + 1024 + 32768 + 1024 = 180224 fits: 2 x 2 x 4 = 16,
+    # appended after the gathered tuples.
     d = wl.catalog("resnet50")[0]
     sps = sp.enumerate_space(d)
     st = [s for s in sps if s["kind"] == sp.KIND_IGEMM_TC_STEM]
