@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 template <int BM, int BN, int BK, bool ROW>
 __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
-                                                       const __grid_constant__ CUtensorMap, TcArgs a) {
+                                                       const __grid_constant__ CUtensorMap tmY, TcArgs a) {
   static_assert(!ROW || BK == 64, "row-halo k-blocks are 64 channels");
   constexpr int SUBK = BK < 64 ? BK : 64;
   constexpr int NSUB = BK / SUBK;
@@ -810,10 +810,22 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
     }
     const int row = (BM == 128) ? quad * 32 + lane : quad * 16 + lane;
     const bool row_ok = (BM == 128 || lane < 16);
+    // y_tma: stage each tile in its own buffer (after the barriers) in the box
+    // layout of the y map -- 3-D [N P][Q][K] for row tiles (q >= Q clipped), 2-D
+    // [M][K] for multi-tile im2col tiles -- and store it with TMA from one thread.
+    const int n_epi = n_epi_warps * 32;
+    const int issuer = split_roles ? 64 : 0;
+    uint8_t* stg = smem_raw + a.recv_off;
+    const uint32_t EB = a.out_f32 ? 4u : 2u;
+    const uint32_t IB = BN * EB < 128u ? BN * EB : 128u;
     for (int i = 0; i < ntl; ++i) {
       const int buf = i & 1;
       int q0, p0, n0, mrow0, mvalid;
       tile_coords(tile0 + i, q0, p0, n0, mrow0, mvalid);
+      if (a.y_tma) {   // the previous tile's store must have read the staging buffer
+        if ((int)threadIdx.x == issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"r"(n_epi) : "memory");
+      }
       float bv[16];
       const int nb0 = nbase + c_begin;
 #pragma unroll
@@ -843,7 +855,36 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
             }
           }
         }
-        if (row_ok && row < mvalid && nb < a.K) {
+        if (a.y_tma) {
+          if (row_ok) {
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float t = __uint_as_float(raw[j]) + bv[j];
+              v[j] = a.relu ? fmaxf(t, 0.0f) : t;
+            }
+            const uint32_t cb = (uint32_t)c * EB, jb = cb / IB, cin = cb % IB;
+            uint8_t* sub = stg + (size_t)jb * BM * IB;
+            const uint32_t swm = IB / 16 - 1;
+            for (uint32_t qq = 0; qq < EB; ++qq) {   // 16 values = EB 16-byte pieces
+              uint32_t off = (uint32_t)row * IB + cin + qq * 16;
+              off ^= ((off >> 7) & swm) << 4;
+              uint4 u;
+              if (a.out_f32) {
+                u = make_uint4(__float_as_uint(v[4 * qq]), __float_as_uint(v[4 * qq + 1]),
+                               __float_as_uint(v[4 * qq + 2]), __float_as_uint(v[4 * qq + 3]));
+              } else {
+                __nv_bfloat162 b0 = __floats2bfloat162_rn(v[8 * qq], v[8 * qq + 1]);
+                __nv_bfloat162 b1 = __floats2bfloat162_rn(v[8 * qq + 2], v[8 * qq + 3]);
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[8 * qq + 4], v[8 * qq + 5]);
+                __nv_bfloat162 b3 = __floats2bfloat162_rn(v[8 * qq + 6], v[8 * qq + 7]);
+                u = make_uint4(*reinterpret_cast<uint32_t*>(&b0), *reinterpret_cast<uint32_t*>(&b1),
+                               *reinterpret_cast<uint32_t*>(&b2), *reinterpret_cast<uint32_t*>(&b3));
+              }
+              *reinterpret_cast<uint4*>(sub + off) = u;
+            }
+          }
+        } else if (row_ok && row < mvalid && nb < a.K) {
           float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
@@ -856,7 +897,25 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + buf);
+      if (a.y_tma) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 2, %0;" ::"r"(n_epi) : "memory");
+        if ((int)threadIdx.x == issuer) {
+          for (uint32_t jb = 0; jb < BN * EB / IB; ++jb) {
+            const int ncol = nbase + (int)(jb * (IB / EB));
+            if constexpr (ROW)
+              asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                               reinterpret_cast<uint64_t>(&tmY)),
+                           "r"(smem_u32(stg + (size_t)jb * BM * IB)), "r"(ncol), "r"(q0), "r"(n0 * a.P + p0)
+                           : "memory");
+            else
+              tma_store_2d(&tmY, stg + (size_t)jb * BM * IB, ncol, mrow0);
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
     }
+    if (a.y_tma && (int)threadIdx.x == issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
 
   tc_fence_before();
@@ -1232,6 +1291,43 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.recv_off = (int)tc_ring_bytes(pb.bm, pb.bn, pb.bk, pb.stages, pb.row != 0);
   a.tab_off = a.bar_off + 1024;
   plan->smem = (size_t)a.tab_off + (pb.gather ? (size_t)pb.bm * 16 + (size_t)a.kblocks * pb.bk * 8 : 0);
+  if (pb.row || pb.mt) {
+    // Multi-tile kinds: TMA-store epilogue from a staging buffer after the
+    // barriers, when it fits in shared memory (a launch-time choice; the space
+    // is unchanged).  The ring stays busy with the next tile meanwhile.
+    static const bool no_ytma = getenv("TP_NO_YTMA") && atoi(getenv("TP_NO_YTMA")) != 0;
+    const int eb = pb.out_f32 ? 4 : 2;
+    const int ib = pb.bn * eb < 128 ? pb.bn * eb : 128;
+    const size_t stage_bytes = (size_t)pb.bm * pb.bn * eb;
+    a.y_tma = 0;
+    if (!no_ytma && plan->smem + stage_bytes <= 232448 && ((size_t)pb.K * eb) % 16 == 0) {
+      const CUtensorMapSwizzle sw = ib == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                              : (ib == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+      const CUtensorMapDataType dt = pb.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+      CUresult ry;
+      if (pb.row) {
+        cuuint64_t dims[3] = {(cuuint64_t)pb.K, (cuuint64_t)pb.Q, (cuuint64_t)pb.N * pb.P};
+        cuuint64_t strides[2] = {(cuuint64_t)pb.K * eb, (cuuint64_t)pb.Q * pb.K * eb};
+        cuuint32_t box[3] = {(cuuint32_t)(ib / eb), (cuuint32_t)pb.bm, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        ry = drv.encodeTiled(&plan->tmY, dt, 3, pb.y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      } else {
+        cuuint64_t dims[2] = {(cuuint64_t)pb.K, (cuuint64_t)pb.M};
+        cuuint64_t strides[1] = {(cuuint64_t)pb.K * eb};
+        cuuint32_t box[2] = {(cuuint32_t)(ib / eb), (cuuint32_t)pb.bm};
+        cuuint32_t es[2] = {1, 1};
+        ry = drv.encodeTiled(&plan->tmY, dt, 2, pb.y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      }
+      if (ry == CUDA_SUCCESS) {
+        a.y_tma = 1;
+        a.recv_off = (int)((plan->smem + 1023) / 1024 * 1024);
+        plan->smem = (size_t)a.recv_off + stage_bytes;
+        if (plan->smem > 232448) { a.y_tma = 0; plan->smem = (size_t)a.tab_off; }
+      }
+    }
+  }
   cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
   if (e != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));

@@ -409,7 +409,9 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     if (st != TP_OK) return st;
     plan->ctas_per_sm = tc_occupancy(plan->tc);
     const int64_t ctas = (int64_t)plan->tc.grid.x * plan->tc.grid.y * plan->tc.grid.z;
-    if (plan->tc.args.y_tma && ctas <= (int64_t)sm_count) plan->tc.args.y_tma = 0;
+    if (plan->tc.args.y_tma && ctas <= (int64_t)sm_count &&
+        (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER))   // one tile per CTA
+      plan->tc.args.y_tma = 0;
   } else {
     tp_status st = direct_prepare(L, s, xk, w, reinterpret_cast<const float*>(bias), yk, &plan->dp);
     if (st != TP_OK) return st;
