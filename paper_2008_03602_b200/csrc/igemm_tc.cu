@@ -146,7 +146,15 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     advance(step);
   };
 
-  if (!GATHER && (warp == 0 || warp == 3)) {
+  // TMA producer warps (k-block j goes to producer j mod nprod): warp 0, 3, 2, 4
+  // in rank order, at most one per ring stage.  A TMA issue costs the issuing
+  // thread ~50-90 cycles (tools/micro/tma_issue.cu) and threads issue in parallel.
+  const int nprod_hw = blockDim.x == 256 ? 4 : 3;
+  const int nprod = nprod_hw < stages ? (nprod_hw < a.nprod ? nprod_hw : a.nprod)
+                                      : (stages < a.nprod ? stages : a.nprod);
+  const int prank = warp == 0 ? 0 : (warp == 3 ? 1 : (warp == 2 ? 2 : (warp == 4 ? 3 : 99)));
+  const bool is_prod = !GATHER && prank < nprod;
+  if (is_prod) {
     const int rs = kb0 / a.cblocks;
     p_cb = kb0 - rs * a.cblocks;
     p_s = rs % a.S;
@@ -315,8 +323,8 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       if (trace && threadIdx.x == 0 && kb - kb0 < kTraceK) trace[20 + kb - kb0] = gtimer();
       if (++stage == stages) { stage = 0; phase ^= 1u; }
     }
-  } else if (!GATHER && (warp == 0 || warp == 3)) {
-    // ---------------- TMA producers: warp 0 even, warp 3 odd k-blocks (one elected lane each) ----------------
+  } else if (is_prod) {
+    // ---------------- TMA producers: k-blocks j = prank (mod nprod), one elected lane each ----------------
     const uint32_t lead = elect_one();
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // Every operand this grid reads is now final: the next kernel in the
@@ -324,12 +332,12 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (trace && warp == 0 && lane == 0) trace[53] = gtimer();
     const int pre = a.w_early ? (nkb < stages ? nkb : stages) : 0;   // weight boxes already in flight
-    if (warp == 3) advance(1);
+    if (prank > 0) advance(prank);
     while (p_kb < kb1) {
       const int j = p_kb - kb0;
       mbar_wait(empty + p_stage, p_phase ^ 1u);   // free on the first ring pass
       if (trace && warp == 0 && lane == 0 && j < kTraceK) trace[20 + j] = gtimer();
-      produce(lead, j < pre ? 1 : 7, 2);
+      produce(lead, j < pre ? 1 : 7, nprod);
       if (trace && warp == 0 && lane == 0 && j < 8) trace[54 + j / 2] = gtimer();
     }
   } else if (warp == 1) {
@@ -1261,6 +1269,10 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   {
     static const int dbg = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
     a.dbg = dbg;
+  }
+  {
+    static const int nprod_env = getenv("TP_NPROD") ? atoi(getenv("TP_NPROD")) : 4;
+    a.nprod = nprod_env < 1 ? 1 : nprod_env;   // producer warps cap (experiments: TP_NPROD)
   }
   a.w_early = 0;   // set per launch sequence by the runtime (time_plan / tuner phase B)
   a.a_tiled = a_tiled ? 1 : 0;

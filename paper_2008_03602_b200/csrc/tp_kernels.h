@@ -74,6 +74,7 @@ struct TcArgs {
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
   int dbg;                     // TP_DEBUG_TC env (experiments only): bit0 skip A TMA, bit1 skip B TMA
   int a_tiled;                 // 1: A is a tiled [M][C] map (1x1 / stride 1 / pad 0 layers), not im2col
+  int nprod;                   // igemm_tc: cap on TMA producer warps (4 = all available)
   int y_tma;                   // igemm_tc split 1: epilogue staged in the ring smem, TMA 2-D store of y
   int R, pcols, patch_off;     // stem kind: filter rows, patch pixels per row, patch offset in smem
   int prow, pbuf, pc_async;    // stem kind: patch row pitch (elements), bytes per patch buffer, cp.async path
