@@ -331,12 +331,23 @@ def concurrent_tune(layers, k=4, sms_each=37, trials=1000, config=4, timing_cfg=
 # solo latency of the winner of a tuner that ran alone - 1.
 
 
-def _tune_share(layer_ids, layers, part, trials, config, seed):
+def _make_share_buffers(layer_ids, layers, part, config):
     out = {}
     for i in layer_ids:
         d = layers[i]
         x, w, b = datagen.make_inputs(d, datagen.data_seed(config, i))
-        buf = tp.LayerBuffers(d, x, w, b, part=part)
+        out[i] = tp.LayerBuffers(d, x, w, b, part=part)
+    return out
+
+
+def _tune_share(layer_ids, layers, part, trials, config, seed, bufs=None):
+    # Buffers are created before any concurrent tuner starts: a torch allocation
+    # in one thread while another thread's stream is capturing a CUDA graph
+    # fails with cudaErrorStreamCaptureUnsupported.
+    bufs = bufs if bufs is not None else _make_share_buffers(layer_ids, layers, part, config)
+    out = {}
+    for i in layer_ids:
+        buf = bufs[i]
         best, m, recs = tp.tune(buf, part, trials, seed)
         out[i] = {"space_index": int(best["space_index"]), "reported_us": float(m["median_us"]),
                   "candidates": len(recs)}
@@ -381,10 +392,13 @@ def interference(cat: str, k: int = 4, sms_each: int = 36, trials: int = 1000, c
         else:
             parts = iso_parts if mode == "isolated" else tp.Partition.shared(k, device=device)
             errs = []
+            share_bufs = [_make_share_buffers(assign[j], layers, parts[j], config) for j in range(k)]
+            import torch
+            torch.cuda.synchronize()
 
             def worker(j):
                 try:
-                    results[j] = _tune_share(assign[j], layers, parts[j], trials, config, seed)
+                    results[j] = _tune_share(assign[j], layers, parts[j], trials, config, seed, share_bufs[j])
                 except Exception as e:   # surfaced below
                     errs.append(repr(e))
 
