@@ -168,19 +168,30 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       // Expand into the swizzled im2col tile b (after the MMAs of tile i-2 released it).
       mbar_wait(a_empty + b, ((uint32_t)(i >> 1) & 1u) ^ 1u);
       uint8_t* at = a_s + (size_t)b * NSUB * A_SUB;
+      // Chunk columns past K_g are all padding: when the count of real chunk
+      // columns divides 96 they are zeroed on the first use of each of the two
+      // tile buffers and skipped afterwards.  Thread pt owns chunk column
+      // pt % CHn for rows pt / CHn + j (96 / CHn); its 8 k-table entries stay in
+      // registers (CH = KP / 8 in {8, 16, 24, 32} divides 96).
       const int mstep = a.sw * C;
-      for (int idx = pt; idx < BM * CH; idx += kProd) {
-        const int m = idx % BM, ch = idx / BM, k0 = ch * 8;
+      const int CHv = (a.Kg + 7) >> 3;
+      const int CHn = (i >= 2 && kProd % CHv == 0) ? CHv : CH;
+      const int myc = pt % CHn, rstep = kProd / CHn, k0 = myc * 8;
+      int o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = ktab[k0 + j];
+      uint8_t* colb = at + (size_t)(k0 >> 6) * A_SUB;
+      const uint32_t cpos = (uint32_t)((k0 & 63) >> 3);
+      for (int m = pt / CHn; m < BM; m += rstep) {
         const int mo = m * mstep;
         uint32_t v[4];
 #pragma unroll
         for (int j = 0; j < 8; j += 2) {
-          const int o0 = ktab[k0 + j], o1 = ktab[k0 + j + 1];
-          const uint32_t lo = o0 >= 0 ? patch[o0 + mo] : 0u, hi = o1 >= 0 ? patch[o1 + mo] : 0u;
+          const uint32_t lo = o[j] >= 0 ? patch[o[j] + mo] : 0u, hi = o[j + 1] >= 0 ? patch[o[j + 1] + mo] : 0u;
           v[j / 2] = lo | (hi << 16);
         }
-        const uint32_t off = (uint32_t)m * 128 + ((uint32_t)(((k0 & 63) >> 3) ^ (m & 7)) << 4);
-        *reinterpret_cast<uint4*>(at + (size_t)(k0 >> 6) * A_SUB + off) = make_uint4(v[0], v[1], v[2], v[3]);
+        const uint32_t off = (uint32_t)m * 128 + ((cpos ^ (uint32_t)(m & 7)) << 4);
+        *reinterpret_cast<uint4*>(colb + off) = make_uint4(v[0], v[1], v[2], v[3]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();

@@ -1093,9 +1093,10 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   const size_t patch = 2 * (size_t)a.pbuf;
   a.patch_off = (int)((size_t)pb.bn * kp * 2 + 2 * (size_t)pb.bm * kp * 2);
   a.tab_off = a.patch_off + (int)patch;
-  // Output staging for the TMA-store epilogue (reserved at fp32 size: the space's budget).
+  // Output staging for the TMA-store epilogue (the space budgets it at fp32
+  // size; a bf16 output allocates half, which can fit one more CTA per SM).
   a.recv_off = (a.tab_off + kp * 4 + 1023) / 1024 * 1024;
-  a.bar_off = a.recv_off + pb.bm * pb.bn * 4;
+  a.bar_off = a.recv_off + pb.bm * pb.bn * (pb.out_f32 ? 4 : 2);
   {
     static const bool no_ytma = getenv("TP_NO_YTMA") && atoi(getenv("TP_NO_YTMA")) != 0;
     const int eb = pb.out_f32 ? 4 : 2;
