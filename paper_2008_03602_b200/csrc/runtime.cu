@@ -852,6 +852,9 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     std::vector<int> free_slots;
     for (int i = kWindow - 1; i >= 0; --i) free_slots.push_back(i);
     std::vector<int32_t> inflight;   // candidate indices, in enqueue order
+    std::vector<cudaGraphExec_t> slot_exec(kWindow, nullptr);   // executable graph per window slot
+    std::vector<int> slot_nodes(kWindow, 0);
+    const bool graph_update = !(getenv("TP_GRAPH_UPDATE") && atoi(getenv("TP_GRAPH_UPDATE")) == 0);
     auto harvest = [&](int32_t i) -> tp_status {
       Cand& c = cs[i];
       cudaEvent_t* ev = pb.ev.data() + (size_t)c.slot * 2 * groups;
@@ -862,8 +865,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         e = cudaEventElapsedTime(&ms, ev[2 * g], ev[2 * g + 1]);
         per.push_back(ms * 1000.0 / c.n);
       }
-      if (c.exec) cudaGraphExecDestroy(c.exec);
-      c.exec = nullptr;
+      c.exec = nullptr;   // the window slot keeps the executable graph for reuse
       free_slots.push_back(c.slot);
       if (e != cudaSuccess) {
         c.m.status = TP_ECUDA;
@@ -921,7 +923,31 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
           e = ce != cudaSuccess ? ce : ee;
         }
         const auto te2 = std::chrono::steady_clock::now();
-        if (e == cudaSuccess) e = cudaGraphInstantiate(&c.exec, graph, 0);
+        if (e == cudaSuccess) {
+          // Reuse the slot's executable graph when the new capture has the same
+          // topology (n kernel nodes in a chain): cudaGraphExecUpdate rewrites
+          // the node parameters (function, grid, attributes) in place, far
+          // cheaper than instantiating; any mismatch falls back to instantiate.
+          cudaGraphExec_t& se = slot_exec[c.slot];
+          const int nodes = c.n * c.plan.kernels_per_call;
+          bool updated = false;
+          if (se && slot_nodes[c.slot] == nodes && graph_update) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(se, graph, &info) == cudaSuccess) {
+              updated = true;
+            } else {
+              cudaGetLastError();
+            }
+          }
+          if (!updated) {
+            if (se) cudaGraphExecDestroy(se);
+            se = nullptr;
+            e = cudaGraphInstantiate(&se, graph, 0);
+            slot_nodes[c.slot] = e == cudaSuccess ? nodes : 0;
+            if (e != cudaSuccess) se = nullptr;
+          }
+          c.exec = se;
+        }
         if (graph) cudaGraphDestroy(graph);
         if (prof) {
           host_warm_us += std::chrono::duration<double, std::micro>(te1 - te0).count();
@@ -945,7 +971,9 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       if (e != cudaSuccess) {
         c.m.status = TP_ECUDA;
         set_error(std::string("timing enqueue: ") + cudaGetErrorString(e));
-        if (c.exec) cudaGraphExecDestroy(c.exec);
+        if (slot_exec[c.slot]) cudaGraphExecDestroy(slot_exec[c.slot]);
+        slot_exec[c.slot] = nullptr;
+        slot_nodes[c.slot] = 0;
         c.exec = nullptr;
         free_slots.push_back(c.slot);
         cudaGetLastError();
@@ -970,6 +998,12 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       tp_status h = harvest(i);
       if (err == TP_OK) err = h;
     }
+    const auto tD = std::chrono::steady_clock::now();
+    for (cudaGraphExec_t ex : slot_exec)
+      if (ex) cudaGraphExecDestroy(ex);
+    if (prof)
+      fprintf(stderr, "[tp] slot graph destroy %.0f us\n",
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tD).count());
     const auto tC = std::chrono::steady_clock::now();
     if (prof) {
       auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
@@ -983,6 +1017,8 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     }
     // C12b: a raced candidate that beat every fully-timed one is re-timed with
     // the full protocol, so the winner's record is always a full measurement.
+    const auto tR = std::chrono::steady_clock::now();
+    int n_retimed = 0;
     if (err == TP_OK && groups > 1) {
       double best_full = 1e30;
       for (int32_t i = 0; i < n_cand; ++i)
@@ -994,6 +1030,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         if (!c.live || c.m.status != TP_OK || c.groups == groups || !(c.m.median_us < best_full)) continue;
         tp_measurement m = c.m;
         err = time_plan(part, c.plan, tm, pr, &m);
+        ++n_retimed;
         if (err == TP_OK) {
           c.m = m;
           c.groups = groups;
@@ -1001,6 +1038,9 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         }
       }
     }
+    if (prof)
+      fprintf(stderr, "[tp] C12b re-timed %d raced winners in %.0f us\n", n_retimed,
+              std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tR).count());
     if (err != TP_OK) {
       for (int32_t i = 0; i < n_cand; ++i)
         if (i < cap) records[i] = cs[i].m;

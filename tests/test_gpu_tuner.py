@@ -162,3 +162,27 @@ def test_tune_guided_measures_distinct_candidates_and_returns_argmin():
     assert all(r["status"] == 0 for r in recs)
     assert recs[sp.argmin(recs)]["space_index"] == best["space_index"] == m["space_index"]
     assert np.max(np.abs(buf.output() - ref)) / np.max(np.abs(ref)) <= 2e-2
+
+
+def test_graph_update_times_the_right_schedule(monkeypatch):
+    """The tuner reuses a window slot's executable graph through
+    cudaGraphExecUpdate (new function / grid / attributes in the same chain
+    topology).  If an update silently kept the old parameters, every candidate
+    would time the same kernel: the per-candidate medians must match those of
+    freshly instantiated graphs (TP_GRAPH_UPDATE=0) candidate by candidate."""
+    d = wl.catalog("resnet50")[16]                        # l3.b1.c2: wide spread of schedule latencies
+    x, w, b = datagen.make_inputs(d, 3)
+    buf = tp.LayerBuffers(d, x, w, b)
+    idx = list(range(0, tp.space_size(d), 7))[:96]
+    tm = tp.timing()
+    monkeypatch.setenv("TP_GRAPH_UPDATE", "1")
+    upd = tp.tune_subset(buf, None, idx, timing_cfg=tm)
+    monkeypatch.setenv("TP_GRAPH_UPDATE", "0")
+    ins = tp.tune_subset(buf, None, idx, timing_cfg=tm)
+    a = np.array([r["median_us"] for r in upd])
+    c = np.array([r["median_us"] for r in ins])
+    ok = np.array([r["status"] == 0 and q["status"] == 0 for r, q in zip(upd, ins)])
+    assert ok.all()
+    ratio = a / c
+    assert a.max() / a.min() > 2.0                         # the candidates really differ
+    assert np.median(np.abs(ratio - 1)) < 0.05 and np.abs(ratio - 1).max() < 0.35, ratio
