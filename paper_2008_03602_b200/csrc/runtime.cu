@@ -928,10 +928,14 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
           // topology (n kernel nodes in a chain): cudaGraphExecUpdate rewrites
           // the node parameters (function, grid, attributes) in place, far
           // cheaper than instantiating; any mismatch falls back to instantiate.
+          // Thread-block-cluster launches are never updated (the cluster
+          // dimension is a launch attribute of the node) -- slot_nodes < 0
+          // marks a slot whose graph must not be updated either.
           cudaGraphExec_t& se = slot_exec[c.slot];
-          const int nodes = c.n * c.plan.kernels_per_call;
+          const bool clustered = c.plan.s.kind != TP_KIND_DIRECT && c.plan.tc.cluster_z > 1;
+          const int nodes = clustered ? -1 : c.n * c.plan.kernels_per_call;
           bool updated = false;
-          if (se && slot_nodes[c.slot] == nodes && graph_update) {
+          if (se && nodes > 0 && slot_nodes[c.slot] == nodes && graph_update) {
             cudaGraphExecUpdateResultInfo info;
             if (cudaGraphExecUpdate(se, graph, &info) == cudaSuccess) {
               updated = true;

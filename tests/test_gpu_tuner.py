@@ -170,7 +170,7 @@ def test_graph_update_times_the_right_schedule(monkeypatch):
     topology).  If an update silently kept the old parameters, every candidate
     would time the same kernel: the per-candidate medians must match those of
     freshly instantiated graphs (TP_GRAPH_UPDATE=0) candidate by candidate."""
-    d = wl.catalog("resnet50")[16]                        # l3.b1.c2: wide spread of schedule latencies
+    d = wl.catalog("resnet50")[22]                        # l4.b1.c2: split-K clusters and plain grids
     x, w, b = datagen.make_inputs(d, 3)
     buf = tp.LayerBuffers(d, x, w, b)
     idx = list(range(0, tp.space_size(d), 7))[:96]
@@ -185,4 +185,8 @@ def test_graph_update_times_the_right_schedule(monkeypatch):
     assert ok.all()
     ratio = a / c
     assert a.max() / a.min() > 2.0                         # the candidates really differ
-    assert np.median(np.abs(ratio - 1)) < 0.05 and np.abs(ratio - 1).max() < 0.35, ratio
+    dev = np.abs(ratio - 1)
+    assert np.median(dev) < 0.05 and np.percentile(dev, 95) < 0.15 and dev.max() < 0.35, ratio
+    # the winner is the same schedule or one within noise of it
+    wu, wi = int(np.argmin(a)), int(np.argmin(c))
+    assert wu == wi or abs(c[wu] / c[wi] - 1) < 0.05
