@@ -475,10 +475,15 @@ struct TunerScratch {
   double* d = nullptr;
   double* h = nullptr;
   size_t cap = 0;
+  int64_t* g_idx = nullptr;    // gate check-point indices / values (reused: cudaMalloc and
+  double* g_vals = nullptr;    // cudaFree per call cost up to 100s of ms on some hosts)
+  size_t g_cap = 0;
   EventPool pa, pb;
   ~TunerScratch() {
     if (d) cudaFree(d);
     if (h) cudaFreeHost(h);
+    if (g_idx) cudaFree(g_idx);
+    if (g_vals) cudaFree(g_vals);
   }
 };
 static void delete_scratch(void* s) { delete static_cast<TunerScratch*>(s); }
@@ -611,15 +616,16 @@ struct Gate {
   double tol = 0;
   int64_t* d_idx = nullptr;
   double* d_vals = nullptr;
+  bool owned = true;   // false: the buffers belong to the partition's TunerScratch
   std::vector<double> vals;
   ~Gate() {
-    if (d_idx) cudaFree(d_idx);
-    if (d_vals) cudaFree(d_vals);
+    if (owned && d_idx) cudaFree(d_idx);
+    if (owned && d_vals) cudaFree(d_vals);
   }
 };
 
 static tp_status gate_setup(const Layer& L, const int64_t* check_idx, const double* check_ref, int32_t n_check,
-                            double tol, Gate* g) {
+                            double tol, Gate* g, TunerScratch* sc = nullptr) {
   const int64_t total = L.M * L.d.k;
   if (n_check > 0) {
     g->idx.assign(check_idx, check_idx + n_check);
@@ -634,8 +640,22 @@ static tp_status gate_setup(const Layer& L, const int64_t* check_idx, const doub
   }
   g->tol = tol > 0 ? tol : (L.d.dtype == TP_DTYPE_BF16 || L.d.out_dtype == TP_DTYPE_BF16 ? 2e-2 : 1e-5);
   g->vals.resize(g->idx.size());
-  TP_CK(cudaMalloc(&g->d_idx, g->idx.size() * sizeof(int64_t)));
-  TP_CK(cudaMalloc(&g->d_vals, g->idx.size() * sizeof(double)));
+  if (sc) {
+    if (sc->g_cap < g->idx.size()) {
+      if (sc->g_idx) cudaFree(sc->g_idx);
+      if (sc->g_vals) cudaFree(sc->g_vals);
+      sc->g_idx = nullptr; sc->g_vals = nullptr; sc->g_cap = 0;
+      TP_CK(cudaMalloc(&sc->g_idx, g->idx.size() * sizeof(int64_t)));
+      TP_CK(cudaMalloc(&sc->g_vals, g->idx.size() * sizeof(double)));
+      sc->g_cap = g->idx.size();
+    }
+    g->d_idx = sc->g_idx;
+    g->d_vals = sc->g_vals;
+    g->owned = false;
+  } else {
+    TP_CK(cudaMalloc(&g->d_idx, g->idx.size() * sizeof(int64_t)));
+    TP_CK(cudaMalloc(&g->d_vals, g->idx.size() * sizeof(double)));
+  }
   TP_CK(cudaMemcpy(g->d_idx, g->idx.data(), g->idx.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   return TP_OK;
 }
@@ -688,6 +708,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
                                     size_t ws_bytes, Gate* gate, const tp_timing& tm, tp_measurement* records,
                                     int32_t cap, int32_t* n_records) {
   cudaStream_t st = part->stream;
+  const auto t_entry = std::chrono::steady_clock::now();
   const std::vector<tp_schedule> table = space_table(L);
   const int groups = std::max(1, tm.groups);
   const int ncheck = (int)gate->idx.size();
@@ -730,6 +751,9 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
     // Host-side phase timing (TP_PROFILE=1 prints one line per call to stderr).
     static const bool prof = getenv("TP_PROFILE") && atoi(getenv("TP_PROFILE")) != 0;
     const auto tA = std::chrono::steady_clock::now();
+    if (prof)
+      fprintf(stderr, "[tp] measure setup (space table, candidates) %.0f us\n",
+              std::chrono::duration<double, std::micro>(tA - t_entry).count());
     double host_a_plan_us = 0, host_a_sync_us = 0, host_a_us = 0;
     double host_b_us = 0;   // time spent in make/capture/instantiate/enqueue (excl. harvest waits)
     double host_warm_us = 0, host_cap_us = 0, host_inst_us = 0;
@@ -1381,6 +1405,16 @@ tp_status tp_tune_subset(const tp_conv_desc* d, tp_partition* part, const int64_
                          const void* x, const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
                          const int64_t* check_idx, const double* check_ref, int32_t n_check, double tol,
                          const tp_timing* timing, tp_measurement* records, int32_t cap, int32_t* n_records) {
+  static const bool prof = getenv("TP_PROFILE") && atoi(getenv("TP_PROFILE")) != 0;
+  struct CallTimer {
+    bool on;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~CallTimer() {
+      if (on)
+        fprintf(stderr, "[tp] tp_tune_subset total %.0f us\n",
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } call_timer{prof};
   Layer L;
   tp_status st = make_layer(d, &L);
   if (st != TP_OK) return st;
@@ -1393,12 +1427,25 @@ tp_status tp_tune_subset(const tp_conv_desc* d, tp_partition* part, const int64_
   if (st != TP_OK) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   TP_CK(cudaSetDevice(p->device));
-  Gate gate;
-  st = gate_setup(L, check_idx, check_ref, n_check, tol, &gate);
-  if (st != TP_OK) return st;
-  CtxGuard g(p);
-  const tp_timing tm = timing ? *timing : default_timing();
-  return measure_candidates(L, p, cand, n_cand, x, w, bias, y, ws, ws_bytes, &gate, tm, records, cap, n_records);
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::micro>(b - a).count();
+  };
+  const auto t0 = now();
+  std::chrono::steady_clock::time_point t1, t2;
+  {
+    Gate gate;
+    st = gate_setup(L, check_idx, check_ref, n_check, tol, &gate, &scratch_of(p));
+    if (st != TP_OK) return st;
+    t1 = now();
+    CtxGuard g(p);
+    const tp_timing tm = timing ? *timing : default_timing();
+    st = measure_candidates(L, p, cand, n_cand, x, w, bias, y, ws, ws_bytes, &gate, tm, records, cap, n_records);
+    t2 = now();
+  }
+  if (call_timer.on)
+    fprintf(stderr, "[tp] gate_setup %.0f us, measure %.0f us, teardown %.0f us\n", us(t0, t1), us(t1, t2), us(t2, now()));
+  return st;
 }
 
 tp_status tp_tune(const tp_conv_desc* d, tp_partition* part, int32_t trials, uint64_t seed, const void* x,
