@@ -381,3 +381,32 @@ def test_tma_store_epilogue_bit_exact_small_partition(d):
         if not ok:
             bad.append((i, s["bm"], s["bn"], s["bk"], s["stages"]))
     assert not bad, f"{len(bad)} schedules differ, first: {bad[:5]}"
+
+
+@pytest.mark.parametrize("d", [mk(2, 128, 4, 57, 24, 3, 3, 1, 1, out=tp.FP32, epi=1),
+                               mk(1, 64, 6, 60, 40, 3, 3, 1, 1, epi=3),
+                               mk(1, 64, 128, 128, 128, 3, 3, 1, 1, out=tp.FP32, epi=1)],
+                         ids=lambda d: f"ytma_mt_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_o{d['out_dtype']}")
+def test_multitile_tma_store_epilogue_in_partition(d):
+    """Row-halo and multi-tile im2col kinds store y through the staged TMA
+    epilogue (3-D [N P][Q][K] map for row tiles, q >= Q clipped): every such
+    schedule in a 25% partition matches the oracle (bit-exact for integer data
+    with fp32 output, within one bf16 rounding otherwise)."""
+    part = tp.Partition.get(0.25)
+    x, w, b = datagen.make_inputs(d, 31, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b, part=part)
+    bad, n = [], 0
+    for i in range(tp.space_size(d)):
+        s = tp.space_get(d, i)
+        if s["kind"] not in (tp.KIND_IGEMM_TC_ROW, tp.KIND_IGEMM_TC_MT):
+            continue
+        n += 1
+        buf.poison()
+        tp.conv2d_run(buf, s, part)
+        part.sync()
+        y = buf.output()
+        ok = np.array_equal(y, ref) if d["out_dtype"] == tp.FP32 else rel_err(y, ref) <= 2 ** -8
+        if not ok:
+            bad.append((i, s["kind"], s["bm"], s["bn"], s["stages"], s["tiles_per_cta"]))
+    assert n > 0 and not bad, f"{len(bad)}/{n} schedules differ, first: {bad[:5]}"
