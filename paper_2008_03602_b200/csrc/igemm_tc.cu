@@ -1039,7 +1039,8 @@ static tp_status tf32_prepare(const TcProblem& pb, bool a_tiled, TcPlan* plan) {
   a.H = pb.H; a.W = pb.W; a.C = pb.C; a.Kg = pb.R * pb.S * pb.C;
   a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
   a.a_tiled = a_tiled ? 1 : 0;
-  a.dbg = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
+  static const int dbg_env = getenv("TP_DEBUG_TC") ? atoi(getenv("TP_DEBUG_TC")) : 0;
+  a.dbg = dbg_env;   // experiments only (bit2: no hi/lo split work, bit3: 1xTF32)
   // [hi rings][lo rings][split-K receive buffer BM x (BN + 4) fp32][barriers]; all 1 KiB multiples.
   a.recv_off = (int)((size_t)pb.stages * (pb.bm + pb.bn) * 256);
   a.bar_off = a.recv_off + (a.split_k > 1 ? pb.bm * (pb.bn + 4) * 4 : 0);
