@@ -122,9 +122,9 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     p_kb += step;
   };
   // parts: bit0 A (im2col) boxes, bit1 B (weight) boxes, bit2 the stage's expect_tx.
-  // Two producer warps (0 and 3) take alternate k-blocks (step 2): a TMA issue
-  // costs ~90 cycles of the issuing thread (measured, tools/micro/tma_issue.cu)
-  // and independent threads issue in parallel.
+  // The producer warps (up to four, see is_prod below) take k-blocks round
+  // robin (step = nprod): a TMA issue costs ~90 cycles of the issuing thread
+  // (measured, tools/micro/tma_issue.cu) and independent threads issue in parallel.
   auto produce = [&](uint32_t lead, int parts, int step) {
     uint8_t* sa = a_tiles + (size_t)p_stage * A_STAGE;
     uint8_t* sbp = b_tiles + (size_t)p_stage * B_STAGE;
