@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   const int KP = a.bk, NSUB = KP >> 6, CH = KP >> 3;        // 16-byte chunks per row
   uint8_t* b_s = smem_raw;
   uint8_t* a_s = smem_raw + (size_t)NSUB * B_SUB;
-  uint16_t* patch0 = reinterpret_cast<uint16_t*>(smem_raw + a.patch_off);   // two buffers of a.pbuf bytes
+  uint16_t* patch0 = reinterpret_cast<uint16_t*>(smem_raw + a.patch_off);   // pdist + 1 buffers of a.pbuf bytes
   int* ktab = reinterpret_cast<int*>(smem_raw + a.tab_off);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + a.bar_off);
   uint64_t* b_full = bars;        // weights staged (3 producer warps)
@@ -56,8 +56,9 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   uint64_t* t_empty = bars + 7;   // [2] accumulator drained (4 epilogue warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
 
-  const int tile0 = blockIdx.x * a.tpc;
-  const int ntl = a.ntiles - tile0 < a.tpc ? a.ntiles - tile0 : a.tpc;
+  int tile0, ntl;
+  tile_span(a.ntiles, a.tpc, a.slots, tile0, ntl);
+  if (ntl <= 0) return;   // past the resident slots (whole CTA, before any barrier)
   const int nbase = blockIdx.y * BN;
   // Patch row r of a tile holds input elements e0 - sh1 .. e0 - sh1 + prow - 1 of
   // input row h0 + r (e0 = (q0 s_w - p_w) C; sh1 = (p_w C) & 1 makes the row
@@ -153,17 +154,22 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if (ntl > 0) stage_patch(tile0, 0);
+    // Patches run a.pdist tiles ahead through pdist + 1 buffers (one cp.async
+    // group per tile, empty past the last tile, so that "wait until pdist
+    // groups are pending" always means "tile i's patch has landed").
+    const int PD = a.pdist;
+    for (int j = 0; j < PD; ++j) {
+      if (j < ntl) stage_patch(tile0 + j, j);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     for (int i = 0; i < ntl; ++i) {
       const int b = i & 1;
-      const uint16_t* patch =
-          reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(patch0) + (size_t)b * a.pbuf);
-      if (i + 1 < ntl) {
-        stage_patch(tile0 + i + 1, b ^ 1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-      }
+      const uint16_t* patch = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(patch0) +
+                                                                (size_t)(i % (PD + 1)) * a.pbuf);
+      if (i + PD < ntl) stage_patch(tile0 + i + PD, (i + PD) % (PD + 1));
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      if (PD == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+      else asm volatile("cp.async.wait_group 1;" ::: "memory");
       asm volatile("bar.sync 1, 96;" ::: "memory");
       // Expand into the swizzled im2col tile b (after the MMAs of tile i-2 released it).
       mbar_wait(a_empty + b, ((uint32_t)(i >> 1) & 1u) ^ 1u);
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full + b);
-      asm volatile("bar.sync 1, 96;" ::: "memory");   // buffer b is refilled for tile i + 2
+      asm volatile("bar.sync 1, 96;" ::: "memory");   // tile i's patch buffer is refilled next iteration
     }
   } else if (warp == 3) {
     // ---------------- MMA issuer ----------------

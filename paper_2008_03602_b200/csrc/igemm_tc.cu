@@ -634,8 +634,9 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
 
   const int tpc = a.tpc;
   const bool split_roles = tpc > 1;     // warps 2..7 drain while warps 0/1 run ahead
-  const int tile0 = blockIdx.x * tpc;
-  const int ntl = a.ntiles - tile0 < tpc ? a.ntiles - tile0 : tpc;
+  int tile0, ntl;
+  tile_span(a.ntiles, tpc, a.slots, tile0, ntl);
+  if (ntl <= 0) return;                 // past the resident slots (whole CTA, before any barrier)
   const int nbase = blockIdx.y * BN;
   const int kpt = a.kblocks;            // k-blocks per tile = (C / 64) * 3
   const uint32_t ncols = (uint32_t)(split_roles ? 2 * BN : BN) <= 32 ? 32u : (uint32_t)(split_roles ? 2 * BN : BN);
@@ -1091,13 +1092,19 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   a.prow = (a.pcols * pb.C + 3) & ~1;   // even pitch >= pcols C + 1 (row shifted by (pw C) & 1)
   a.pbuf = (int)(((size_t)pb.R * a.prow * 2 + 1023) / 1024 * 1024);
   a.pc_async = ((pb.W * pb.C) % 2 == 0) ? 1 : 0;   // cp.async 4-byte words need even rows
-  const size_t patch = 2 * (size_t)a.pbuf;
   a.patch_off = (int)((size_t)pb.bn * kp * 2 + 2 * (size_t)pb.bm * kp * 2);
-  a.tab_off = a.patch_off + (int)patch;
   // Output staging for the TMA-store epilogue (the space budgets it at fp32
-  // size; a bf16 output allocates half, which can fit one more CTA per SM).
+  // size and two patch buffers; a bf16 output allocates half, which can fit
+  // one more CTA per SM, or a third patch buffer: patches run two tiles ahead).
+  static const int pdist_env = getenv("TP_STEM_PDIST") ? atoi(getenv("TP_STEM_PDIST")) : 2;
+  const size_t budget = (size_t)a.patch_off + 2 * (size_t)a.pbuf + (size_t)(kp * 4 + 1023) / 1024 * 1024 +
+                        (size_t)pb.bm * pb.bn * 4;
+  const size_t stg = (size_t)pb.bm * pb.bn * (pb.out_f32 ? 4 : 2);
+  a.pdist = (pdist_env >= 2 && (size_t)a.patch_off + 3 * (size_t)a.pbuf + (size_t)(kp * 4 + 1023) / 1024 * 1024 +
+                                       stg <= budget) ? 2 : 1;
+  a.tab_off = a.patch_off + (int)((size_t)(a.pdist + 1) * a.pbuf);
   a.recv_off = (a.tab_off + kp * 4 + 1023) / 1024 * 1024;
-  a.bar_off = a.recv_off + pb.bm * pb.bn * (pb.out_f32 ? 4 : 2);
+  a.bar_off = a.recv_off + (int)stg;
   {
     static const bool no_ytma = getenv("TP_NO_YTMA") && atoi(getenv("TP_NO_YTMA")) != 0;
     const int eb = pb.out_f32 ? 4 : 2;

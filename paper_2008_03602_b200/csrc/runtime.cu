@@ -154,8 +154,28 @@ int cached_occupancy(const void* fn, int block, size_t smem) {
     auto it = g_occ.find(key);
     if (it != g_occ.end()) return it->second;
   }
+  // Resident CTAs per SM from the resource counts (B200: 228 KiB shared memory
+  // per SM with 1 KiB reserved per CTA, 2048 threads, 64K registers); the
+  // occupancy calculator reported 1 for every multi-tile schedule inside green
+  // contexts while ncu showed ~2.8 resident stem CTAs, so the larger is kept.
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem) != cudaSuccess) n = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem) != cudaSuccess) {
+    n = 0;
+    cudaGetLastError();
+  }
+  {
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) {
+      const size_t per_cta = smem + fa.sharedSizeBytes + 1024;
+      const int by_smem = (int)(233472 / per_cta);
+      const int by_thr = 2048 / std::max(1, block);
+      const int regs = (std::max(1, fa.numRegs) + 7) / 8 * 8;
+      const int by_reg = 65536 / (regs * 32 * ((block + 31) / 32));
+      n = std::max(n, std::min(std::min(by_smem, by_thr), std::min(by_reg, 32)));
+    } else {
+      cudaGetLastError();
+    }
+  }
   n = std::max(1, n);
   std::lock_guard<std::mutex> lk(g_cache_mu);
   g_occ[key] = n;
@@ -408,6 +428,25 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     tp_status st = tc_prepare(pb, &plan->tc);
     if (st != TP_OK) return st;
     plan->ctas_per_sm = tc_occupancy(plan->tc);
+    // Multi-tile kinds: when the frozen grid has more CTA columns than the
+    // tuned partition holds at once, the resident CTAs take balanced tile spans
+    // instead of leaving a partial last wave (the SMs are those of the tuning
+    // partition once frozen, sm_tuned -- reading C15 -- else this partition's).
+    {
+      static const bool no_slots = getenv("TP_NO_SLOTS") && atoi(getenv("TP_NO_SLOTS")) != 0;
+      const bool multi = s.kind == TP_KIND_IGEMM_TC_ROW || s.kind == TP_KIND_IGEMM_TC_MT ||
+                         s.kind == TP_KIND_IGEMM_TC_STEM;
+      const int sms = s.sm_tuned > 0 ? s.sm_tuned : sm_count;
+      // Resident CTAs per SM: the occupancy calculator, capped by TMEM (512
+      // columns per SM; these kinds allocate two BN-column accumulators) -- a
+      // CTA past that cap would wait in tcgen05.alloc for a whole span to end.
+      const int tmem_ctas = 512 / std::max(32, 2 * s.bn);
+      const int per_sm = std::max(1, std::min(plan->ctas_per_sm, tmem_ctas));
+      const int64_t cols = (int64_t)sms * per_sm / std::max(1u, plan->tc.grid.y);
+      plan->tc.args.slots = 0;
+      if (!no_slots && multi && plan->tc.args.tpc > 1 && cols >= 1 && cols < (int64_t)plan->tc.grid.x)
+        plan->tc.args.slots = (int)cols;
+    }
     const int64_t ctas = (int64_t)plan->tc.grid.x * plan->tc.grid.y * plan->tc.grid.z;
     if (plan->tc.args.y_tma && ctas <= (int64_t)sm_count &&
         (s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER))   // one tile per CTA

@@ -236,4 +236,21 @@ static __device__ __forceinline__ void store16(void* y, int64_t m, int K, int n0
 }
 
 
+// Tiles of one CTA in the multi-tile kinds.  Default: `tpc` consecutive tiles
+// from blockIdx.x * tpc.  With slots > 0 (fewer resident CTA columns than
+// grid.x, see TcArgs::slots) CTA x < slots takes the balanced span
+// [x ntiles / slots, (x + 1) ntiles / slots) and the rest get none, so the
+// last wave is not a partial one (the grid itself stays the frozen geometry).
+static __device__ __forceinline__ void tile_span(int ntiles, int tpc, int slots, int& tile0, int& ntl) {
+  const int x = (int)blockIdx.x;
+  if (slots > 0) {
+    if (x >= slots) { tile0 = ntiles; ntl = 0; return; }
+    tile0 = (int)((int64_t)x * ntiles / slots);
+    ntl = (int)((int64_t)(x + 1) * ntiles / slots) - tile0;
+    return;
+  }
+  tile0 = x * tpc;
+  ntl = ntiles - tile0 < tpc ? ntiles - tile0 : tpc;
+}
+
 }  // namespace tp

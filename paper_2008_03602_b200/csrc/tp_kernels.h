@@ -69,6 +69,9 @@ struct TcArgs {
   int tab_off;                 // gathered kind: byte offset of the pixel / k tables
   int nqb;                     // row-halo kind: q-blocks per output row, ceil(Q / BM)
   int ntiles, tpc;             // row-halo kind: N*P*nqb tiles, consecutive tiles per CTA
+  int slots;                   // multi-tile kinds: > 0 = resident CTA columns of the tuned partition
+                               //   (SMs x CTAs/SM / grid.y) when fewer than grid.x; the first `slots`
+                               //   CTAs split the tiles into balanced spans, the rest exit (tile_span)
   int cluster_red;             // 1: split-K reduced through DSMEM in a (1,1,split_k) cluster
   int bar_off;                 // byte offset of the mbarriers in dynamic shared memory
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
@@ -78,6 +81,7 @@ struct TcArgs {
   int y_tma;                   // igemm_tc split 1: epilogue staged in the ring smem, TMA 2-D store of y
   int R, pcols, patch_off;     // stem kind: filter rows, patch pixels per row, patch offset in smem
   int prow, pbuf, pc_async;    // stem kind: patch row pitch (elements), bytes per patch buffer, cp.async path
+  int pdist;                   // stem kind: patch prefetch distance in tiles (1 or 2; pdist + 1 buffers)
   int w_early;                 // 1: weight (B) boxes of the first ring pass are issued before
                                //    griddepcontrol.wait -- only when the preceding kernel in the
                                //    stream is a launch of this plan (weights are layer constants)

@@ -288,6 +288,7 @@ class Partition:
     def probe_smids(self, ctas: int) -> np.ndarray:
         import torch
         buf = torch.full((ctas,), -1, dtype=torch.int32, device=f"cuda:{self.device}")
+        torch.cuda.synchronize(self.device)   # the fill runs on torch's stream, the probe on the partition's
         _ck(_lib.tp_partition_probe(self.handle, ctas, buf.data_ptr()), "tp_partition_probe")
         return buf.cpu().numpy()
 

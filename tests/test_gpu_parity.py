@@ -410,3 +410,33 @@ def test_multitile_tma_store_epilogue_in_partition(d):
         if not ok:
             bad.append((i, s["kind"], s["bm"], s["bn"], s["stages"], s["tiles_per_cta"]))
     assert n > 0 and not bad, f"{len(bad)}/{n} schedules differ, first: {bad[:5]}"
+
+
+@pytest.mark.parametrize("d", [mk(2, 128, 4, 57, 24, 3, 3, 1, 1, out=tp.FP32, epi=1),
+                               mk(1, 64, 6, 60, 40, 3, 3, 1, 1, out=tp.FP32, epi=1),
+                               STEM_TINY[0], STEM_TINY[1]],
+                         ids=lambda d: f"slots_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_r{d['r']}")
+@pytest.mark.parametrize("sm_tuned", [1, 3, 7])
+def test_multitile_balanced_spans_bit_exact(d, sm_tuned):
+    """Multi-tile kinds (row-halo, multi-tile im2col, stem): when the frozen
+    grid has more CTA columns than the tuned partition holds (sm_tuned x
+    CTAs/SM / grid.y), the resident CTAs take balanced tile spans of uneven
+    length and the rest exit (TcArgs::slots).  Every such schedule, frozen at
+    a few SMs so that the spans are ragged, must match the oracle bit-exactly."""
+    x, w, b = datagen.make_inputs(d, 37, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    bad, n = [], 0
+    for i in range(tp.space_size(d)):
+        s = tp.space_get(d, i)
+        if s["kind"] not in (tp.KIND_IGEMM_TC_ROW, tp.KIND_IGEMM_TC_MT, tp.KIND_IGEMM_TC_STEM) or \
+                s["tiles_per_cta"] < 2:
+            continue
+        s = dict(s, sm_tuned=sm_tuned)
+        n += 1
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        if not np.array_equal(buf.output(), ref):
+            bad.append((i, s["kind"], s["bm"], s["bn"], s["tiles_per_cta"]))
+    assert n > 0 and not bad, f"{len(bad)}/{n} schedules differ, first: {bad[:5]}"
