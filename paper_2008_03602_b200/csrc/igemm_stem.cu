@@ -61,9 +61,9 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   if (ntl <= 0) return;   // past the resident slots (whole CTA, before any barrier)
   const int nbase = blockIdx.y * BN;
   // Patch row r of a tile holds input elements e0 - sh1 .. e0 - sh1 + prow - 1 of
-  // input row h0 + r (e0 = (q0 s_w - p_w) C; sh1 = (p_w C) & 1 makes the row
+  // input row h0 + r (e0 = (q0 s_w - p_w) C; sh1 = a.psh = (p_w C) & 1 makes the row
   // start on a 4-byte word, since q0 s_w C is even).
-  const int C = a.C, prow = a.prow, sh1 = (a.pw * C) & 1;
+  const int C = a.C, prow = a.prow, sh1 = a.psh;   // (16-byte mode: a 16-byte boundary, psh = (-p_w C) mod 8)
 
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
@@ -137,7 +137,15 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
         const bool hv = (unsigned)h < (unsigned)a.H;
         const uint16_t* xr = ximg + (int64_t)(hv ? h : 0) * WC;
         uint16_t* pr = pbase + r * prow;
-        if (a.pc_async) {
+        if (a.pc_async == 2) {
+          for (int vi = pt; vi < (prow >> 3); vi += kProd) {
+            const int g = e0 + 8 * vi;
+            const bool ok = hv && g >= 0 && g < WC;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(pr + 8 * vi)),
+                         "l"(ok ? xr + g : xr), "r"(ok ? 16 : 0)
+                         : "memory");
+          }
+        } else if (a.pc_async) {
           for (int wi = pt; wi < nw; wi += kProd) {
             const int g = e0 + 2 * wi;
             const bool ok = hv && g >= 0 && g < WC;
@@ -235,6 +243,13 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     uint8_t* stg = smem_raw + a.recv_off;
     const uint32_t EB = a.out_f32 ? 4u : 2u;
     const uint32_t IB = BN * EB < 128u ? BN * EB : 128u;
+    // Bias of the CTA's BN columns staged once (zero past K and without a
+    // bias); ReLU as a max against 0 (or -inf without ReLU).
+    float* bias_s = reinterpret_cast<float*>(smem_raw + a.bar_off + 128);
+    for (int j = (int)threadIdx.x - 128; j < BN; j += 128)
+      bias_s[j] = (a.has_bias && nbase + j < a.K) ? __ldg(a.bias + nbase + j) : 0.0f;
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    const float lo = a.relu ? 0.0f : __int_as_float(0xff800000u);
     for (int i = 0; i < ntl; ++i) {
       const int t = tile0 + i, b = i & 1;
       const int qb = t % a.nqb, prw = t / a.nqb;
@@ -254,14 +269,10 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
         float v[16];
 #pragma unroll
         for (int g = 0; g < 16; g += 4) {
-          float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (a.has_bias && nb + g + 4 <= a.K) bv = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
+          const float4 bv = *reinterpret_cast<const float4*>(bias_s + c + g);
           const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float sv = __uint_as_float(raw[g + j]) + b4[j];
-            v[g + j] = a.relu ? fmaxf(sv, 0.0f) : sv;
-          }
+          for (int j = 0; j < 4; ++j) v[g + j] = fmaxf(__uint_as_float(raw[g + j]) + b4[j], lo);
         }
         if (a.y_tma) {
           if (row_ok) {

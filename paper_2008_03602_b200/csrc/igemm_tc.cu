@@ -1092,6 +1092,23 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   a.prow = (a.pcols * pb.C + 3) & ~1;   // even pitch >= pcols C + 1 (row shifted by (pw C) & 1)
   a.pbuf = (int)(((size_t)pb.R * a.prow * 2 + 1023) / 1024 * 1024);
   a.pc_async = ((pb.W * pb.C) % 2 == 0) ? 1 : 0;   // cp.async 4-byte words need even rows
+  a.psh = (pb.pw * pb.C) & 1;
+  {
+    // 16-byte mode: shift each patch row by psh = (-pw C) mod 8 elements so that
+    // every tile's row segment starts on a 16-byte boundary (needs BM s_w C and
+    // W C multiples of 8, so no 16-byte chunk straddles the image border), with
+    // a pitch that is a multiple of 8 -- only when the patch buffer size (and
+    // so the validated shared-memory budget) stays the same.
+    static const bool no_v16 = getenv("TP_STEM_V16") && atoi(getenv("TP_STEM_V16")) == 0;
+    const int sh8 = (8 - (pb.pw * pb.C) % 8) % 8;
+    const int prow8 = (a.pcols * pb.C + sh8 + 7) / 8 * 8;
+    const int pbuf8 = (int)(((size_t)pb.R * prow8 * 2 + 1023) / 1024 * 1024);
+    if (!no_v16 && (pb.bm * pb.sw * pb.C) % 8 == 0 && (pb.W * pb.C) % 8 == 0 && pbuf8 == a.pbuf) {
+      a.pc_async = 2;
+      a.psh = sh8;
+      a.prow = prow8;
+    }
+  }
   a.patch_off = (int)((size_t)pb.bn * kp * 2 + 2 * (size_t)pb.bm * kp * 2);
   // Output staging for the TMA-store epilogue (the space budgets it at fp32
   // size and two patch buffers; a bf16 output allocates half, which can fit
@@ -1128,7 +1145,7 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
   plan->block = dim3(256);
   plan->cluster_z = 1;
-  plan->smem = (size_t)a.bar_off + 128;
+  plan->smem = (size_t)a.bar_off + 128 + (size_t)pb.bn * 4;   // + the staged bias (inside the budget's 1 KiB)
   cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
   if (e != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));

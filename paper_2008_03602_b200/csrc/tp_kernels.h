@@ -82,6 +82,8 @@ struct TcArgs {
   int R, pcols, patch_off;     // stem kind: filter rows, patch pixels per row, patch offset in smem
   int prow, pbuf, pc_async;    // stem kind: patch row pitch (elements), bytes per patch buffer, cp.async path
   int pdist;                   // stem kind: patch prefetch distance in tiles (1 or 2; pdist + 1 buffers)
+  int psh;                     // stem kind: elements a patch row starts before its first input
+                               //   element ((pw C) & 1; (-pw C) mod 8 in the 16-byte mode pc_async = 2)
   int w_early;                 // 1: weight (B) boxes of the first ring pass are issued before
                                //    griddepcontrol.wait -- only when the preceding kernel in the
                                //    stream is a launch of this plan (weights are layer constants)

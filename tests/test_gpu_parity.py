@@ -301,7 +301,11 @@ def test_tf32x3_random_parity_fp32_bar(d):
 STEM_TINY = [mk(2, 3, 10, 70, 64, 3, 3, 1, 1, out=tp.FP32, epi=1),     # VGG conv1_1-like, 2 images, Q = 70
              mk(1, 3, 23, 140, 64, 7, 7, 2, 3, out=tp.FP32, epi=1),    # R50 conv1-like (7x7 s2 p3), Q = 70
              mk(1, 3, 9, 132, 32, 3, 3, 2, 1, out=tp.FP32, epi=1),     # MobileNetV2 conv0-like (3x3 s2)
-             mk(1, 5, 6, 80, 40, 3, 3, 1, 1, out=tp.FP32, epi=1)]      # C = 5, K = 40 (ragged N tile)
+             mk(1, 5, 6, 80, 40, 3, 3, 1, 1, out=tp.FP32, epi=1),      # C = 5, K = 40 (ragged N tile)
+             # W C % 8 = 0: the 16-byte patch staging mode (rows shifted to 16-byte boundaries)
+             mk(2, 3, 10, 72, 64, 3, 3, 1, 1, out=tp.FP32, epi=1),     # VGG conv1_1-like, Q = 72
+             mk(1, 3, 23, 136, 64, 7, 7, 2, 3, out=tp.FP32, epi=1),    # R50 conv1-like, Q = 68
+             mk(1, 3, 9, 128, 32, 3, 3, 2, 1, out=tp.FP32, epi=1)]     # MobileNetV2 conv0-like, Q = 64
 
 
 def _stem_scheds(d):
