@@ -191,19 +191,32 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       const int CHv = (a.Kg + 7) >> 3;
       const int CHn = (i >= 2 && kProd % CHv == 0) ? CHv : CH;
       const int myc = pt % CHn, rstep = kProd / CHn, k0 = myc * 8;
-      int o[8];
+      // Per k: the shared-memory address of its element for pixel 0 (padding
+      // k reads element 0 and is masked to zero), so a row costs 8 adds, 8
+      // 2-byte loads, 4 byte-permutes and 4 masks (no per-element predicates).
+      uint32_t pa[8], mk[4];
+      const uint32_t pbase_s = smem_u32(patch);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = ktab[k0 + j];
+      for (int j = 0; j < 8; ++j) {
+        const int oj = ktab[k0 + j];
+        pa[j] = pbase_s + 2u * (uint32_t)(oj >= 0 ? oj : 0);
+        if (j & 1) mk[j >> 1] |= oj >= 0 ? 0xFFFF0000u : 0u;
+        else mk[j >> 1] = oj >= 0 ? 0x0000FFFFu : 0u;
+      }
       uint8_t* colb = at + (size_t)(k0 >> 6) * A_SUB;
       const uint32_t cpos = (uint32_t)((k0 & 63) >> 3);
       for (int m = pt / CHn; m < BM; m += rstep) {
-        const int mo = m * mstep;
+        const uint32_t mo2 = 2u * (uint32_t)(m * mstep);
+        uint32_t e[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint16_t h;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(pa[j] + mo2));
+          e[j] = h;
+        }
         uint32_t v[4];
 #pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-          const uint32_t lo = o[j] >= 0 ? patch[o[j] + mo] : 0u, hi = o[j + 1] >= 0 ? patch[o[j + 1] + mo] : 0u;
-          v[j / 2] = lo | (hi << 16);
-        }
+        for (int q = 0; q < 4; ++q) v[q] = __byte_perm(e[2 * q], e[2 * q + 1], 0x5410) & mk[q];
         const uint32_t off = (uint32_t)m * 128 + ((cpos ^ (uint32_t)(m & 7)) << 4);
         *reinterpret_cast<uint4*>(colb + off) = make_uint4(v[0], v[1], v[2], v[3]);
       }
