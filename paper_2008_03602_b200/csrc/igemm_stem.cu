@@ -126,8 +126,15 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     // Stream tile t's patch into buffer pb: with cp.async (4-byte words, zero
     // fill outside the image) when the input rows are whole words, else by
     // plain loads.
-    auto stage_patch = [&](int t, int pbi) {
-      const int qb = t % a.nqb, prw = t / a.nqb, p = prw % a.P, n = prw / a.P;
+    // Tiles are staged in order tile0, tile0 + 1, ...: their (q-block, row,
+    // image) advance as a counter instead of two divisions per tile.
+    int s_qb = tile0 % a.nqb, s_p = (tile0 / a.nqb) % a.P, s_n = (tile0 / a.nqb) / a.P;
+    auto stage_patch = [&](int pbi) {
+      const int qb = s_qb, p = s_p, n = s_n;
+      if (++s_qb == a.nqb) {
+        s_qb = 0;
+        if (++s_p == a.P) { s_p = 0; ++s_n; }
+      }
       const int e0 = (qb * BM * a.sw - a.pw) * C - sh1;
       const int h0 = p * a.sh - a.ph;
       uint16_t* pbase = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(patch0) + (size_t)pbi * a.pbuf);
@@ -167,14 +174,14 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     // groups are pending" always means "tile i's patch has landed").
     const int PD = a.pdist;
     for (int j = 0; j < PD; ++j) {
-      if (j < ntl) stage_patch(tile0 + j, j);
+      if (j < ntl) stage_patch(j);
       else asm volatile("cp.async.commit_group;" ::: "memory");
     }
     for (int i = 0; i < ntl; ++i) {
       const int b = i & 1;
       const uint16_t* patch = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(patch0) +
                                                                 (size_t)(i % (PD + 1)) * a.pbuf);
-      if (i + PD < ntl) stage_patch(tile0 + i + PD, (i + PD) % (PD + 1));
+      if (i + PD < ntl) stage_patch((i + PD) % (PD + 1));
       else asm volatile("cp.async.commit_group;" ::: "memory");
       if (PD == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
       else asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -263,9 +270,11 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       bias_s[j] = (a.has_bias && nbase + j < a.K) ? __ldg(a.bias + nbase + j) : 0.0f;
     asm volatile("bar.sync 2, 128;" ::: "memory");
     const float lo = a.relu ? 0.0f : __int_as_float(0xff800000u);
+    int e_qb = tile0 % a.nqb, e_prw = tile0 / a.nqb;   // tile (q-block, output row), advanced per tile
     for (int i = 0; i < ntl; ++i) {
-      const int t = tile0 + i, b = i & 1;
-      const int qb = t % a.nqb, prw = t / a.nqb;
+      const int b = i & 1;
+      const int qb = e_qb, prw = e_prw;
+      if (++e_qb == a.nqb) { e_qb = 0; ++e_prw; }
       const int q = qb * BM + row;
       __syncwarp();
       mbar_wait(t_full + b, (uint32_t)(i >> 1) & 1u);
