@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     // Tiles are staged in order tile0, tile0 + 1, ...: their (q-block, row,
     // image) advance as a counter instead of two divisions per tile.
     int s_qb = tile0 % a.nqb, s_p = (tile0 / a.nqb) % a.P, s_n = (tile0 / a.nqb) / a.P;
+    const int v_nv = prow >> 3, v_r0 = pt / v_nv, v_vi0 = pt % v_nv, v_dr = kProd / v_nv, v_dv = kProd % v_nv;
     auto stage_patch = [&](int pbi) {
       const int qb = s_qb, p = s_p, n = s_n;
       if (++s_qb == a.nqb) {
@@ -139,20 +140,26 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       const int h0 = p * a.sh - a.ph;
       uint16_t* pbase = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(patch0) + (size_t)pbi * a.pbuf);
       const uint16_t* ximg = xg + (int64_t)n * a.H * WC;
-      for (int r = 0; r < a.R; ++r) {
+      if (a.pc_async == 2) {
+        // The R x (prow / 8) chunks of the patch as one flat range over the
+        // 96 producer threads (a row alone has fewer chunks than threads).
+        for (int r = v_r0, vi = v_vi0; r < a.R;) {
+          const int h = h0 + r, g = e0 + 8 * vi;
+          const bool ok = (unsigned)h < (unsigned)a.H && g >= 0 && g < WC;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(pbase + r * prow + 8 * vi)),
+                       "l"(ok ? ximg + (int64_t)h * WC + g : ximg), "r"(ok ? 16 : 0)
+                       : "memory");
+          vi += v_dv;
+          r += v_dr;
+          if (vi >= v_nv) { vi -= v_nv; ++r; }
+        }
+      }
+      for (int r = 0; r < a.R && a.pc_async != 2; ++r) {
         const int h = h0 + r;
         const bool hv = (unsigned)h < (unsigned)a.H;
         const uint16_t* xr = ximg + (int64_t)(hv ? h : 0) * WC;
         uint16_t* pr = pbase + r * prow;
-        if (a.pc_async == 2) {
-          for (int vi = pt; vi < (prow >> 3); vi += kProd) {
-            const int g = e0 + 8 * vi;
-            const bool ok = hv && g >= 0 && g < WC;
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(pr + 8 * vi)),
-                         "l"(ok ? xr + g : xr), "r"(ok ? 16 : 0)
-                         : "memory");
-          }
-        } else if (a.pc_async) {
+        if (a.pc_async) {
           for (int wi = pt; wi < nw; wi += kProd) {
             const int g = e0 + 2 * wi;
             const bool ok = hv && g >= 0 && g < WC;
