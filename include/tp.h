@@ -17,13 +17,15 @@
  * Conventions (all functions):
  *   - Every function returns tp_status; nothing throws or aborts across the ABI.
  *     On failure a thread-local message is available from tp_last_error().
- *   - Device pointers (x, w, bias, y, ws) are device memory of the *primary*
+ *   - Device pointers (x, w, bias, y, ws) are 16-byte aligned (tensor-core
+ *     kinds; TP_EINVAL otherwise) device memory of the *primary*
  *     context of `device` (e.g. PyTorch allocations); the caller owns them.
  *     Host arrays (records, check_*, out structs) are owned by the caller.
  *   - libtp owns green contexts, their streams and events, TMA descriptors and
  *     the kernel instantiation table; tp_shutdown() frees them.
  *   - Host-only functions (tp_space_*, tp_output_shape, tp_select_best,
- *     tp_status_str, tp_last_error) never touch the GPU and work without one.
+ *     tp_gate_points, tp_search_next, tp_status_str, tp_last_error) never
+ *     touch the GPU and work without one.
  *   - Threading: one tuner thread per partition; calls on *different*
  *     partitions may run concurrently from different host threads (a green
  *     context may be current to one thread at a time, cuda.h cuGreenCtxCreate).
@@ -195,6 +197,11 @@ tp_status tp_space_get(const tp_conv_desc* d, int64_t idx, tp_schedule* out);
  * Fisher-Yates (reading C17).  *n_out = min(trials, |space|) <= cap. */
 tp_status tp_space_sample(const tp_conv_desc* d, int32_t trials, uint64_t seed,
                           int64_t* idx_out, int32_t cap, int32_t* n_out);
+/* Check points of the consensus gate (a10, used by tp_tune* when n_check == 0):
+ * min(n, N*K*P*Q) distinct flat NKPQ logical indices, drawn uniformly without
+ * replacement (Floyd's algorithm over SplitMix64 seeded by the output size),
+ * sorted ascending.  *n_out <= cap; TP_EINVAL if cap is too small. */
+tp_status tp_gate_points(const tp_conv_desc* d, int32_t n, int64_t* idx_out, int32_t cap, int32_t* n_out);
 /* argmin over status==TP_OK records by median_us, ties -> lowest space_index
  * (reading C13).  *best = index into records, or -1 if none is OK. */
 tp_status tp_select_best(const tp_measurement* records, int32_t n, int32_t* best);
@@ -239,7 +246,7 @@ tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partit
  *   check_idx/check_ref/n_check : flat output indices (NKPQ logical) and
  *     reference values (e.g. the fp64 oracle's); a candidate fails the gate if
  *     max|y - ref| > tol * max|ref|.  n_check == 0 -> consensus gate: the first
- *     OK candidate's values at 4096 fixed points become the reference.
+ *     OK candidate's values at the 4096 tp_gate_points become the reference.
  *   tol <= 0 -> 2e-2 for bf16 inputs, 1e-5 for fp32 (north_star).
  *   records (cap records_cap) receive one tp_measurement per candidate in
  *   selection order; *n_records = number measured.
@@ -287,6 +294,29 @@ tp_status tp_tune_guided(const tp_conv_desc* d, tp_partition* part, int32_t tria
 tp_status tp_cross_eval(const tp_conv_desc* d, const tp_schedule* tuned_at_p, tp_partition* part_q,
                         const void* x, const void* w, const void* bias, void* y, void* ws,
                         size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
+
+/* ---- the same calls with GPU% given as a fraction (SURVEY 8(b) spelling) --
+ * sm_fraction in (0, 1] selects the cached partition of (device of the last
+ * tp_init, fraction, TP_PART_FINE_GRAINED) -- exactly the handle
+ * tp_partition_get returns -- and forwards to tp_conv2d_run / tp_tune /
+ * tp_cross_eval; errors as those calls plus TP_EINVAL (fraction out of range)
+ * and TP_ECAPACITY (partition cannot be granted).  tp_partition_open is
+ * tp_partition_get without the requested count; tp_partition_stream returns the
+ * partition's CUstream (wrap it with torch.cuda.ExternalStream). */
+tp_status tp_partition_open(int32_t device, double sm_fraction, int32_t flags, tp_partition** part,
+                            int32_t* sm_granted);
+tp_status tp_partition_stream(tp_partition* part, void** cu_stream);
+tp_status tp_conv2d_run_at(const tp_conv_desc* d, const tp_schedule* s, double sm_fraction,
+                           const void* x, const void* w, const void* bias, void* y,
+                           void* ws, size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
+tp_status tp_tune_at(const tp_conv_desc* d, double sm_fraction, int32_t trials, uint64_t seed,
+                     const void* x, const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
+                     const int64_t* check_idx, const double* check_ref, int32_t n_check, double tol,
+                     const tp_timing* timing, tp_schedule* best, tp_measurement* best_m,
+                     tp_measurement* records, int32_t records_cap, int32_t* n_records);
+tp_status tp_cross_eval_at(const tp_conv_desc* d, const tp_schedule* tuned_at_p, double q,
+                           const void* x, const void* w, const void* bias, void* y, void* ws,
+                           size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
 
 /* ---- operand preparation (a5; outside the timed region) ----------------
  * fp32 logical NCHW x -> layout/dtype of desc (NHWC or NCHW, bf16 RNE or fp32).

@@ -126,14 +126,23 @@ static CUcontext current_ctx() {
 // largest value requested for that function in any context: a partition that
 // needs less can never lower it under another context's cached entry.
 static std::map<const void*, size_t> g_smem_fn_max;
+// Serialises the whole read-max -> cudaFuncSetAttribute -> cache-update
+// sequence: with concurrent tuners (one host thread per green context) a
+// thread setting a smaller value after another raised it would leave the
+// other's cache entry claiming a limit the function no longer has.
+static std::mutex g_smem_set_mu;
 
 cudaError_t ensure_smem_attr(const void* fn, size_t smem) {
   const auto key = std::make_pair(fn, current_ctx());
-  size_t want;
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_smem_attr.find(key);
     if (it != g_smem_attr.end() && it->second >= smem) return cudaSuccess;
+  }
+  std::lock_guard<std::mutex> set_lk(g_smem_set_mu);
+  size_t want;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
     size_t& m = g_smem_fn_max[fn];
     m = std::max(m, smem);
     want = m;
@@ -402,8 +411,9 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     plan->kernels_per_call = 3;
   }
   if (s.kind != TP_KIND_DIRECT) {
-    if ((reinterpret_cast<uintptr_t>(xk) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(yk)) & 15) {
-      set_error("x, w, y must be 16-byte aligned for the tensor-core path");
+    if ((reinterpret_cast<uintptr_t>(xk) | reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(yk) |
+         ((L.d.epilogue & TP_EPI_BIAS) ? reinterpret_cast<uintptr_t>(bias) : 0)) & 15) {
+      set_error("x, w, y (and bias when used) must be 16-byte aligned for the tensor-core path");
       return TP_EINVAL;
     }
     TcProblem pb;
@@ -673,9 +683,7 @@ static tp_status gate_setup(const Layer& L, const int64_t* check_idx, const doub
     for (int64_t v : g->idx)
       if (v < 0 || v >= total) { set_error("check index out of range"); return TP_EINVAL; }
   } else {
-    const int64_t n = std::min<int64_t>(4096, total);
-    g->idx.resize(n);
-    for (int64_t i = 0; i < n; ++i) g->idx[i] = (i * total) / n;   // fixed, spread points
+    g->idx = gate_points(L, 4096);   // seeded uniform sample (tp_gate_points)
   }
   g->tol = tol > 0 ? tol : (L.d.dtype == TP_DTYPE_BF16 || L.d.out_dtype == TP_DTYPE_BF16 ? 2e-2 : 1e-5);
   g->vals.resize(g->idx.size());
@@ -1137,7 +1145,13 @@ using namespace tp;
 
 extern "C" {
 
-tp_status tp_init(int32_t device) { return init_device(device, nullptr); }
+static std::atomic<int32_t> g_default_device{0};   // device of the last tp_init (fraction-taking calls)
+
+tp_status tp_init(int32_t device) {
+  tp_status st = init_device(device, nullptr);
+  if (st == TP_OK) g_default_device = device;
+  return st;
+}
 
 int64_t tp_launch_count(void) { return g_launches.load(); }
 
@@ -1638,6 +1652,54 @@ tp_status tp_gather_output(const tp_conv_desc* d, tp_partition* part, const void
   TP_CK(cudaMemcpyAsync(vals, gate.d_vals, sizeof(double) * n, cudaMemcpyDeviceToHost, p->stream));
   TP_CK(cudaStreamSynchronize(p->stream));
   return TP_OK;
+}
+
+// ---- SURVEY 8(b) spelling: GPU% given as a fraction -------------------------
+// Each resolves the cached partition of (default device, fraction,
+// TP_PART_FINE_GRAINED) -- the same one tp_partition_get returns -- and
+// forwards to the partition-taking call.
+
+tp_status tp_partition_open(int32_t device, double sm_fraction, int32_t flags, tp_partition** part,
+                            int32_t* sm_granted) {
+  return tp_partition_get(device, sm_fraction, flags, part, nullptr, sm_granted);
+}
+
+tp_status tp_partition_stream(tp_partition* part, void** cu_stream) {
+  if (!cu_stream) { set_error("null argument"); return TP_EINVAL; }
+  return tp_partition_info(part, nullptr, nullptr, nullptr, cu_stream);
+}
+
+static tp_status part_at(double sm_fraction, tp_partition** p) {
+  return tp_partition_get(g_default_device.load(), sm_fraction, TP_PART_FINE_GRAINED, p, nullptr, nullptr);
+}
+
+tp_status tp_conv2d_run_at(const tp_conv_desc* d, const tp_schedule* s, double sm_fraction, const void* x,
+                           const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
+                           const tp_timing* timing, tp_measurement* out) {
+  tp_partition* p = nullptr;
+  tp_status st = part_at(sm_fraction, &p);
+  if (st != TP_OK) return st;
+  return tp_conv2d_run(d, s, p, x, w, bias, y, ws, ws_bytes, timing, out);
+}
+
+tp_status tp_tune_at(const tp_conv_desc* d, double sm_fraction, int32_t trials, uint64_t seed, const void* x,
+                     const void* w, const void* bias, void* y, void* ws, size_t ws_bytes, const int64_t* check_idx,
+                     const double* check_ref, int32_t n_check, double tol, const tp_timing* timing, tp_schedule* best,
+                     tp_measurement* best_m, tp_measurement* records, int32_t cap, int32_t* n_records) {
+  tp_partition* p = nullptr;
+  tp_status st = part_at(sm_fraction, &p);
+  if (st != TP_OK) return st;
+  return tp_tune(d, p, trials, seed, x, w, bias, y, ws, ws_bytes, check_idx, check_ref, n_check, tol, timing, best,
+                 best_m, records, cap, n_records);
+}
+
+tp_status tp_cross_eval_at(const tp_conv_desc* d, const tp_schedule* tuned_at_p, double q, const void* x,
+                           const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
+                           const tp_timing* timing, tp_measurement* out) {
+  tp_partition* p = nullptr;
+  tp_status st = part_at(q, &p);
+  if (st != TP_OK) return st;
+  return tp_cross_eval(d, tuned_at_p, p, x, w, bias, y, ws, ws_bytes, timing, out);
 }
 
 }  // extern "C"

@@ -7,6 +7,7 @@
 // "Schedule space v0"; this file and oracle/space.py implement that table
 // independently and tests/test_space.py checks them bit-exactly.
 #include <algorithm>
+#include <unordered_set>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -384,6 +385,31 @@ static uint64_t splitmix64_next(uint64_t& state) {
   return z ^ (z >> 31);
 }
 
+// Fallback check points of the consensus gate (a10, used when the caller
+// passes no oracle points): n distinct flat NKPQ indices drawn uniformly
+// without replacement (Floyd's algorithm over SplitMix64 seeded by the output
+// size), sorted.  A fixed stride i*total/n is not used: on VGG-19 b16 it is a
+// multiple of P*Q, so every point lands in output column q = 0.
+std::vector<int64_t> gate_points(const Layer& L, int64_t n) {
+  const int64_t total = L.M * L.d.k;
+  std::vector<int64_t> out;
+  if (total <= n) {
+    out.resize(total);
+    for (int64_t i = 0; i < total; ++i) out[i] = i;
+    return out;
+  }
+  uint64_t state = 0x7470676174650000ull ^ (uint64_t)total;
+  std::unordered_set<int64_t> seen;
+  seen.reserve((size_t)n * 2);
+  for (int64_t j = total - n; j < total; ++j) {
+    const int64_t t = (int64_t)(splitmix64_next(state) % (uint64_t)(j + 1));
+    seen.insert(seen.count(t) ? j : t);
+  }
+  out.assign(seen.begin(), seen.end());
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
 }  // namespace tp
 
 using namespace tp;
@@ -461,6 +487,18 @@ tp_status tp_space_sample(const tp_conv_desc* d, int32_t trials, uint64_t seed, 
   }
   for (int64_t i = 0; i < t; ++i) idx_out[i] = a[i];
   *n_out = (int32_t)t;
+  return TP_OK;
+}
+
+tp_status tp_gate_points(const tp_conv_desc* d, int32_t n, int64_t* idx_out, int32_t cap, int32_t* n_out) {
+  Layer L;
+  tp_status st = make_layer(d, &L);
+  if (st != TP_OK) return st;
+  if (n < 0 || !idx_out || !n_out) { set_error("bad gate-point arguments"); return TP_EINVAL; }
+  const std::vector<int64_t> v = gate_points(L, n);
+  if ((int64_t)v.size() > cap) { set_error("gate-point output capacity too small"); return TP_EINVAL; }
+  std::copy(v.begin(), v.end(), idx_out);
+  *n_out = (int32_t)v.size();
   return TP_OK;
 }
 

@@ -44,6 +44,7 @@ int64_t stem_patch_bytes(const Layer& L, int bm);                    // 3xTF32 t
 int64_t tf32_smem_bytes(int bm, int bn, int stages, int split);
 int64_t row_stage_bytes(int bm, int bn);                    // row-halo kind: one pipeline stage
 bool schedule_in_space(const Layer& L, const tp_schedule& s);
+std::vector<int64_t> gate_points(const Layer& L, int64_t n);   // consensus-gate fallback points (a10)
 
 constexpr int64_t kSmemLimit = 232448;  // 227 KiB per CTA
 

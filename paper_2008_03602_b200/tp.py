@@ -14,6 +14,11 @@ from dataclasses import dataclass
 
 import numpy as np
 
+# Concurrent tuners (one green-context stream each) need more
+# hardware work queues than the default 8; read when the CUDA context is
+# created, so it only takes effect if libtp is imported before CUDA starts.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtp.so")
 if not os.path.exists(LIB_PATH):
@@ -89,6 +94,13 @@ _sig("tp_space_size", _P(ConvDesc), _P(_i64))
 _sig("tp_space_get", _P(ConvDesc), _i64, _P(Schedule))
 _sig("tp_space_sample", _P(ConvDesc), _i32, _u64, _P(_i64), _i32, _P(_i32))
 _sig("tp_select_best", _P(Measurement), _i32, _P(_i32))
+_sig("tp_gate_points", _P(ConvDesc), _i32, _P(_i64), _i32, _P(_i32))
+_sig("tp_partition_open", _i32, _dbl, _i32, _P(_vp), _P(_i32))
+_sig("tp_partition_stream", _vp, _P(_vp))
+_sig("tp_conv2d_run_at", _P(ConvDesc), _P(Schedule), _dbl, _vp, _vp, _vp, _vp, _vp, _sz, _P(Timing), _P(Measurement))
+_sig("tp_tune_at", _P(ConvDesc), _dbl, _i32, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _P(_i64), _P(_dbl), _i32, _dbl,
+     _P(Timing), _P(Schedule), _P(Measurement), _P(Measurement), _i32, _P(_i32))
+_sig("tp_cross_eval_at", _P(ConvDesc), _P(Schedule), _dbl, _vp, _vp, _vp, _vp, _vp, _sz, _P(Timing), _P(Measurement))
 _sig("tp_workspace_size", _P(ConvDesc), _P(Schedule), _P(_sz))
 _sig("tp_workspace_size_max", _P(ConvDesc), _P(_sz))
 _sig("tp_conv2d_run", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(Timing), _P(Measurement))
@@ -203,6 +215,15 @@ def select_best(records: list[dict]) -> int:
     return b.value
 
 
+def gate_points(d: dict, n: int = 4096) -> np.ndarray:
+    """The consensus gate's fallback check points (flat NKPQ indices, sorted)."""
+    out = np.empty(max(1, n), dtype=np.int64)
+    m = _i32()
+    _ck(_lib.tp_gate_points(ctypes.byref(desc(d)), int(n), out.ctypes.data_as(_P(_i64)), out.shape[0],
+                            ctypes.byref(m)), "tp_gate_points")
+    return out[:m.value].copy()
+
+
 def search_next(d: dict, sm_granted: int, measured_idx, measured_us, batch: int, explore: float = 0.25,
                 seed: int = 42) -> list[int]:
     """Next batch of space indices from the model-guided search (host-only)."""
@@ -243,6 +264,14 @@ def timing(warmup=3, groups=5, n_min=10, target_group_us=20.0, use_graph=1, flus
     return Timing(warmup, groups, n_min, target_group_us, use_graph, flush_l2, prune_ratio)
 
 
+def device_sm_count(device: int = 0) -> int:
+    """SMs of the device: the granted count of its whole-device partition."""
+    rq, gr, h = _i32(), _i32(), _vp()
+    _ck(_lib.tp_partition_get(device, 1.0, 0, ctypes.byref(h), ctypes.byref(rq), ctypes.byref(gr)),
+        "tp_partition_get")
+    return gr.value
+
+
 @dataclass
 class Partition:
     handle: int
@@ -263,14 +292,16 @@ class Partition:
     def split(cls, k: int, sms_each: int, device: int = 0, flags: int = PART_FINE_GRAINED) -> list["Partition"]:
         hs, gr = (_vp * k)(), (_i32 * k)()
         _ck(_lib.tp_partition_split(device, k, sms_each, flags, hs, gr), "tp_partition_split")
-        return [cls(hs[i], device, sms_each, gr[i], sms_each / 148.0, owned=True) for i in range(k)]
+        total = device_sm_count(device)
+        return [cls(hs[i], device, sms_each, gr[i], sms_each / total, owned=True) for i in range(k)]
 
     @classmethod
     def shared(cls, k: int, device: int = 0) -> list["Partition"]:
         """k unpartitioned whole-device handles, one stream each (f3: no SM isolation)."""
         hs = (_vp * k)()
         _ck(_lib.tp_partition_shared(device, k, hs), "tp_partition_shared")
-        return [cls(hs[i], device, 148, 148, 1.0, owned=True) for i in range(k)]
+        total = device_sm_count(device)
+        return [cls(hs[i], device, total, total, 1.0, owned=True) for i in range(k)]
 
     def stream(self) -> int:
         s = _vp()
@@ -460,6 +491,43 @@ def tune_subset(buf: LayerBuffers, part: Partition | None, cand_idx, check_idx=N
                             ctypes.byref(timing_cfg) if timing_cfg is not None else None, recs, cap,
                             ctypes.byref(nrec)), "tp_tune_subset")
     return [meas_to_dict(recs[i]) for i in range(nrec.value)]
+
+
+def conv2d_run_at(buf: LayerBuffers, sched: dict, sm_fraction: float, timing_cfg: Timing | None = None) -> dict:
+    """tp_conv2d_run_at: the run call with GPU% as a fraction."""
+    x, w, b, y, ws, wsb = buf.ptrs()
+    m = Measurement()
+    _ck(_lib.tp_conv2d_run_at(ctypes.byref(buf.cd), ctypes.byref(dict_to_sched(sched)), float(sm_fraction), x, w, b,
+                              y, ws, wsb, ctypes.byref(timing_cfg or timing()), ctypes.byref(m)), "tp_conv2d_run_at")
+    return meas_to_dict(m)
+
+
+def tune_at(buf: LayerBuffers, sm_fraction: float, trials: int, seed: int, check_idx=None, check_ref=None,
+            tol: float = 0.0, timing_cfg: Timing | None = None):
+    """tp_tune_at: (best schedule, best measurement, records) at a GPU% fraction."""
+    x, w, b, y, ws, wsb = buf.ptrs()
+    cap = max(1, min(trials, space_size(buf.d)))
+    recs = (Measurement * cap)()
+    nrec = _i32()
+    best, best_m = Schedule(), Measurement()
+    ci, cr, nc = _check_arrays(check_idx, check_ref)
+    st = _lib.tp_tune_at(ctypes.byref(buf.cd), float(sm_fraction), int(trials), int(seed), x, w, b, y, ws, wsb,
+                         ci.ctypes.data_as(_P(_i64)) if nc else None, cr.ctypes.data_as(_P(_dbl)) if nc else None, nc,
+                         float(tol), ctypes.byref(timing_cfg) if timing_cfg is not None else None,
+                         ctypes.byref(best), ctypes.byref(best_m), recs, cap, ctypes.byref(nrec))
+    records = [meas_to_dict(recs[i]) for i in range(nrec.value)]
+    _ck(st, "tp_tune_at")
+    return sched_to_dict(best), meas_to_dict(best_m), records
+
+
+def cross_eval_at(buf: LayerBuffers, tuned_sched: dict, q: float, timing_cfg: Timing | None = None) -> dict:
+    """tp_cross_eval_at: schedule tuned at p (frozen geometry) run at fraction q."""
+    x, w, b, y, ws, wsb = buf.ptrs()
+    m = Measurement()
+    _ck(_lib.tp_cross_eval_at(ctypes.byref(buf.cd), ctypes.byref(dict_to_sched(tuned_sched)), float(q), x, w, b, y,
+                              ws, wsb, ctypes.byref(timing_cfg) if timing_cfg is not None else None, ctypes.byref(m)),
+        "tp_cross_eval_at")
+    return meas_to_dict(m)
 
 
 def cross_eval(buf: LayerBuffers, tuned_sched: dict, part_q: Partition | None,

@@ -28,6 +28,52 @@ def test_sample_properties():
     assert sp.sample(1000, 10, 1) != sp.sample(1000, 10, 2)
 
 
+def test_sample_hand_vector():
+    # Reading C17 worked by hand from the published SplitMix64(0) outputs above:
+    # o0 = 0xE220A8397B1DCDAF, o1 = 0x6E789E6AA1B965F4, o2 = 0x06C45D188009454F.
+    # n = 10, t = 3: o0 mod 10 = 5 -> swap a[0], a[5]; o1 mod 9 = 0 -> j = 1 (no swap);
+    # o2 mod 8 = 7 -> j = 9, swap a[2], a[9]  =>  [5, 1, 9].
+    # n = 6, t = 3: o0 mod 6 = 1 -> swap a[0], a[1]; o1 mod 5 = 0 -> j = 1; o2 mod 4 = 3 -> j = 5 => [1, 0, 5].
+    # (A swap index drawn as next() mod n would give [1, 5, 9] and [0, 2, 1].)
+    assert (0xE220A8397B1DCDAF % 10, 0x6E789E6AA1B965F4 % 9, 0x06C45D188009454F % 8) == (5, 0, 7)
+    assert sp.sample(10, 3, 0) == [5, 1, 9]
+    assert sp.sample(6, 3, 0) == [1, 0, 5]
+
+
+def test_direct_smem_depthwise_hand():
+    # Depthwise smem (reading C25): halo rows x halo cols x (lanes_k vec_k) channels +
+    # R S (lanes_k vec_k) weights, fp32 -- the CTA's channel tile, which the kernel allocates even
+    # where lanes_k vec_k exceeds C.  MobileNetV2 dw.960.7.s1 (C = K = 960, 7x7, 3x3 s1 p1):
+    # threads 64, tile_q 1, vec_k 8, tile_p 1: ceil(960/8) = 120 -> np2 128, lanes_k = min(128, 64) = 64,
+    #   lanes_q = 1; channel tile 512, halo 3 x 3: 4 (9 x 512 + 9 x 512) = 36864 B.
+    # threads 512, tile_q 4, vec_k 8, tile_p 1: lanes_k = 128, lanes_q = 4, 16 output columns -> 18 input
+    #   columns; channel tile 1024 (> C = 960): 4 (3 x 18 x 1024 + 9 x 1024) = 258048 B > 232448 -> invalid.
+    d = [x for x in wl.catalog("mobilenetv2") if x["name"] == "mb2.dw.960.7.s1"][0]
+    assert sp.direct_smem_bytes(d, 64, 1, 8, 1) == 36864
+    assert sp.direct_smem_bytes(d, 512, 4, 8, 1) == 258048
+    assert not sp._valid_direct(d, 512, 4, 8, 1, 1) and sp._valid_direct(d, 512, 4, 8, 1, 0)
+    # dense (g = 1) branch: at most 16 input channels staged.  cfg1 (C = 64, 56x56, K = 64, 3x3 s1):
+    # threads 256, tile_q 2, vec_k 4, tile_p 2: lanes_k = min(np2(16), 128) = 16, lanes_q = 256 / 32 = 8;
+    # 16 output columns -> 18 input columns, 2 output rows -> 4 input rows, channel tile 64:
+    # 4 (4 x 18 x 16 + 9 x 16 x 64) = 4 (1152 + 9216) = 41472 B.
+    assert sp.direct_smem_bytes(wl.catalog("cfg1")[0], 256, 2, 4, 2) == 41472
+
+
+def test_mobilenetv2_space_totals():
+    # Mirror totals with reading C25: direct 3628 + IGEMM_TC 6148 + gathered 48 + stem 8 = 9832;
+    # the SURVEY 8(a) a2 count (10,180, stem on the direct kind) clamps the depthwise channel tile at C
+    # and so admits 20 more direct schedules: 9776 + 384 (stem's direct space) = 10,160 here.
+    cat = wl.catalog("mobilenetv2")
+    kinds = {}
+    for d in cat:
+        for x in sp.enumerate_space(d):
+            kinds[x["kind"]] = kinds.get(x["kind"], 0) + 1
+    assert kinds == {sp.KIND_DIRECT: 3628, sp.KIND_IGEMM_TC: 6148, sp.KIND_IGEMM_TC_GATHER: 48,
+                     sp.KIND_IGEMM_TC_STEM: 8}
+    stem = [d for d in cat if sp.layer_kind(d) == sp.KIND_IGEMM_TC_GATHER]
+    assert len(stem) == 1 and kinds[sp.KIND_DIRECT] + kinds[sp.KIND_IGEMM_TC] + _direct_count(stem[0]) == 10160
+
+
 def test_argmin_tie_break():
     recs = [dict(status=0, median_us=5.0, space_index=9), dict(status=4, median_us=1.0, space_index=1),
             dict(status=0, median_us=5.0, space_index=3), dict(status=0, median_us=6.0, space_index=0)]
@@ -225,6 +271,27 @@ def test_libtp_argmin_matches_mirror():
         recs = [dict(status=int(rng.choice([0, 0, 0, 5])), median_us=float(rng.choice([1.5, 2.0, 2.5, 3.0])),
                      space_index=int(i)) for i in rng.permutation(n)]
         assert tp.select_best(recs) == sp.argmin(recs)
+
+
+@pytest.mark.parametrize("d", SHAPES, ids=[d["name"] for d in SHAPES])
+def test_gate_points_cover_the_output(d):
+    # Consensus-gate fallback points (a10): distinct, sorted, in range, and spread over
+    # pixels AND channels (a fixed stride i*total/4096 put every VGG-19 b16 point in column q = 0).
+    tp = _lib_or_skip()
+    P, Q = sp.out_pq(d)
+    total = d["n"] * d["k"] * P * Q
+    idx = tp.gate_points(d, 4096)
+    assert len(idx) == min(4096, total) and np.all(np.diff(idx) > 0) and idx[0] >= 0 and idx[-1] < total
+    assert np.array_equal(idx, tp.gate_points(d, 4096))   # deterministic
+    q = idx % Q
+    p = (idx // Q) % P
+    k = (idx // (P * Q)) % d["k"]
+    n = idx // (P * Q * d["k"])
+    pix = len(set(zip(n.tolist(), p.tolist(), q.tolist())))
+    assert len(set(q.tolist())) >= min(Q, len(idx) // 8)
+    assert len(set(p.tolist())) >= min(P, len(idx) // 8)
+    assert len(set(k.tolist())) >= min(d["k"], len(idx) // 8) * 0.9
+    assert pix >= min(d["n"] * P * Q, len(idx)) * 0.5
 
 
 def test_libtp_output_shape():
