@@ -16,9 +16,10 @@
                           partition), plus the measured launch floor.
 
 Everything here is orchestration: every step of the path runs in libtp's
-kernels.  Correctness gating uses libtp's consensus gate (the first OK
-candidate's values at 4096 fixed points); oracle parity of the winners is
-checked by tests/ and bench.py.
+kernels.  Correctness gating: pass ``checks`` -- per layer (check_idx,
+check_ref), the stored fp64 oracle points of ``refs.load`` -- and every
+candidate is gated against the oracle; without them libtp's
+consensus gate applies (the first OK candidate's values at tp_gate_points).
 """
 from __future__ import annotations
 
@@ -89,16 +90,23 @@ def make_buffers(layers: list[dict], part=None, config: int = 2, device: int = 0
     return out
 
 
-def tune_layers(layers, bufs, part, trials=1000, seed=42, timing_cfg=None) -> list[dict]:
+def _check(checks, i):
+    return (None, None) if checks is None else checks[i]
+
+
+def tune_layers(layers, bufs, part, trials=1000, seed=42, timing_cfg=None, checks=None) -> list[dict]:
     """Tune each layer inside `part`; returns per-layer dicts with the best
     schedule, its measurement and the tuning throughput."""
     res = []
-    for d, buf in zip(layers, bufs):
+    for i, (d, buf) in enumerate(zip(layers, bufs)):
         t0 = time.perf_counter()
-        best, m, recs = tp.tune(buf, part, trials, seed, timing_cfg=timing_cfg)
+        ci, cr = _check(checks, i)
+        best, m, recs = tp.tune(buf, part, trials, seed, check_idx=ci, check_ref=cr, timing_cfg=timing_cfg)
         el = time.perf_counter() - t0
         res.append({"layer": d["name"], "mult": d.get("mult", 1), "best": best, "best_m": m,
-                    "candidates": len(recs), "ok": sum(1 for r in recs if r["status"] == 0), "wall_s": el})
+                    "candidates": len(recs), "ok": sum(1 for r in recs if r["status"] == 0),
+                    "raced": sum(1 for r in recs if r["status"] == 0 and r["groups"] == 1), "wall_s": el,
+                    "oracle_gate": checks is not None})
     return res
 
 
@@ -144,8 +152,32 @@ def partition_context(part) -> dict:
             "copy_bw_gbs": bw, "floor_us": fl}
 
 
+def pd_check(per_layer: list[dict], fractions, k_cv: float = 3.0) -> dict:
+    """P-D: with exhaustive tuning the diagonal is its column's
+    minimum up to noise: M[q][q] <= M[p][q] (1 + eps), eps = k_cv x the larger
+    coefficient of variation (std / mean over the timed groups) of the two
+    cells.  Also the plain 10% rule of round 1."""
+    viol, viol10, cells = [], [], 0
+    for row in per_layer:
+        m, cv = row["matrix_us"], row["matrix_cv"]
+        for q in fractions:
+            dq = m[str(q)][str(q)]
+            for p in fractions:
+                if p == q:
+                    continue
+                cells += 1
+                eps = k_cv * max(cv[str(q)][str(q)], cv[str(p)][str(q)])
+                if dq > m[str(p)][str(q)] * (1.0 + eps):
+                    viol.append({"layer": row["layer"], "tuned_at": p, "run_at": q, "diag_us": dq,
+                                 "cell_us": m[str(p)][str(q)], "eps": eps})
+            if dq > min(m[str(p)][str(q)] for p in fractions) * 1.10:
+                viol10.append({"layer": row["layer"], "q": q})
+    return {"rule": f"M[q][q] <= M[p][q] (1 + {k_cv} CV)", "cells": cells, "violations": viol,
+            "pass": not viol, "violations_gt10pct": viol10}
+
+
 def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3, timing_cfg=None,
-               log=print) -> dict:
+               log=print, checks=None, bufs=None) -> dict:
     """a13: tune every layer at each fraction p, then run each frozen best(p)
     at every fraction q.  Returns per-layer matrices M[p][q] (median us), the
     model sums Sum_l mult_l * M_l[p][q] (reading C21), the diagonal check
@@ -153,28 +185,32 @@ def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3,
     pk = peaks()
     parts = {f: tp.Partition.get(f) for f in fractions}
     ctx = {f: partition_context(parts[f]) for f in fractions}
-    bufs = make_buffers(layers, None, config)
+    bufs = bufs if bufs is not None else make_buffers(layers, None, config)
     tuned = {}
     tune_stats = {}
     for p in fractions:
         t0 = time.perf_counter()
-        tuned[p] = tune_layers(layers, bufs, parts[p], trials, datagen.sampler_seed(fractions.index(p)), timing_cfg)
+        tuned[p] = tune_layers(layers, bufs, parts[p], trials, datagen.sampler_seed(fractions.index(p)), timing_cfg,
+                               checks)
         el = time.perf_counter() - t0
         n = sum(r["candidates"] for r in tuned[p])
         tune_stats[p] = {"candidates": n, "ok": sum(r["ok"] for r in tuned[p]), "wall_s": el,
-                         "candidates_per_s": n / el}
+                         "candidates_per_s": n / el, "raced": sum(r["raced"] for r in tuned[p]),
+                         "oracle_gate": checks is not None}
         log(f"tuned at {p}: {n} candidates in {el:.1f}s")
     per_layer = []
     model = {p: {q: 0.0 for q in fractions} for p in fractions}
     for li, d in enumerate(layers):
-        mat = {}
+        mat, cvm = {}, {}
         for p in fractions:
-            row = {}
+            row, cvr = {}, {}
             for q in fractions:
                 m = tp.cross_eval(bufs[li], tuned[p][li]["best"], parts[q], timing_cfg)
                 row[q] = m["median_us"]
+                cvr[q] = m["std_us"] / m["mean_us"] if m["mean_us"] > 0 else 0.0
                 model[p][q] += d.get("mult", 1) * m["median_us"]
             mat[p] = row
+            cvm[p] = cvr
         diag = {}
         for q in fractions:
             bm = tuned[q][li]["best_m"]
@@ -182,6 +218,7 @@ def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3,
                                bm["kind"])
         per_layer.append({"layer": d["name"], "mult": d.get("mult", 1),
                           "matrix_us": {str(p): {str(q): mat[p][q] for q in fractions} for p in fractions},
+                          "matrix_cv": {str(p): {str(q): cvm[p][q] for q in fractions} for p in fractions},
                           "best_schedule": {str(p): {k: tuned[p][li]["best"][k] for k in
                                                      ("space_index", "kind", "bm", "bn", "bk", "stages", "threads",
                                                       "split_k", "tile_q", "vec_k", "tile_p", "smem_stage", "grid_x",
@@ -201,13 +238,7 @@ def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3,
                                                                 "threads", "split_k", "tile_q", "vec_k", "tile_p",
                                                                 "smem_stage")}
     # P-D: with exhaustive tuning the diagonal is the column minimum up to noise.
-    viol = []
-    for row in per_layer:
-        for q in fractions:
-            col = [row["matrix_us"][str(p)][str(q)] for p in fractions]
-            if row["matrix_us"][str(q)][str(q)] > min(col) * 1.10:
-                viol.append({"layer": row["layer"], "q": q, "diag": row["matrix_us"][str(q)][str(q)],
-                             "col_min": min(col)})
+    pd = pd_check(per_layer, fractions)
     return {"fractions": list(fractions), "partitions": {str(f): ctx[f] for f in fractions}, "peaks": pk,
             "tune": {str(p): tune_stats[p] for p in fractions},
             "model_sum_us": {str(p): {str(q): model[p][q] for q in fractions} for p in fractions},
@@ -215,7 +246,7 @@ def cross_eval(layers, fractions=(0.10, 0.25, 0.50, 1.0), trials=1000, config=3,
             "aggregate_5k": dict(aggregate_5k({str(p): {str(q): model[p][q] for q in fractions} for p in fractions},
                                               fractions),
                                  untuned_total_ms=sum(model_default[q] for q in fractions)),
-            "diagonal_violations_gt10pct": viol, "layers": per_layer}
+            "pd_check": pd, "diagonal_violations_gt10pct": pd["violations_gt10pct"], "layers": per_layer}
 
 
 def _lpt(layers, k):
@@ -231,7 +262,7 @@ def _lpt(layers, k):
 
 
 def concurrent_tune(layers, k=4, sms_each=37, trials=1000, config=4, timing_cfg=None, flags=tp.PART_FINE_GRAINED,
-                    log=print) -> dict:
+                    log=print, checks=None) -> dict:
     """a14: k disjoint partitions of sms_each SMs (one split), one host thread
     per partition tuning its LPT share of the layers concurrently.  Then the
     winners are timed solo (one partition busy) and co-running (all k busy)."""
@@ -262,8 +293,11 @@ def concurrent_tune(layers, k=4, sms_each=37, trials=1000, config=4, timing_cfg=
             out = []
             t0 = time.perf_counter()
             for i in assign[j]:
-                best, m, recs = tp.tune(bufs[i], parts[j], trials, datagen.sampler_seed(1), timing_cfg=timing_cfg)
-                out.append({"layer": layers[i]["name"], "idx": i, "best": best, "best_m": m, "candidates": len(recs)})
+                ci, cr = _check(checks, i)
+                best, m, recs = tp.tune(bufs[i], parts[j], trials, datagen.sampler_seed(1), check_idx=ci, check_ref=cr,
+                                        timing_cfg=timing_cfg)
+                out.append({"layer": layers[i]["name"], "idx": i, "best": best, "best_m": m, "candidates": len(recs),
+                            "ok": sum(1 for r in recs if r["status"] == 0)})
             results[j] = {"wall_s": time.perf_counter() - t0, "layers": out}
         except Exception as e:   # surfaced below
             errors.append(repr(e))
@@ -301,7 +335,7 @@ def concurrent_tune(layers, k=4, sms_each=37, trials=1000, config=4, timing_cfg=
             d = layers[r["idx"]]
             layers_out.append({"layer": r["layer"], "tuner": j, "sm_granted": ctx[j]["sm_granted"],
                                "best_us": r["best_m"]["median_us"], "solo_us": solo[r["layer"]],
-                               "corun_us": co[r["layer"]], "candidates": r["candidates"],
+                               "corun_us": co[r["layer"]], "candidates": r["candidates"], "ok": r["ok"],
                                "schedule": {kk: r["best"][kk] for kk in ("space_index", "kind", "bm", "bn", "bk",
                                                                          "stages", "threads", "split_k")},
                                "roofline": roofline(d, solo[r["layer"]], ctx[j]["sm_granted"],
@@ -309,7 +343,8 @@ def concurrent_tune(layers, k=4, sms_each=37, trials=1000, config=4, timing_cfg=
                                                     r["best_m"]["kind"])})
     for p in parts:
         p.close()
-    return {"k": k, "sms_each_requested": sms_each, "sms_each_split": asked, "partitions": ctx, "peaks": pk, "wall_s": wall, "candidates": n,
+    return {"k": k, "sms_each_requested": sms_each, "sms_each_split": asked, "partitions": ctx, "peaks": pk,
+            "oracle_gate": checks is not None, "wall_s": wall, "candidates": n,
             "candidates_per_s": n / wall, "per_tuner_wall_s": [results[j]["wall_s"] for j in range(k)],
             "assignment": [[layers[i]["name"] for i in a] for a in assign], "layers": layers_out}
 

@@ -11,6 +11,10 @@ P:841).
 """
 from __future__ import annotations
 
+import glob
+import json
+import os
+
 import numpy as np
 
 # Fixed-size record exchanged between ranks (float64 row).
@@ -88,8 +92,94 @@ def finalists(records: list[dict], k: int = 3) -> dict[tuple[int, int], list[dic
     return {key: sorted(v, key=lambda r: (r["median_us"], r["space_index"]))[:k] for key, v in by.items()}
 
 
-def gpu_busy_us(records: list[dict], warmup: int = 3) -> float:
+def is_raced(r: dict, full_groups: int = 5) -> bool:
+    """Reading C12b: a raced candidate's record has a single timed group."""
+    return r["status"] == 0 and full_groups > 1 and r["groups"] == 1
+
+
+def raced_frac(records: list[dict], full_groups: int = 5) -> float:
+    ok = [r for r in records if r["status"] == 0]
+    return sum(1 for r in ok if is_raced(r, full_groups)) / max(1, len(ok))
+
+
+def gpu_busy_us(records: list[dict], warmup: int = 3, full_groups: int = 5) -> float:
     """Kernel time a tuning pass spent on the GPU for these records: per
-    candidate, the gate launch + warm-ups + groups x n timed launches, each
-    at the candidate's median latency (SURVEY 8(d) "GPU-busy fraction")."""
-    return sum((1 + warmup + r["groups"] * r["n_per_group"]) * r["median_us"] for r in records if r["status"] == 0)
+    candidate, the gate launch + its warm-ups (1 for a raced candidate, reading
+    C12b; `warmup` otherwise) + groups x n timed launches, each at the
+    candidate's median latency (SURVEY 8(d) "GPU-busy fraction")."""
+    return sum((1 + (1 if is_raced(r, full_groups) else warmup) + r["groups"] * r["n_per_group"]) * r["median_us"]
+               for r in records if r["status"] == 0)
+
+
+# ---------------------------------------------------------------------------------------------
+# Record log and resume (the orchestrator analog, PAPER.md P:921-925 [src]: a tuning job that
+# dies part-way must not redo the measurements it already made).  Every rank appends its
+# records, one JSON object per line, to <dir>/rank<r>.jsonl as each (job, layer) unit
+# finishes; a restarted job reads every rank's log, skips the (job, layer, space_index)
+# triples already measured and merges the logged records with the new ones.
+class RecordLog:
+    def __init__(self, directory: str, rank: int):
+        os.makedirs(directory, exist_ok=True)
+        self.path = os.path.join(directory, f"rank{rank}.jsonl")
+        # A rank that died mid-write leaves a torn last line: cut it, so the next
+        # append starts on a fresh line.
+        if os.path.exists(self.path):
+            with open(self.path, "rb+") as f:
+                data = f.read()
+                if data and not data.endswith(b"\n"):
+                    f.truncate(data.rfind(b"\n") + 1)
+
+    def append(self, records: list[dict], job: int, layer: int, rank: int) -> None:
+        with open(self.path, "a") as f:
+            for r in records:
+                row = {k: r[k] for k in REC_FIELDS if k in r}
+                row.update(job=job, layer=layer, rank=rank)
+                f.write(json.dumps(row) + "\n")
+            f.flush()
+            os.fsync(f.fileno())
+
+    @staticmethod
+    def load(directory: str) -> list[dict]:
+        """All complete lines of every rank's log (a torn last line is dropped)."""
+        out = []
+        for path in sorted(glob.glob(os.path.join(directory, "rank*.jsonl"))):
+            with open(path) as f:
+                for ln in f:
+                    try:
+                        row = json.loads(ln)
+                    except json.JSONDecodeError:
+                        continue
+                    if all(k in row for k in REC_FIELDS):
+                        out.append(row)
+        return out
+
+
+def measured_set(records: list[dict]) -> set[tuple[int, int, int]]:
+    return {(int(r["job"]), int(r["layer"]), int(r["space_index"])) for r in records}
+
+
+def run_sharded(units: dict, measure, rank: int, world: int, log: RecordLog | None = None,
+                resumed: list[dict] | None = None) -> np.ndarray:
+    """Measure this rank's share of every unit and return its packed records.
+
+    units: {(job, layer): [space_index, ...]} in selection order (the full list,
+    identical on every rank); measure(key, idx_list) -> list of record dicts.
+    Rank r takes the round-robin share of each list (shard), minus what
+    `resumed` (records read back from a RecordLog) already holds; the resumed
+    records that belong to this rank's share are returned with the new ones."""
+    done = measured_set(resumed or [])
+    blocks = []
+    for key in sorted(units):
+        mine = shard(units[key], rank, world)
+        mine_set = {int(c) for c in mine}
+        todo = [c for c in mine if (key[0], key[1], int(c)) not in done]
+        old = [r for r in (resumed or []) if (int(r["job"]), int(r["layer"])) == key
+               and int(r["space_index"]) in mine_set]
+        if old:
+            blocks.append(pack(old, key[0], key[1], rank))
+        if todo:
+            recs = measure(key, todo)
+            if log is not None:
+                log.append(recs, key[0], key[1], rank)
+            blocks.append(pack(recs, key[0], key[1], rank))
+    return np.concatenate(blocks) if blocks else np.zeros((0, len(REC_FIELDS)))

@@ -68,3 +68,21 @@ def test_aggregate_5k_sweet_spot():
     a = ex.aggregate_5k(m, fr)
     assert a["total_ms_by_tuned_at"]["0.25"] == pytest.approx(sum(m["0.25"][str(q)] for q in fr))
     assert a["sweet_spot_tuned_at"] == min(fr, key=lambda p: sum(m[str(p)][str(q)] for q in fr))
+
+
+def test_pd_check_flags_a_diagonal_above_its_column():
+    fr = (0.1, 1.0)
+
+    def row(m, cv=0.01):
+        return {"layer": "x", "matrix_us": {str(p): {str(q): m[(p, q)] for q in fr} for p in fr},
+                "matrix_cv": {str(p): {str(q): cv for q in fr} for p in fr}}
+    ok = row({(0.1, 0.1): 10.0, (1.0, 0.1): 10.2, (0.1, 1.0): 5.0, (1.0, 1.0): 4.0})
+    r = ex.pd_check([ok], fr)
+    assert r["pass"] and r["cells"] == 2
+    # diagonal 10.0 vs off-diagonal 9.5 at q = 0.1: 10.0 > 9.5 (1 + 3 x 0.01) -> violation
+    bad = row({(0.1, 0.1): 10.0, (1.0, 0.1): 9.5, (0.1, 1.0): 5.0, (1.0, 1.0): 4.0})
+    r = ex.pd_check([bad], fr)
+    assert not r["pass"] and r["violations"][0]["tuned_at"] == 1.0 and r["violations"][0]["run_at"] == 0.1
+    # the same gap is noise when the cells' CV is 2%: eps = 0.06 and 10.0 <= 9.5 x 1.06
+    assert ex.pd_check([row({(0.1, 0.1): 10.0, (1.0, 0.1): 9.5, (0.1, 1.0): 5.0, (1.0, 1.0): 4.0}, 0.02)],
+                       fr)["pass"]

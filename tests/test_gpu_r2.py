@@ -1,0 +1,324 @@
+"""GPU parity and path tests added in round 2 (VERDICT r01 "Next round" 3, 8):
+
+* epilogue codes 0 (none) and 2 (ReLU only) in the integer sweeps (SURVEY 8(d):
+  parity with and without the epilogue);
+* VGG-19 b16 at full size: schedules of every kind of every layer, and the
+  exhaustive-tune winners, against 4096 stored oracle points;
+* all 30 MobileNetV2 layers on random data;
+* concurrent tuners (a14): k host threads x tp_tune on disjoint green contexts,
+  gated on oracle points, winners checked against the full oracle output;
+* the fraction-taking entry points of SURVEY 8(b);
+* f2 (model-level cross-eval) and f3 (interference) drivers;
+* bench.py --gpus 2 and the resumable sharded tuning job (two ranks on one GPU,
+  TP_BENCH_DEVICE: the ranks' kernels never wait on each other);
+* compute-sanitizer memcheck / racecheck / synccheck on every kernel kind.
+"""
+import json
+import os
+import subprocess
+import sys
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import conv as oc
+from oracle import space as sp
+from paper_2008_03602_b200 import datagen, refs, shard, tp, workloads as wl
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _init():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test without a GPU")
+    tp.init(0)
+    yield
+
+
+def bf16_round(a):
+    return torch.tensor(np.asarray(a, dtype=np.float32)).bfloat16().double().numpy()
+
+
+def oracle_ref(d, x, w, b):
+    if d["dtype"] == tp.BF16:
+        x, w = bf16_round(x), bf16_round(w)
+    return oc.conv2d_c(d, x, w, b if d["epilogue"] & 1 else None, relu=bool(d["epilogue"] & 2))
+
+
+def rel_err(y, ref):
+    return float(np.max(np.abs(y - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+def mk(n, c, h, w, k, r, s, st=1, pad=0, g=1, dtype=tp.BF16, out=None, epi=3):
+    return dict(n=n, c=c, h=h, w=w, k=k, r=r, s=s, stride_h=st, stride_w=st, pad_h=pad, pad_w=pad, dil_h=1, dil_w=1,
+                groups=g, in_layout=tp.NHWC, dtype=dtype, out_dtype=dtype if out is None else out, epilogue=epi)
+
+
+def kinds_of(d):
+    out = {}
+    for i in range(tp.space_size(d)):
+        s = tp.space_get(d, i)
+        out.setdefault(s["kind"], []).append(s)
+    return out
+
+
+# ------------------------------------------------------------------ epilogue 0 / 2, every schedule (O11)
+EPI_SHAPES = [mk(1, 64, 10, 9, 64, 3, 3, 1, 1, out=tp.FP32),          # TMA im2col kind + split-K clusters
+              mk(1, 64, 6, 60, 40, 3, 3, 1, 1, out=tp.FP32),          # + row-halo kind
+              mk(1, 3, 23, 140, 64, 7, 7, 2, 3, out=tp.FP32),         # gathered + stem kinds
+              mk(1, 64, 128, 128, 128, 3, 3, 1, 1, out=tp.FP32),      # + multi-tile kind
+              mk(1, 36, 9, 9, 40, 3, 3, 1, 1, dtype=tp.FP32),         # direct + 3xTF32 kinds
+              mk(1, 16, 9, 9, 16, 3, 3, 2, 1, g=16, dtype=tp.FP32)]   # depthwise direct
+
+
+@pytest.mark.parametrize("epi", [0, 2])
+@pytest.mark.parametrize("d", EPI_SHAPES, ids=lambda d: f"{d['c']}x{d['h']}x{d['w']}_k{d['k']}_g{d['groups']}")
+def test_every_schedule_bit_exact_epilogue_variants(d, epi):
+    """Epilogue code 0 (no bias, no ReLU: negative outputs must survive) and 2
+    (ReLU without bias): every schedule of every kind equals the oracle bit
+    for bit on integer data."""
+    d = dict(d, epilogue=epi)
+    x, w, b = datagen.make_inputs(d, 41 + epi, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    if epi == 0:
+        assert ref.min() < 0
+    buf = tp.LayerBuffers(d, x, w, b)
+    step = 1 if tp.space_size(d) <= 1200 else 3     # the 128x128 layer: every third schedule (~500)
+    bad, n = [], 0
+    for i in range(0, tp.space_size(d), step):
+        s = tp.space_get(d, i)
+        n += 1
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        if not np.array_equal(buf.output(), ref):
+            bad.append((i, s["kind"], s["bm"], s["bn"], s["split_k"], s["tiles_per_cta"]))
+    assert not bad, f"{len(bad)}/{n} schedules differ, first: {bad[:5]}"
+
+
+# ------------------------------------------------------------------ VGG-19 b16 at full size, every kind
+def _vgg_exhaustive_winners():
+    p = os.path.join(ROOT, "profiles", "r01_exhaustive_vgg19_25.json")
+    out = {}
+    if os.path.exists(p):
+        d = json.load(open(p))
+        for name, med in d["layers"].items():
+            med = np.asarray(med, dtype=np.float64)
+            if np.isfinite(med).any():
+                out[name] = (len(med), int(np.nanargmin(np.where(med > 0, med, np.nan))))
+    return out
+
+
+VGG = wl.catalog("vgg19_b16")
+
+
+@pytest.mark.parametrize("li", range(len(VGG)), ids=[d["name"] for d in VGG])
+def test_vgg_full_size_every_kind_vs_oracle(li):
+    """Full BASELINE size (batch 16): for every kind in the layer's space, four
+    seeded schedules (first, last and two sampled) plus the winner of the
+    recorded exhaustive tune at 25%, run in a 25% partition with the geometry
+    frozen at its granted SMs, against the 4096 stored oracle points."""
+    d = VGG[li]
+    part = tp.Partition.get(0.25)
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(4, li))
+    idx, ref = refs.load("vgg19_b16", 4, VGG)[li]
+    buf = tp.LayerBuffers(d, x, w, b, part=part)
+    chosen = []
+    for kind, scheds in kinds_of(d).items():
+        pick = {0, len(scheds) - 1} | {int(j) for j in sp.sample(len(scheds), 2, 100 + li + kind)}
+        chosen += [scheds[j] for j in sorted(pick)]
+    win = _vgg_exhaustive_winners().get(d["name"])
+    if win is not None and win[0] == tp.space_size(d):
+        chosen.append(tp.space_get(d, win[1]))
+    bad = []
+    for s in chosen:
+        s = dict(s, sm_tuned=part.sm_granted)
+        buf.y.fill_(0xFF)
+        torch.cuda.synchronize()
+        tp.conv2d_run(buf, s, part)
+        part.sync()
+        err = rel_err(buf.gather(idx, part), ref)
+        if not err <= 2e-2:
+            bad.append((s["space_index"], s["kind"], s["bm"], s["bn"], s["tiles_per_cta"], err))
+    assert len({s["kind"] for s in chosen}) == len(kinds_of(d))
+    assert not bad, f"{len(bad)}/{len(chosen)} schedules off, first: {bad[:5]}"
+
+
+# ------------------------------------------------------------------ all 30 MobileNetV2 layers, random data
+MB = wl.catalog("mobilenetv2")
+
+
+@pytest.mark.parametrize("li", range(len(MB)), ids=[d["name"] for d in MB])
+def test_mobilenetv2_layer_random_parity(li):
+    d = MB[li]
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(5, li))
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    chosen = []
+    for kind, scheds in kinds_of(d).items():
+        chosen += [scheds[j] for j in sp.sample(len(scheds), 4, 7 + li)]
+    for s in chosen:
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        err = rel_err(buf.output(), ref)
+        assert err <= 2e-2, (s["space_index"], s["kind"], err)
+
+
+# ------------------------------------------------------------------ a14: concurrent tuners, oracle-gated
+def test_concurrent_tuners_oracle_gate_and_winners():
+    """4 disjoint green contexts (one split), one host thread each running
+    tp_tune on its own two ResNet-50 layers with oracle check points: every
+    record passes the oracle gate, and each winner's full output (left in y by
+    tp_tune) matches the full fp64 oracle output."""
+    layers = wl.catalog("resnet50")
+    share = [[1, 12], [2, 16], [5, 19], [10, 22]]
+    parts = tp.Partition.split(4, 32)
+    try:
+        work = {}
+        for j, ids in enumerate(share):
+            for li in ids:
+                d = layers[li]
+                x, w, b = datagen.make_inputs(d, datagen.data_seed(2, li))
+                ref = oracle_ref(d, x, w, b)
+                idx = datagen.sample_points(ref.size, 4096, 61 + li)
+                work[li] = (tp.LayerBuffers(d, x, w, b, part=parts[j]), ref, idx)
+        torch.cuda.synchronize()
+        results, errors = {}, []
+
+        def worker(j):
+            try:
+                for li in share[j]:
+                    buf, ref, idx = work[li]
+                    best, m, recs = tp.tune(buf, parts[j], 96, datagen.sampler_seed(1), check_idx=idx,
+                                            check_ref=ref.reshape(-1)[idx])
+                    results[li] = (best, m, recs, buf.output())
+            except Exception as e:   # surfaced below
+                errors.append(repr(e))
+
+        th = [threading.Thread(target=worker, args=(j,)) for j in range(4)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert not errors, errors
+        for j, ids in enumerate(share):
+            for li in ids:
+                best, m, recs, y = results[li]
+                assert all(r["status"] == 0 for r in recs), [r for r in recs if r["status"]][:3]
+                assert best["sm_tuned"] == parts[j].sm_granted
+                assert rel_err(y, work[li][1]) <= 2e-2, (layers[li]["name"], best)
+    finally:
+        for p in parts:
+            p.close()
+
+
+# ------------------------------------------------------------------ SURVEY 8(b) fraction-taking entry points
+def test_fraction_entry_points_match_partition_calls():
+    d = wl.catalog("resnet50")[2]
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(2, 2))
+    idx, ref = refs.load("resnet50", 2, wl.catalog("resnet50"))[2]
+    buf = tp.LayerBuffers(d, x, w, b)
+    best, m, recs = tp.tune_at(buf, 0.25, 32, 42, check_idx=idx, check_ref=ref)
+    part = tp.Partition.get(0.25)
+    assert m["sm_granted"] == part.sm_granted and best["sm_tuned"] == part.sm_granted
+    assert all(r["status"] == 0 for r in recs) and len(recs) == 32
+    assert rel_err(buf.gather(idx), ref) <= 2e-2
+    r = tp.conv2d_run_at(buf, best, 0.5)
+    c = tp.cross_eval_at(buf, best, 0.5)
+    assert r["status"] == 0 and c["status"] == 0 and r["sm_granted"] == c["sm_granted"] == tp.Partition.get(0.5).sm_granted
+    assert c["ctas"] == m["ctas"]          # frozen geometry (reading C15)
+
+
+# ------------------------------------------------------------------ f2 / f3 drivers
+def test_model_cross_eval_driver_f2():
+    from paper_2008_03602_b200 import experiments as ex
+    layers = wl.catalog("resnet50")[1:4]
+    fr = (0.25, 1.0)
+    checks = refs.load("resnet50", 2, wl.catalog("resnet50"))[1:4]
+    res = ex.cross_eval(layers, fr, trials=24, config=2, checks=checks, log=lambda *a: None)
+    assert set(res["model_sum_us"]) == {"0.25", "1.0"}
+    for row in res["layers"]:
+        for p in ("0.25", "1.0"):
+            assert all(v > 0 for v in row["matrix_us"][p].values())
+        assert set(row["default_us"]) == {"0.25", "1.0"}
+    assert res["tune"]["0.25"]["ok"] == res["tune"]["0.25"]["candidates"] == 3 * 24
+    assert res["pd_check"]["cells"] == 3 * 2
+    agg = res["aggregate_5k"]
+    assert agg["sweet_spot_tuned_at"] in fr and agg["untuned_total_ms"] > 0
+
+
+def test_interference_driver_f3():
+    from paper_2008_03602_b200 import experiments as ex
+    res = ex.interference("cfg1", k=2, sms_each=36, trials=24, log=lambda *a: None)
+    assert set(res["modes"]) == {"isolated", "shared", "time_sliced"}
+    for mode, r in res["modes"].items():
+        assert r["candidates"] == 24 and r["candidates_per_s"] > 0
+        assert all(row["solo_us"] > 0 for row in r["layers"])
+
+
+# ------------------------------------------------------------------ multi-rank paths (two ranks, one GPU)
+def _run(cmd, env_extra, timeout=900):
+    env = dict(os.environ, TP_BENCH_DEVICE="0", **env_extra)
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_bench_gpus2_launches_two_ranks():
+    """bench.py --gpus 2 with no torchrun environment re-launches itself as two
+    ranks; the job's candidates are the two weak-scaling jobs' lists, all
+    measured (each rank its round-robin share) and all oracle-gated OK."""
+    out = _run([sys.executable, "bench.py", "--gpus", "2", "--steps", "1", "--warmup", "0", "--no-cpu", "--no-e2e",
+                "--workload", "mobilenetv2", "--fraction", "0.5"], {})
+    line = out[-1]
+    n = sum(tp.space_size(d) for d in MB)
+    assert line["n_gpus"] == 2 and line["config"]["candidates_per_step"] == 2 * n
+    assert line["candidates_total"] == 2 * n and line["candidates_ok"] == 2 * n
+    assert line["config"]["sm_granted"] == tp.Partition.get(0.5).sm_granted
+
+
+def test_tune_job_two_ranks_union_merge_and_resume(tmp_path):
+    """The sharded tuning job: the two ranks' logged candidates are exactly the
+    single list of every layer; rank 0's merged argmin equals the argmin over
+    the union of the logs; a --resume run re-measures nothing."""
+    log = str(tmp_path / "log")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + os.getpid() % 1000),
+           "-m", "paper_2008_03602_b200.tune_job", "--workload", "cfg1", "--fraction", "0.5", "--log-dir", log]
+    first = _run(cmd, {})[-1]
+    cat = wl.catalog("cfg1")
+    logged = shard.RecordLog.load(log)
+    full = {(0, li, i) for li, d in enumerate(cat) for i in tp.space_sample(d, 1000, 42)}
+    assert shard.measured_set(logged) == full and len(logged) == len(full)
+    assert {r["rank"] for r in logged} == {0, 1}
+    merged = shard.merge_best(logged)
+    assert [w["merged_argmin"] for w in first["winners"]] == [merged[(0, li)]["space_index"] for li in range(len(cat))]
+    again = _run(cmd + ["--resume"], {})[-1]
+    assert again["resumed"] == len(full) and again["measured_by_rank0"] == 0 and again["records"] == len(full)
+    assert len(shard.RecordLog.load(log)) == len(full)
+
+
+# ------------------------------------------------------------------ compute-sanitizer on every kernel kind
+SANITIZER = "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer_every_kind(tool):
+    """One tiny launch of every kernel kind (TMA im2col with and without the
+    split-K cluster, global split-K fallback, gathered, row-halo, multi-tile,
+    stem, 3xTF32, direct, the pack/gather kernels) under compute-sanitizer;
+    0 errors reported."""
+    if not os.path.exists(SANITIZER):
+        pytest.fail("compute-sanitizer missing")
+    cmd = [SANITIZER, "--tool", tool, "--error-exitcode", "17", "--print-limit", "20",
+           sys.executable, os.path.join(ROOT, "tools", "sanitize_kinds.py")]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
+    tail = (r.stdout[-4000:] + r.stderr[-4000:])
+    assert r.returncode == 0, tail
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail
+    assert "sanitize_kinds ok" in r.stdout, tail

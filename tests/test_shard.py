@@ -89,5 +89,44 @@ def test_gpu_busy_counts_gate_warmup_and_groups():
     recs = [dict(status=0, median_us=2.0, n_per_group=10, groups=5), dict(status=0, median_us=4.0, n_per_group=10,
                                                                            groups=1),
             dict(status=5, median_us=1.0, n_per_group=0, groups=0)]
-    # (1 + 3 + 50) * 2 + (1 + 3 + 10) * 4
-    assert shard.gpu_busy_us(recs) == 54 * 2.0 + 14 * 4.0
+    # full protocol: (gate 1 + 3 warm-ups + 5 x 10) * 2; raced (C12b, one group): (1 + 1 warm-up + 10) * 4
+    assert shard.gpu_busy_us(recs) == 54 * 2.0 + 12 * 4.0
+    assert shard.raced_frac(recs) == 0.5
+
+
+def _fake_measure(calls):
+    def measure(key, idx):
+        calls.append((key, list(idx)))
+        rng = random.Random(hash(key) & 0xFFFF)
+        base = {i: rng.choice([1.0, 1.5, 2.0]) for i in range(1000)}
+        return [dict(space_index=int(i), status=0, median_us=base[int(i)] + 0.001 * i, min_us=0.9, mean_us=1.0,
+                     std_us=0.1, sm_granted=148, ctas=10, threads_per_cta=128, waves=1, n_per_group=10, groups=5)
+                for i in idx]
+    return measure
+
+
+def test_record_log_resume(tmp_path):
+    units = {(0, 0): sp.sample(300, 1000, 1), (0, 1): sp.sample(200, 50, 2), (1, 0): sp.sample(120, 1000, 3)}
+    # reference: one uninterrupted single-rank pass
+    full = shard.unpack(shard.run_sharded(units, _fake_measure([]), 0, 1))
+    # an interrupted pass: rank 0 of 2 logs unit (0, 0) and dies with a torn last line
+    log = shard.RecordLog(str(tmp_path), 0)
+    calls = []
+    shard.run_sharded({(0, 0): units[(0, 0)]}, _fake_measure(calls), 0, 2, log=log)
+    with open(log.path, "a") as f:
+        f.write('{"job": 0, "layer": 1, "space_ind')
+    logged = shard.RecordLog.load(str(tmp_path))
+    assert len(logged) == len(shard.shard(units[(0, 0)], 0, 2))
+    # restart (both ranks): rank 0 re-measures nothing of unit (0, 0); the union covers every candidate once
+    calls = []
+    blocks = [shard.run_sharded(units, _fake_measure(calls), r, 2, log=shard.RecordLog(str(tmp_path), r),
+                                resumed=logged) for r in range(2)]
+    remeasured = {(k, i) for k, idx in calls for i in idx}
+    assert not any(k == (0, 0) and i in set(shard.shard(units[(0, 0)], 0, 2)) for k, i in remeasured)
+    merged = shard.unpack(np.concatenate(blocks))
+    assert sorted((r["job"], r["layer"], r["space_index"]) for r in merged) == \
+        sorted((r["job"], r["layer"], r["space_index"]) for r in full)
+    a, b = shard.merge_best(merged), shard.merge_best(full)
+    assert {k: v["space_index"] for k, v in a.items()} == {k: v["space_index"] for k, v in b.items()}
+    # the log now holds every record exactly once (the torn line is ignored)
+    assert len(shard.measured_set(shard.RecordLog.load(str(tmp_path)))) == len(full)
