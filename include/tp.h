@@ -235,8 +235,9 @@ tp_status tp_conv2d_run(const tp_conv_desc* d, const tp_schedule* s, tp_partitio
  * cluster barrier, [66] all slices received, [67] reduction stored; gathered kind,
  * first 8 k-blocks: [68..75] chunks stored, [76..83] past the proxy fence, [84..91]
  * past the empty-slot wait.
- * cap >= grid CTAs: one launch, *rows = CTAs.  cap >= 2 x grid CTAs: two back-to-back
- * launches (rows [0, CTAs) the first, [CTAs, 2 CTAs) the second; exposes the PDL overlap). */
+ * cap >= k x grid CTAs (k <= 4): k back-to-back launches captured in one CUDA graph (the
+ * timing protocol's launch mode), rows [l CTAs, (l+1) CTAs) for launch l; *rows = k x CTAs.
+ * The later launches expose the PDL overlap as the tuner measures it. */
 tp_status tp_conv2d_trace(const tp_conv_desc* d, const tp_schedule* s, tp_partition* part, const void* x,
                           const void* w, const void* bias, void* y, void* ws, size_t ws_bytes,
                           uint64_t* trace_host, int32_t cap, int32_t* rows);
@@ -294,6 +295,23 @@ tp_status tp_tune_guided(const tp_conv_desc* d, tp_partition* part, int32_t tria
 tp_status tp_cross_eval(const tp_conv_desc* d, const tp_schedule* tuned_at_p, tp_partition* part_q,
                         const void* x, const void* w, const void* bias, void* y, void* ws,
                         size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
+
+/* Model-level run (reading C21): layers 0..n-1 run in order
+ * inside `part` -- layer i+1 starts its reads only after layer i's outputs are
+ * complete -- `reps` times back to back, captured as ONE CUDA graph.  Ordering
+ * is a flag chain where both neighbours are TMA im2col launches (a global
+ * arrival counter, acquire/release at gpu scope) and grid
+ * completion (PDL griddepcontrol.wait) elsewhere, so layer i+1 may read layer
+ * i's y (x[i+1] == y[i]).  Per-layer arrays of length n: descs, scheds (any
+ * schedule of each layer's space), device pointers x, w, bias (may be NULL),
+ * y, ws and ws_bytes as for tp_conv2d_run.  timing == NULL and out == NULL:
+ * one asynchronous replay.  Otherwise warmup replays, then `groups` timed
+ * replays; out->median_us = per-sequence latency (group time / reps),
+ * n_per_group = reps.  Errors: as tp_conv2d_run for any layer. */
+tp_status tp_chain_run(int32_t n_layers, const tp_conv_desc* descs, const tp_schedule* scheds, tp_partition* part,
+                       const void* const* x, const void* const* w, const void* const* bias, void* const* y,
+                       void* const* ws, const size_t* ws_bytes, int32_t reps, const tp_timing* timing,
+                       tp_measurement* out);
 
 /* ---- the same calls with GPU% given as a fraction (SURVEY 8(b) spelling) --
  * sm_fraction in (0, 1] selects the cached partition of (device of the last

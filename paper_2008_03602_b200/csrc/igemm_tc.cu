@@ -79,18 +79,13 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   unsigned long long* trace =
       a.trace ? a.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTraceSlots
               : nullptr;
+  if (a.dep_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Entry stamps stay in registers until the prologue is done: a global store
+  // here would make the release fence below wait for it.
+  unsigned long long tr_entry = 0, tr_gt = 0;
   if (trace && threadIdx.x == 0) {
-    trace[0] = gtimer();
-    unsigned long long g;
-    unsigned sm;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    trace[63] = g;
-    trace[62] = sm;
-    unsigned ncta;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
-    trace[61] = ncta;
-    trace[60] = (unsigned long long)a.cluster_red;
+    tr_entry = gtimer();
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_gt));
   }
   const int kb0 = (split * a.kblocks) / a.split_k;   // 32-bit: M, k-blocks < 2^31 (checked on the host)
   const int kb1 = ((split + 1) * a.kblocks) / a.split_k;
@@ -236,10 +231,22 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   // a release arrive would also wait for this thread's outstanding memory operations)
   if (a.cluster_red) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // provably warp-uniform
-  if (trace && threadIdx.x == 0) trace[1] = gtimer();
+  if (trace && threadIdx.x == 0) {
+    trace[1] = gtimer();
+    trace[0] = tr_entry;
+    trace[63] = tr_gt;
+    unsigned sm, ncta;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncta));
+    trace[62] = sm;
+    trace[61] = ncta;
+    trace[60] = (unsigned long long)a.cluster_red;
+  }
   // Every warp sleeps in the PDL wait rather than spinning on an mbarrier while
-  // the previous grid may still run on this SM (co-resident CTAs).
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the previous grid may still run on this SM (co-resident CTAs).  In a flag
+  // chain only the TMA producers wait (on the arrival counter): no other warp
+  // touches memory the predecessors write.
+  if (GATHER || a.dep_wait == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (GATHER && warp != 1) {
     // ---------------- gather producers (all warps but the MMA warp) ----------------
@@ -326,7 +333,12 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   } else if (is_prod) {
     // ---------------- TMA producers: k-blocks j = prank (mod nprod), one elected lane each ----------------
     const uint32_t lead = elect_one();
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (a.dep_wait > 0) {
+      if (lead) dep_wait_acquire(a.dep_ctr, a.dep_wait);
+      __syncwarp();
+    } else {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     // Every operand this grid reads is now final: the next kernel in the
     // stream may be scheduled (programmatic dependent launch).
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -406,6 +418,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   for (int c = c_begin; c < c_end; c += 16) {
     uint32_t raw[16];
     tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c, raw);
+    if (!GATHER && trace && threadIdx.x == 0 && c == c_begin) trace[68] = gtimer();
     const int nb = nbase + c;
     float bv[16];
 #pragma unroll
@@ -460,7 +473,11 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
           float t = __uint_as_float(raw[i]) + bv[i];
           v[i] = a.relu ? fmaxf(t, 0.0f) : t;
         }
-        store16(a.y, m, a.K, nb, v, a.out_f32);
+        if (a.dbg & 4) {   // experiments only: no y stores
+          if (v[0] == 12345.0f) store16(a.y, m, a.K, nb, v, a.out_f32);
+        } else {
+          store16(a.y, m, a.K, nb, v, a.out_f32);
+        }
       }
     } else if (a.cluster_red) {
       // Row segment -> the owner CTA's receive slot [split][row - owner_r0]:
@@ -493,6 +510,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     }
   }
 
+  if (!GATHER && trace && threadIdx.x == 0) trace[69] = gtimer();
   if (a.split_k == 1 && a.y_tma) {
     // generic-proxy smem writes -> visible to the TMA engine; one thread stores.
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -503,6 +521,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       for (int j = 0; j < BN * EB / IB; ++j)
         tma_store_2d(&tmY, smem_raw + (size_t)j * BM * IB, nbase + j * (IB / EB), m0);
       tma_store_commit_wait();
+      if (a.dep_signal) tma_store_wait_all();   // the writes, not only the smem reads
     }
   }
   if (a.split_k > 1 && a.cluster_red) {
@@ -579,9 +598,11 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     }
   }
 
+  if (!GATHER && trace && threadIdx.x == 0) trace[70] = gtimer();
   tc_fence_before();
   __syncthreads();
   if (trace && threadIdx.x == 0) trace[3] = gtimer();
+  if (a.dep_signal && threadIdx.x == 0) dep_signal_release(a.dep_ctr);
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
@@ -1301,6 +1322,10 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     a.nprod = nprod_env < 1 ? 1 : nprod_env;   // producer warps cap (experiments: TP_NPROD)
   }
   a.w_early = 0;   // set per launch sequence by the runtime (time_plan / tuner phase B)
+  a.dep_ctr = nullptr;   // flag chain: set per launch by the runtime (timing graphs)
+  a.dep_wait = 0;
+  a.dep_signal = 0;
+  a.dep_early = 0;
   a.a_tiled = a_tiled ? 1 : 0;
   a.y_tma = y_tma;
   plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.mt ? 3 : (pb.row ? 2 : (pb.gather ? 1 : 0))));

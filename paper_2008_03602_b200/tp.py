@@ -113,6 +113,8 @@ _sig("tp_tune_guided", _P(ConvDesc), _vp, _i32, _i32, _dbl, _u64, _vp, _vp, _vp,
      _i32, _dbl, _P(Timing), _P(Schedule), _P(Measurement), _P(Measurement), _i32, _P(_i32))
 _sig("tp_cross_eval", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(Timing), _P(Measurement))
 _sig("tp_conv2d_trace", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(_u64), _i32, _P(_i32))
+_sig("tp_chain_run", _i32, _P(ConvDesc), _P(Schedule), _vp, _P(_vp), _P(_vp), _P(_vp), _P(_vp), _P(_vp), _P(_sz), _i32,
+     _P(Timing), _P(Measurement))
 _sig("tp_pack_input", _P(ConvDesc), _vp, _vp, _vp)
 _sig("tp_pack_weights", _P(ConvDesc), _vp, _vp, _vp)
 _sig("tp_gather_output", _P(ConvDesc), _vp, _vp, _P(_i64), _i32, _P(_dbl))
@@ -421,11 +423,11 @@ def conv2d_run(buf: LayerBuffers, sched: dict, part: Partition | None = None, ti
 
 
 def conv2d_trace(buf: "LayerBuffers", sched: dict, part: Partition | None = None, launches: int = 1) -> np.ndarray:
-    """In-kernel timeline of one (or two back-to-back) tensor-core launches:
-    (launches * ctas, 96) uint64 (see tp.h)."""
+    """In-kernel timeline of 1-4 back-to-back tensor-core launches, captured in
+    one CUDA graph: (launches * ctas, 96) uint64 (see tp.h)."""
     x, w, b, y, ws, wsb = buf.ptrs()
     cap = int(sched.get("grid_x", 0) * sched.get("grid_y", 0) * sched.get("grid_z", 0)) or 65536
-    cap *= max(1, min(2, launches))
+    cap *= max(1, min(4, launches))
     out = np.zeros((cap, 96), dtype=np.uint64)
     rows = _i32()
     _ck(_lib.tp_conv2d_trace(ctypes.byref(buf.cd), ctypes.byref(dict_to_sched(sched)), _h(part), x, w, b, y, ws,
@@ -537,6 +539,32 @@ def cross_eval(buf: LayerBuffers, tuned_sched: dict, part_q: Partition | None,
     _ck(_lib.tp_cross_eval(ctypes.byref(buf.cd), ctypes.byref(dict_to_sched(tuned_sched)), _h(part_q), x, w, b, y,
                            ws, wsb, ctypes.byref(timing_cfg) if timing_cfg is not None else None, ctypes.byref(m)),
         "tp_cross_eval")
+    return meas_to_dict(m)
+
+
+def chain_run(bufs: list, scheds: list[dict], part: Partition | None = None, reps: int = 1,
+              timing_cfg: Timing | None = None, measure: bool = False):
+    """tp_chain_run: the layers of `bufs` in order (layer i+1 may read layer
+    i's y as its x), `reps` times, as one graph.  measure=True -> the timing
+    protocol over whole sequences; returns the measurement dict (median_us per
+    sequence) or None for a single asynchronous replay."""
+    n = len(bufs)
+    descs = (ConvDesc * n)(*[b.cd for b in bufs])
+    ss = (Schedule * n)(*[dict_to_sched(s) for s in scheds])
+    ptr = lambda vals: (_vp * n)(*vals)   # noqa: E731
+    xs = ptr([b.x.data_ptr() for b in bufs])
+    ws_ = ptr([b.w.data_ptr() for b in bufs])
+    bs = ptr([b.b.data_ptr() for b in bufs])
+    ys = ptr([b.y.data_ptr() for b in bufs])
+    wk = ptr([b.ws.data_ptr() for b in bufs])
+    wb = (_sz * n)(*[b.ws.numel() for b in bufs])
+    if not measure and timing_cfg is None:
+        _ck(_lib.tp_chain_run(n, descs, ss, _h(part), xs, ws_, bs, ys, wk, wb, int(reps), None, None), "tp_chain_run")
+        return None
+    m = Measurement()
+    _ck(_lib.tp_chain_run(n, descs, ss, _h(part), xs, ws_, bs, ys, wk, wb, int(reps),
+                          ctypes.byref(timing_cfg) if timing_cfg is not None else None, ctypes.byref(m)),
+        "tp_chain_run")
     return meas_to_dict(m)
 
 

@@ -84,9 +84,11 @@ def full(path, out):
     json.dump({"source": path, "kernels": res}, open(out, "w"), indent=1)
 
 
-def dram(path, out, catalog="resnet50"):
+def dram(path, out, catalog="resnet50", winners=None):
     """Per-launch DRAM traffic (ncu replays with cold caches: the compulsory
-    bytes each tuned layer really moves) next to its algorithmic bytes."""
+    bytes each tuned layer really moves) next to its algorithmic bytes.
+    winners: the bench JSON line (or {layer: space_index}) the capture ran,
+    recorded per layer so bench.py can tell which winners it covers."""
     sys.path.insert(0, ".")
     from paper_2008_03602_b200 import experiments as ex, workloads as wl
     rows = list(csv.reader(open(path)))
@@ -98,17 +100,24 @@ def dram(path, out, catalog="resnet50"):
         e = per.setdefault(r[ii], {"kernel": r[ki].split("(")[0]})
         e[r[mi]] = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1)
     layers = wl.catalog(catalog)
+    win = {}
+    if winners:
+        src = json.load(open(winners))
+        win = {r["layer"]: r["space_index"] for r in src["latency_us"]["per_layer"]} if "latency_us" in src else src
     res = []
     for d, e in zip(layers, per.values()):
         alg = ex.layer_work(d)[1]
         traffic = e.get("dram__bytes_read.sum", 0) + e.get("dram__bytes_write.sum", 0)
-        res.append({"layer": d["name"], "kernel": e["kernel"], "dram_bytes": traffic, "algorithmic_bytes": alg,
+        res.append({"layer": d["name"], "space_index": win.get(d["name"]), "kernel": e["kernel"],
+                    "dram_bytes": traffic, "algorithmic_bytes": alg,
                     "ratio": traffic / alg, "cold_us": e.get("gpu__time_duration.sum")})
     n = len(res)
     json.dump({"source": path, "note": "ncu default cache control (caches flushed before each replay): DRAM bytes are "
                                        "the cold-cache traffic of one launch of each tuned layer",
                "launches": n, "mean_dram_bytes_per_launch": sum(r["dram_bytes"] for r in res) / max(n, 1),
                "mean_algorithmic_bytes_per_launch": sum(r["algorithmic_bytes"] for r in res) / max(n, 1),
+               "dram_over_algorithmic": sum(r["dram_bytes"] for r in res) / max(1.0, sum(r["algorithmic_bytes"]
+                                                                                         for r in res)),
                "layers": res}, open(out, "w"), indent=1)
 
 
