@@ -66,7 +66,16 @@ enum { TP_EPI_BIAS = 1, TP_EPI_RELU = 2 };
  * are gathered into shared memory by CUDA-core warps over the flattened
  * (r, s, c) axis (bf16, g = 1, C % 8 != 0: the C = 3 stems). */
 enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2, TP_KIND_IGEMM_TC_ROW = 3,
-       TP_KIND_IGEMM_TC_MT = 4, TP_KIND_IGEMM_TF32X3 = 5, TP_KIND_IGEMM_TC_STEM = 6 };
+       TP_KIND_IGEMM_TC_MT = 4, TP_KIND_IGEMM_TF32X3 = 5, TP_KIND_IGEMM_TC_STEM = 6, TP_KIND_IGEMM_TC_STRIP = 7 };
+/* IGEMM_TC_STRIP ("strip"): appended after the gathered (and stem) tuples of
+ * gathered layers with C <= 8, stride_w in {1, 2}, R, S <= 8.  A pre-pass inside
+ * the call pads x to NHWC with 8 channels and w to [K][R][S][8] (16-byte pixel
+ * rows, in the workspace); a tile is BM pixels of one output row; per filter row
+ * one TMA box per column phase brings the input strip (element stride s_w) and
+ * one MMA covers two taps of a phase (no-swizzle K-major core matrices 16 B
+ * apart along K).  Knobs BM {64, 128}, BN {32, 64, 128}, stages {2, 4, 6},
+ * tiles_per_cta {1, 2, 4, 8, 16}; bk = 16, threads = 256, split_k = 1;
+ * grid = (ceil(N P ceil(Q / BM) / tiles_per_cta), ceil(K / BN), 1). */
 /* IGEMM_TC_MT ("multi-tile im2col"): appended last to the space of IGEMM_TC
  * layers with ceil(M/64)*ceil(K/32) >= 1024.  The IGEMM_TC k-blocks (one TMA
  * im2col box + one weight box per (channel block, tap), BK = 64) run in the

@@ -26,6 +26,7 @@ KIND_IGEMM_TC_ROW = 3
 KIND_IGEMM_TC_MT = 4
 KIND_IGEMM_TF32X3 = 5
 KIND_IGEMM_TC_STEM = 6
+KIND_IGEMM_TC_STRIP = 7
 DTYPE_BF16 = 0
 DTYPE_FP32 = 1
 SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
@@ -36,6 +37,7 @@ ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)
              ("tiles_per_cta", (1, 2, 4, 8, 16)))
 MT_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("tiles_per_cta", (2, 4, 8)))
 STEM_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128)), ("tiles_per_cta", (2, 4, 8, 16)))
+STRIP_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128)), ("stages", (2, 4, 6)), ("tiles_per_cta", (1, 2, 4, 8, 16)))
 TF32_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("split_k", (1, 2, 4, 8)))
 DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
                 ("tile_p", (1, 2, 4, 8)), ("smem_stage", (0, 1)))
@@ -186,6 +188,29 @@ def _valid_stem(d: dict, bm: int, bn: int, tiles_per_cta: int) -> bool:
     return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))
 
 
+def strip_eligible(d: dict) -> bool:
+    """Strip kind: gathered layers with C <= 8, column
+    stride 1 or 2 and filters of at most 8 x 8."""
+    return (layer_kind(d) == KIND_IGEMM_TC_GATHER and d["c"] <= 8 and d["stride_w"] in (1, 2)
+            and d["s"] <= 8 and d["r"] <= 8)
+
+
+def _valid_strip(d: dict, bm: int, bn: int, stages: int, tiles_per_cta: int) -> bool:
+    # one ring stage = s_w phase boxes of (bm + 2 ceil(T0 / 2) - 1) 16-byte pixels, each rounded
+    # up to 128 B, where T0 = ceil(S / s_w) taps fall in phase 0; resident weights: R rows of
+    # (S + s_w) taps x bn rows x 16 B, rounded up to 1 KiB; + 1 KiB of barriers
+    P, Q = out_pq(d)
+    sw = d["stride_w"]
+    px = bm + 2 * _cdiv(_cdiv(d["s"], sw), 2) - 1
+    if sw * px > 256:                # a TMA box spans at most 256 elements per dimension
+        return False
+    stage = sw * _cdiv(px * 16, 128) * 128
+    weights = _cdiv(d["r"] * (d["s"] + sw) * bn * 16, 1024) * 1024
+    if stages * stage + weights + 1024 > SMEM_LIMIT:
+        return False
+    return bm <= max(64, _np2(Q)) and bn <= max(32, _np2(d["k"]))
+
+
 def tf32_eligible(d: dict) -> bool:
     """3xTF32 tensor-core kind: fp32 dense layers whose NHWC
     pixel rows are 16-byte multiples (C % 4 == 0) and K % 8 == 0."""
@@ -243,6 +268,13 @@ def enumerate_space(d: dict) -> list[dict]:
                          kind=KIND_IGEMM_TC_STEM, space_index=len(out))
                 s.update(geometry(d, s))
                 out.append(s)
+    if strip_eligible(d):        # after the stem tuples; bk = 16, threads = 256, split_k = 1
+        for combo in itertools.product(*[v for _, v in STRIP_KNOBS]):
+            if _valid_strip(d, *combo):
+                s = dict(zip([k for k, _ in STRIP_KNOBS], combo), bk=16, threads=256, split_k=1,
+                         kind=KIND_IGEMM_TC_STRIP, space_index=len(out))
+                s.update(geometry(d, s))
+                out.append(s)
     if mt_eligible(d):           # appended last; threads = 256, bk = 64, split_k = 1
         for combo in itertools.product(*[v for _, v in MT_KNOBS]):
             if _valid_mt(d, *combo):
@@ -258,7 +290,7 @@ def geometry(d: dict, s: dict) -> dict:
     P, Q = out_pq(d)
     if s.get("kind") == KIND_IGEMM_TC_MT:
         g = (_cdiv(_cdiv(d["n"] * P * Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
-    elif s.get("kind") == KIND_IGEMM_TC_STEM:
+    elif s.get("kind") in (KIND_IGEMM_TC_STEM, KIND_IGEMM_TC_STRIP):
         g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
     elif s.get("kind") == KIND_IGEMM_TC_ROW:
         g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <algorithm>
 #include <cstdint>
 
 #include "tp_kernels.h"
@@ -160,6 +161,49 @@ __global__ void empty_kernel(int* sink) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (sink && threadIdx.x == 0 && blockIdx.x == 0x7fffffff) *sink = 1;   // never taken
+}
+
+// Strip-kind pre-pass (TP_KIND_IGEMM_TC_STRIP): x NHWC with C <= 8 channels ->
+// x8 NHWC with 8 (zero padded, 16-byte pixels); w KRSC -> w8 [R][S][K][8].
+// One 16-byte store per pixel / weight row; waits for the producer of x (PDL).
+__global__ void pad_c8_kernel(const uint16_t* __restrict__ x, uint4* __restrict__ x8, int64_t npix, int C,
+                              const uint16_t* __restrict__ w, uint4* __restrict__ w8, int K, int R, int S) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t nw = (int64_t)K * R * S;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix + nw; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint16_t* src;
+    uint4* dst;
+    if (i < npix) {
+      src = x + i * C;
+      dst = x8 + i;
+    } else {
+      const int64_t j = i - npix;                     // (k, r, s) in KRS order
+      const int k = (int)(j / (R * S)), rs = (int)(j - (int64_t)k * R * S);
+      src = w + j * C;
+      dst = w8 + (int64_t)rs * K + k;                 // [r][s][k]
+    }
+    uint32_t v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = c < C ? src[c] : 0u;
+    *dst = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+  }
+}
+
+cudaError_t launch_pad_c8(const void* x, void* x8, int64_t npix, int C, const void* w, void* w8, int K, int R, int S,
+                          int pdl, cudaStream_t st) {
+  const int64_t total = npix + (int64_t)K * R * S;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::min<int64_t>((total + 255) / 256, 148 * 8));
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, pad_c8_kernel, reinterpret_cast<const uint16_t*>(x), reinterpret_cast<uint4*>(x8),
+                            npix, C, reinterpret_cast<const uint16_t*>(w), reinterpret_cast<uint4*>(w8), K, R, S);
 }
 
 // The empty kernel as a link of a flag chain (TcArgs::dep_*): wait for the

@@ -625,10 +625,21 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 // MT (ROW = false) runs the same multi-tile pipeline with the im2col k-blocks
 // of the TMA kind: tile = BM consecutive pixels, k-block = (channel block,
 // tap), one im2col box + one weight box per k-block.
-template <int BM, int BN, int BK, bool ROW>
-__global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
+//
+// STRIP (KM = 2, TP_KIND_IGEMM_TC_STRIP): x and w padded to 8 channels (16-byte
+// pixels); tile = BM pixels of one output row as in ROW; a k-block is a filter
+// row r: one tiled box per column phase f < s_w (element stride s_w) brings
+// the strip of a.strip_px pixels starting at input column q0 s_w - p_w + f.
+// Tap s = f + s_w t of phase f is that strip shifted by t pixels, and ONE MMA
+// (K = 16) covers taps t and t + 1: no-swizzle K-major descriptors with the two
+// core matrices along K 16 B apart (A) and s_w BN 16 B apart (weights laid out
+// [r][s][n][8] in shared memory, loaded once; the s_w zero taps after each
+// row's S taps pair with an odd tap count).
+template <int BM, int BN, int BK, int KM>
+__global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
                                                        const __grid_constant__ CUtensorMap tmY, TcArgs a) {
+  constexpr bool ROW = KM == 1, STRIP = KM == 2;
   static_assert(!ROW || BK == 64, "row-halo k-blocks are 64 channels");
   constexpr int SUBK = BK < 64 ? BK : 64;
   constexpr int NSUB = BK / SUBK;
@@ -636,9 +647,11 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
   constexpr uint32_t A_SUB = BM * SUBK * 2, B_SUB = BN * SUBK * 2;
   constexpr uint32_t A_STRIP = ((BM + 2) * 128 + 1023) / 1024 * 1024;
   constexpr uint32_t B_TAP = BN * 128;
-  constexpr uint32_t A_STAGE = ROW ? A_STRIP : A_SUB * NSUB;
-  constexpr uint32_t B_STAGE = ROW ? 3 * B_TAP : B_SUB * NSUB;
-  constexpr uint32_t A_BYTES = ROW ? (BM + 2) * 128 : A_SUB * NSUB;   // expect_tx of the A part
+  // STRIP: runtime stage size (phase boxes only; the weights are resident)
+  const uint32_t A_STAGE = STRIP ? (uint32_t)a.strip_stage : (ROW ? A_STRIP : A_SUB * NSUB);
+  const uint32_t B_STAGE = STRIP ? 0u : (ROW ? 3 * B_TAP : B_SUB * NSUB);
+  const uint32_t A_BYTES = STRIP ? (uint32_t)(a.sw * a.strip_px * 16)
+                                 : (ROW ? (BM + 2) * 128 : A_SUB * NSUB);   // expect_tx of the A part
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
 
@@ -651,7 +664,10 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;     // [2]
   uint64_t* tempty = tfull + 2;         // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* wfull = tempty + 2;         // STRIP: resident weights landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
+  uint8_t* w_res = smem_raw + a.strip_woff;   // STRIP: [r][S + s_w taps][BN][16 B]
+  const uint32_t w_row = STRIP ? (uint32_t)((a.S + a.sw) * BN * 16) : 0u;
 
   const int tpc = a.tpc;
   const bool split_roles = tpc > 1;     // warps 2..7 drain while warps 0/1 run ahead
@@ -661,7 +677,10 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
   const int nbase = blockIdx.y * BN;
   const int kpt = a.kblocks;            // k-blocks per tile = (C / 64) * 3
   const uint32_t ncols = (uint32_t)(split_roles ? 2 * BN : BN) <= 32 ? 32u : (uint32_t)(split_roles ? 2 * BN : BN);
-  const int n_epi_warps = split_roles ? 6 : (int)(blockDim.x >> 5);
+  // tpc > 1: warps 2.. drain -- 8 of them (two per TMEM lane quadrant) when the
+  // block has 320 threads, else 6 (quadrants 2 and 3 get two warps, 0 and 1 one).
+  const bool epi8 = blockDim.x == 320;
+  const int n_epi_warps = split_roles ? (epi8 ? 8 : 6) : (int)(blockDim.x >> 5);
   unsigned long long* trace =
       a.trace ? a.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
   if (trace && threadIdx.x == 0) {
@@ -677,7 +696,7 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
   // ROW: tile = BM pixels of one output row (q-block t % nqb of row t / nqb);
   // im2col: tile = BM consecutive output pixels m0 = t * BM (rows past M masked).
   auto tile_coords = [&](int t, int& q0, int& p0, int& n0, int& mrow0, int& mvalid) {
-    if constexpr (ROW) {
+    if constexpr (ROW || STRIP) {
       const int qb = t % a.nqb, row = t / a.nqb;
       q0 = qb * BM;
       p0 = row % a.P;
@@ -699,9 +718,20 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
     if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
     for (int i = 0; i < stages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, (uint32_t)n_epi_warps); }
+    mbar_init(wfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+  }
+  if constexpr (STRIP) {
+    // The s_w zero taps after each filter row's S taps (never written by TMA).
+    const int zwords = a.sw * BN;       // 16-byte words of one row's zero taps (s_w x BN x 16 B)
+    for (int i = threadIdx.x; i < a.R * zwords; i += blockDim.x) {
+      const int r = i / zwords, j = i - r * zwords;
+      *reinterpret_cast<uint4*>(w_res + (size_t)r * w_row + (size_t)a.S * BN * 16 + (size_t)j * 16) =
+          make_uint4(0u, 0u, 0u, 0u);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -723,7 +753,14 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
       uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
       uint8_t* sb = b_tiles + (size_t)stage * B_STAGE;
       if (parts & 4) mbar_arrive_expect_tx_p(full + stage, A_BYTES + B_STAGE, lead);
-      if constexpr (ROW) {
+      if constexpr (STRIP) {
+        // filter row r: one strip per column phase (the weights are resident)
+        const uint32_t pb = (uint32_t)a.strip_stage / (uint32_t)a.sw;
+        for (int f = 0; f < a.sw; ++f)
+          if (parts & 1)
+            tma_load_tile_4d_p(sa + f * pb, &tmA, full + stage, 0, q0 * a.sw - a.pw + f, p0 * a.sh - a.ph + r, n0,
+                               lead);
+      } else if constexpr (ROW) {
         // (channel block cb, filter row r): the input strip + the three taps
         if (parts & 1) tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
         if (parts & 2) {
@@ -749,7 +786,9 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
       }
     };
     auto advance = [&](int& cb, int& r, int& sx) {
-      if constexpr (ROW) {
+      if constexpr (STRIP) {
+        ++r;
+      } else if constexpr (ROW) {
         if (++r == 3) { r = 0; ++cb; }
       } else if (++cb == a.cblocks) {
         cb = 0;
@@ -758,7 +797,7 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
     };
     // w_early: the weight boxes of the first tile's first ring pass go out
     // before the PDL wait (weights are layer constants; see TcArgs::w_early).
-    const int npre = (a.w_early && ntl > 0) ? (kpt < stages ? kpt : stages) : 0;
+    const int npre = (!STRIP && a.w_early && ntl > 0) ? (kpt < stages ? kpt : stages) : 0;
     {
       int cb = 0, r = 0, sx = 0;
       for (int kb = 0; kb < npre; ++kb) {
@@ -768,6 +807,11 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if constexpr (STRIP) {
+      // resident weights: one box (8 channels, BN rows, S taps) per filter row
+      mbar_arrive_expect_tx_p(wfull, (uint32_t)(a.R * a.S * BN * 16), lead);
+      for (int r = 0; r < a.R; ++r) tma_load_tile_4d_p(w_res + (size_t)r * w_row, &tmB, wfull, 0, nbase, 0, r, lead);
+    }
     int stage = 0;
     uint32_t phase = 0;
     for (int i = 0; i < ntl; ++i) {
@@ -784,10 +828,15 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
   } else if (warp == 1) {
     // ---------------- MMA issuer: two accumulators, alternating per tile ----------------
     const uint32_t lead = elect_one();
-    const uint64_t adesc0 = make_sdesc(smem_u32(a_tiles), SWZ);
-    const uint64_t bdesc0 = make_sdesc(smem_u32(b_tiles), SWZ);
+    const uint64_t adesc0 = STRIP ? make_sdesc_plain(smem_u32(a_tiles), 16u, 128u) : make_sdesc(smem_u32(a_tiles), SWZ);
+    const uint64_t bdesc0 = STRIP ? make_sdesc_plain(smem_u32(w_res), (uint32_t)(a.sw * BN * 16), 128u)
+                                  : make_sdesc(smem_u32(b_tiles), SWZ);
     int stage = 0;
     uint32_t phase = 0;
+    if constexpr (STRIP) {
+      mbar_wait(wfull, 0);
+      tc_fence_after();
+    }
     for (int i = 0; i < ntl; ++i) {
       const int buf = i & 1;
       if (i >= 2) {
@@ -800,7 +849,18 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
         tc_fence_after();
         const uint64_t ad = adesc0 + ((uint32_t)(stage * A_STAGE) >> 4);
         const uint64_t bd = bdesc0 + ((uint32_t)(stage * B_STAGE) >> 4);
-        if constexpr (ROW) {
+        if constexpr (STRIP) {
+          // filter row kb: per phase f, tap pairs (t, t + 1), t even; tap s = f + s_w t
+          const uint32_t pb = (uint32_t)a.strip_stage / (uint32_t)a.sw;
+          const uint64_t bdr = bdesc0 + ((uint32_t)kb * w_row >> 4);
+          for (int f = 0; f < a.sw; ++f) {
+            const int taps = (a.S - f + a.sw - 1) / a.sw;
+            for (int t = 0; t < taps; t += 2)
+              tc_mma_p(dcol, ad + ((f * pb + (uint32_t)t * 16) >> 4),
+                       bdr + ((uint32_t)(f + a.sw * t) * BN * 16 >> 4), IDESC, (kb > 0 || f > 0 || t > 0) ? 1u : 0u,
+                       lead);
+          }
+        } else if constexpr (ROW) {
 #pragma unroll
           for (int ss = 0; ss < 3; ++ss)
 #pragma unroll
@@ -828,8 +888,8 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
   if (!split_roles || warp >= 2) {
     const int quad = warp & 3;
     int c_begin, c_end;
-    if (split_roles) {               // warps 2..7 -> quadrants 2,3,0,1,2,3
-      const int twin = (quad >= 2) ? 2 : 1;
+    if (split_roles) {               // warps 2..7 -> quadrants 2,3,0,1,2,3 (+ 8,9 -> 0,1 with epi8)
+      const int twin = (epi8 || quad >= 2) ? 2 : 1;
       const int half = (warp >= 6) ? 1 : 0;
       c_begin = half * (BN / twin);
       c_end = c_begin + BN / twin;
@@ -848,12 +908,21 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
     uint8_t* stg = smem_raw + a.recv_off;
     const uint32_t EB = a.out_f32 ? 4u : 2u;
     const uint32_t IB = BN * EB < 128u ? BN * EB : 128u;
+    const uint32_t ystage = (uint32_t)BM * BN * EB;   // bytes of one staged tile
     for (int i = 0; i < ntl; ++i) {
       const int buf = i & 1;
       int q0, p0, n0, mrow0, mvalid;
       tile_coords(tile0 + i, q0, p0, n0, mrow0, mvalid);
-      if (a.y_tma) {   // the previous tile's store must have read the staging buffer
-        if ((int)threadIdx.x == issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      // a.ystage2: two staging buffers alternate, so only the store of tile i - 2
+      // must have read this one (one bulk group may stay in flight)
+      uint8_t* stg_t = stg + (a.ystage2 ? (size_t)buf * ystage : 0);
+      if (a.y_tma) {   // the store that last used this staging buffer must have read it
+        if ((int)threadIdx.x == issuer) {
+          if (a.ystage2)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         asm volatile("bar.sync 2, %0;" ::"r"(n_epi) : "memory");
       }
       float bv[16];
@@ -887,15 +956,35 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
         }
         if (a.y_tma) {
           if (row_ok) {
+            const uint32_t cb = (uint32_t)c * EB, jb = cb / IB, cin = cb % IB;
+            uint8_t* sub = stg_t + (size_t)jb * BM * IB;
+            const uint32_t swm = IB / 16 - 1;
+            if (!a.out_f32) {
+              // bf16: packed bias add (FADD2), one RNE pack per pair, ReLU on the packed pair
+              // (max(rne(x), 0) == rne(max(x, 0)): rounding is monotone and keeps 0).
+              uint32_t pk[8];
+              const __nv_bfloat162 zero2 = __floats2bfloat162_rn(0.0f, 0.0f);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float2 t = __fadd2_rn(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])),
+                                            make_float2(bv[2 * j], bv[2 * j + 1]));
+                __nv_bfloat162 h = __float22bfloat162_rn(t);
+                if (a.relu) h = __hmax2(h, zero2);
+                pk[j] = *reinterpret_cast<uint32_t*>(&h);
+              }
+#pragma unroll
+              for (uint32_t qq = 0; qq < 2; ++qq) {
+                uint32_t off = (uint32_t)row * IB + cin + qq * 16;
+                off ^= ((off >> 7) & swm) << 4;
+                *reinterpret_cast<uint4*>(sub + off) = make_uint4(pk[4 * qq], pk[4 * qq + 1], pk[4 * qq + 2], pk[4 * qq + 3]);
+              }
+            } else {
             float v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const float t = __uint_as_float(raw[j]) + bv[j];
               v[j] = a.relu ? fmaxf(t, 0.0f) : t;
             }
-            const uint32_t cb = (uint32_t)c * EB, jb = cb / IB, cin = cb % IB;
-            uint8_t* sub = stg + (size_t)jb * BM * IB;
-            const uint32_t swm = IB / 16 - 1;
             for (uint32_t qq = 0; qq < EB; ++qq) {   // 16 values = EB 16-byte pieces
               uint32_t off = (uint32_t)row * IB + cin + qq * 16;
               off ^= ((off >> 7) & swm) << 4;
@@ -912,6 +1001,7 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
                                *reinterpret_cast<uint32_t*>(&b2), *reinterpret_cast<uint32_t*>(&b3));
               }
               *reinterpret_cast<uint4*>(sub + off) = u;
+            }
             }
           }
         } else if (row_ok && row < mvalid && nb < a.K) {
@@ -933,13 +1023,13 @@ __global__ void __launch_bounds__(256) igemm_mt_kernel(const __grid_constant__ C
         if ((int)threadIdx.x == issuer) {
           for (uint32_t jb = 0; jb < BN * EB / IB; ++jb) {
             const int ncol = nbase + (int)(jb * (IB / EB));
-            if constexpr (ROW)
+            if constexpr (ROW || STRIP)
               asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                                reinterpret_cast<uint64_t>(&tmY)),
-                           "r"(smem_u32(stg + (size_t)jb * BM * IB)), "r"(ncol), "r"(q0), "r"(n0 * a.P + p0)
+                           "r"(smem_u32(stg_t + (size_t)jb * BM * IB)), "r"(ncol), "r"(q0), "r"(n0 * a.P + p0)
                            : "memory");
             else
-              tma_store_2d(&tmY, stg + (size_t)jb * BM * IB, ncol, mrow0);
+              tma_store_2d(&tmY, stg_t + (size_t)jb * BM * IB, ncol, mrow0);
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
@@ -962,14 +1052,17 @@ using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMa
 
 template <int BM, int BN, int MODE>
 static KernelFn pick_bk(int bk) {
-  if constexpr (MODE == 2) {
-    return bk == 64 ? igemm_mt_kernel<BM, BN, 64, true> : nullptr;
+  if constexpr (MODE == 4) {
+    if constexpr (BN <= 128) return bk == 16 ? igemm_mt_kernel<BM, BN, 16, 2> : nullptr;
+    return nullptr;
+  } else if constexpr (MODE == 2) {
+    return bk == 64 ? igemm_mt_kernel<BM, BN, 64, 1> : nullptr;
   } else if constexpr (MODE == 3) {
     switch (bk) {
-      case 16: return igemm_mt_kernel<BM, BN, 16, false>;
-      case 32: return igemm_mt_kernel<BM, BN, 32, false>;
-      case 64: return igemm_mt_kernel<BM, BN, 64, false>;
-      case 128: return igemm_mt_kernel<BM, BN, 128, false>;
+      case 16: return igemm_mt_kernel<BM, BN, 16, 0>;
+      case 32: return igemm_mt_kernel<BM, BN, 32, 0>;
+      case 64: return igemm_mt_kernel<BM, BN, 64, 0>;
+      case 128: return igemm_mt_kernel<BM, BN, 128, 0>;
     }
   } else {
     switch (bk) {
@@ -985,7 +1078,8 @@ static KernelFn pick_bk(int bk) {
 static KernelFn pick_tc(int bm, int bn, int bk, int mode) {
 #define TP_TC_CASE(M_, N_)                                                                       \
   if (bm == M_ && bn == N_)                                                                      \
-    return mode == 3 ? pick_bk<M_, N_, 3>(bk)                                                    \
+    return mode == 4 ? pick_bk<M_, N_, 4>(bk)                                                    \
+                     : mode == 3 ? pick_bk<M_, N_, 3>(bk)                                        \
                      : (mode == 2 ? pick_bk<M_, N_, 2>(bk)                                       \
                                   : (mode == 1 ? pick_bk<M_, N_, 1>(bk) : pick_bk<M_, N_, 0>(bk)));
   TP_TC_CASE(64, 32) TP_TC_CASE(64, 64) TP_TC_CASE(64, 128) TP_TC_CASE(64, 256)
@@ -1009,6 +1103,113 @@ static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red, b
   size_t off = tc_ring_bytes(bm, bn, bk, stages, row);
   if (cluster_red) off += (size_t)bm * (bn + 4) * 4;
   return (off + 1023) & ~(size_t)1023;
+}
+
+static bool ystage2_enabled() {
+  static const bool on = !(getenv("TP_YSTAGE2") && atoi(getenv("TP_YSTAGE2")) == 0);
+  return on;
+}
+
+static bool mt_epi8() {
+  static const bool on = !(getenv("TP_EPI8") && atoi(getenv("TP_EPI8")) == 0);
+  return on;
+}
+
+// Strip kind (C <= 8 stems): pb.x = x padded to NHWC with 8 channels, pb.w =
+// weights padded and laid out [R][S][K][8] (both written by the pre-pass into the
+// workspace).  A: tiled map (8, W, H, N), box (8, s_w px, 1, 1) with element
+// stride s_w along W (px pixels land), no swizzle; B: tiled map (8, K, S, R),
+// box (8, BN, S, 1) -> shared [s][n][16 B] per filter row.  Shared memory:
+// [ring: stages x s_w phase boxes][resident weights][barriers][y staging].
+static tp_status strip_prepare(const TcProblem& pb, TcPlan* plan) {
+  const DriverApi& drv = driver();
+  const int sw = pb.sw;
+  const int t0 = (pb.S + sw - 1) / sw;
+  const int px = pb.bm + 2 * ((t0 + 1) / 2) - 1;
+  const int phase_bytes = (px * 16 + 127) / 128 * 128;
+  {
+    cuuint64_t dims[4] = {8, (cuuint64_t)pb.W, (cuuint64_t)pb.H, (cuuint64_t)pb.N};
+    cuuint64_t strides[3] = {16, (cuuint64_t)pb.W * 16, (cuuint64_t)pb.H * pb.W * 16};
+    cuuint32_t box[4] = {8, (cuuint32_t)(sw * px), 1, 1};
+    cuuint32_t es[4] = {1, (cuuint32_t)sw, 1, 1};
+    CUresult r = drv.encodeTiled(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.x), dims,
+                                 strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("tensor map (strip A) failed (" + std::to_string((int)r) + ")");
+      return TP_ECUDA;
+    }
+  }
+  {
+    cuuint64_t dims[4] = {8, (cuuint64_t)pb.K, (cuuint64_t)pb.S, (cuuint64_t)pb.R};
+    cuuint64_t strides[3] = {16, (cuuint64_t)pb.K * 16, (cuuint64_t)pb.S * pb.K * 16};
+    cuuint32_t box[4] = {8, (cuuint32_t)pb.bn, (cuuint32_t)pb.S, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = drv.encodeTiled(&plan->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.w), dims,
+                                 strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("tensor map (strip weights) failed (" + std::to_string((int)r) + ")");
+      return TP_ECUDA;
+    }
+  }
+  TcArgs& a = plan->args;
+  std::memset(&a, 0, sizeof(a));
+  a.M = pb.M; a.K = pb.K; a.P = pb.P; a.Q = pb.Q; a.S = pb.S; a.R = pb.R;
+  a.sh = pb.sh; a.sw = pb.sw; a.ph = pb.ph; a.pw = pb.pw;
+  a.bk = 16; a.stages = pb.stages; a.split_k = 1;
+  a.kblocks = pb.R;
+  a.H = pb.H; a.W = pb.W; a.C = 8;
+  a.nqb = (pb.Q + pb.bm - 1) / pb.bm;
+  a.ntiles = pb.N * pb.P * a.nqb;
+  a.tpc = pb.tpc > 1 ? pb.tpc : 1;
+  a.bias = pb.bias; a.y = pb.y; a.out_f32 = pb.out_f32; a.relu = pb.relu; a.has_bias = pb.has_bias;
+  a.trace = pb.trace;
+  a.strip_px = px;
+  a.strip_stage = sw * phase_bytes;
+  const size_t ring = (size_t)pb.stages * a.strip_stage;
+  a.strip_woff = (int)((ring + 1023) / 1024 * 1024);
+  const size_t wbytes = ((size_t)pb.R * (pb.S + sw) * pb.bn * 16 + 1023) / 1024 * 1024;
+  a.bar_off = a.strip_woff + (int)wbytes;
+  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, 16, 4));
+  if (!plan->fn) { set_error("no strip instantiation for this BM x BN"); return TP_EINVALID_CONFIG; }
+  plan->grid = dim3((unsigned)((a.ntiles + a.tpc - 1) / a.tpc), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u);
+  if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
+  plan->block = dim3(a.tpc > 1 && pb.bn >= 128 && mt_epi8() ? 320 : 256);   // + two drain warps (two per quadrant)
+  plan->cluster_z = 1;
+  plan->smem = (size_t)a.bar_off + 1024;
+  // TMA-store epilogue through a staging buffer after the barriers, when it fits
+  // (3-D [N P][Q][K] map as in the row kind: q >= Q is clipped).
+  static const bool no_ytma = getenv("TP_NO_YTMA") && atoi(getenv("TP_NO_YTMA")) != 0;
+  const int eb = pb.out_f32 ? 4 : 2;
+  const int ib = pb.bn * eb < 128 ? pb.bn * eb : 128;
+  const size_t stage_bytes = (size_t)pb.bm * pb.bn * eb;
+  a.y_tma = 0;
+  if (!no_ytma && plan->smem + stage_bytes <= 232448 && ((size_t)pb.K * eb) % 16 == 0) {
+    cuuint64_t dims[3] = {(cuuint64_t)pb.K, (cuuint64_t)pb.Q, (cuuint64_t)pb.N * pb.P};
+    cuuint64_t strides[2] = {(cuuint64_t)pb.K * eb, (cuuint64_t)pb.Q * pb.K * eb};
+    cuuint32_t box[3] = {(cuuint32_t)(ib / eb), (cuuint32_t)pb.bm, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUtensorMapSwizzle swz = ib == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                             : (ib == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+    CUresult ry = drv.encodeTiled(&plan->tmY, pb.out_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                         : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                  3, pb.y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (ry == CUDA_SUCCESS) {
+      a.y_tma = 1;
+      a.recv_off = (int)plan->smem;
+      a.ystage2 = (a.tpc > 1 && ystage2_enabled() && plan->smem + 2 * stage_bytes <= 232448) ? 1 : 0;
+      plan->smem += (a.ystage2 ? 2 : 1) * stage_bytes;
+    }
+  }
+  if (!a.y_tma) std::memset(&plan->tmY, 0, sizeof(plan->tmY));
+  cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    return TP_ECUDA;
+  }
+  return TP_OK;
 }
 
 // 3xTF32 kind: fp32 maps (32-channel boxes = 128-B rows, 128-B swizzle), ring of
@@ -1178,6 +1379,7 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   const DriverApi& drv = driver();
   if (pb.stem) return stem_prepare(pb, plan);
+  if (pb.strip) return strip_prepare(pb, plan);
   const int sub_k = pb.bk < 64 ? pb.bk : 64;
   static const bool no_atile = getenv("TP_NO_ATILE") && atoi(getenv("TP_NO_ATILE")) != 0;
   const bool a_tiled = !pb.gather && !pb.row && !no_atile && pb.R == 1 && pb.S == 1 && pb.sh == 1 && pb.sw == 1 &&
@@ -1326,6 +1528,8 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.dep_wait = 0;
   a.dep_signal = 0;
   a.dep_early = 0;
+  a.ystage2 = 0;
+  a.strip_px = a.strip_stage = a.strip_woff = 0;
   a.a_tiled = a_tiled ? 1 : 0;
   a.y_tma = y_tma;
   plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.mt ? 3 : (pb.row ? 2 : (pb.gather ? 1 : 0))));
@@ -1336,6 +1540,9 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
                              (unsigned)pb.split_k);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
   plan->block = dim3(pb.threads);
+  // Multi-tile kinds with tiles_per_cta > 1: two more drain warps, so each TMEM
+  // lane quadrant has two (the knob stays 256 threads; TP_EPI8=0 turns it off).
+  if ((pb.row || pb.mt) && a.tpc > 1 && pb.threads == 256 && pb.bn >= 128 && mt_epi8()) plan->block = dim3(320);
   // Split-K reduces through DSMEM inside a (1, 1, split_k) cluster when the
   // context can co-schedule such clusters; otherwise (e.g. a green context
   // split without SM co-scheduling) through the global workspace.
@@ -1388,6 +1595,8 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
         a.recv_off = (int)((plan->smem + 1023) / 1024 * 1024);
         plan->smem = (size_t)a.recv_off + stage_bytes;
         if (plan->smem > 232448) { a.y_tma = 0; plan->smem = (size_t)a.tab_off; }
+        // (a second staging buffer for the row / multi-tile im2col kinds was measured slower:
+        //  VGG conv1_2 at 25% 232.7 -> 262.4 us, the extra 16 KiB costs a resident CTA)
       }
     }
   }

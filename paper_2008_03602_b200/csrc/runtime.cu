@@ -344,6 +344,9 @@ struct ConvPlan {
   int kernels_per_call = 1;
   int ctas_per_sm = 1;
   int* dep_ctr = nullptr;   // flag-chain counter in the workspace (tensor-core layers)
+  void* x8 = nullptr;       // strip kind: channel-padded x / w (pre-pass outputs)
+  void* w8 = nullptr;
+  const void* w_user = nullptr;
 };
 
 // Flag chains: launches of the TMA im2col kind inside a
@@ -378,7 +381,7 @@ static cudaError_t launch_plan_chain(const ConvPlan& p, cudaStream_t st, int j) 
 }
 
 struct WsLayout {
-  size_t counters = 0, dep = 0, partials = 0, xbuf = 0, ybuf = 0, total = 0;
+  size_t counters = 0, dep = 0, partials = 0, xbuf = 0, ybuf = 0, x8 = 0, w8 = 0, total = 0;
 };
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -400,6 +403,10 @@ static WsLayout ws_layout(const Layer& L, const tp_schedule& s) {
   if ((s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) && s.split_k > 1) {
     const int64_t tiles = cdiv(L.M, s.bm) * cdiv(L.d.k, s.bn);
     w.partials = off; off = align256(off + (size_t)s.split_k * tiles * s.bm * s.bn * 4);
+  }
+  if (s.kind == TP_KIND_IGEMM_TC_STRIP) {   // channel-padded copies written by the pre-pass
+    w.x8 = off; off = align256(off + (size_t)L.d.n * L.d.h * L.d.w * 16);
+    w.w8 = off; off = align256(off + (size_t)L.d.k * L.d.r * L.d.s * 16);
   }
   if (L.d.in_layout == TP_LAYOUT_NCHW) {
     const int ieb = L.d.dtype == TP_DTYPE_BF16 ? 2 : 4, oeb = L.d.out_dtype == TP_DTYPE_BF16 ? 2 : 4;
@@ -470,6 +477,15 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     pb.mt = s.kind == TP_KIND_IGEMM_TC_MT ? 1 : 0;
     pb.tf32 = s.kind == TP_KIND_IGEMM_TF32X3 ? 1 : 0;
     pb.stem = s.kind == TP_KIND_IGEMM_TC_STEM ? 1 : 0;
+    pb.strip = s.kind == TP_KIND_IGEMM_TC_STRIP ? 1 : 0;
+    if (pb.strip) {
+      plan->x8 = wsb + wl.x8;
+      plan->w8 = wsb + wl.w8;
+      plan->w_user = w;
+      pb.x = plan->x8;
+      pb.w = plan->w8;
+      plan->kernels_per_call += 1;
+    }
     tp_status st = tc_prepare(pb, &plan->tc);
     if (st != TP_OK) return st;
     plan->dep_ctr = reinterpret_cast<int*>(wsb + wl.dep);
@@ -481,7 +497,7 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     {
       static const bool no_slots = getenv("TP_NO_SLOTS") && atoi(getenv("TP_NO_SLOTS")) != 0;
       const bool multi = s.kind == TP_KIND_IGEMM_TC_ROW || s.kind == TP_KIND_IGEMM_TC_MT ||
-                         s.kind == TP_KIND_IGEMM_TC_STEM;
+                         s.kind == TP_KIND_IGEMM_TC_STEM || s.kind == TP_KIND_IGEMM_TC_STRIP;
       const int sms = s.sm_tuned > 0 ? s.sm_tuned : sm_count;
       // Resident CTAs per SM: the occupancy calculator, capped by TMEM (512
       // columns per SM; these kinds allocate two BN-column accumulators) -- a
@@ -511,6 +527,11 @@ static cudaError_t launch_plan(const ConvPlan& p, cudaStream_t st) {
     e = launch_nchw_to_nhwc(p.x_user, p.x_nhwc, p.L.d.n, p.L.d.c, p.L.d.h, p.L.d.w, p.in_eb, st);
     if (e != cudaSuccess) return e;
   }
+  if (p.x8) {
+    e = launch_pad_c8(p.nchw ? p.x_nhwc : p.x_user, p.x8, (int64_t)p.L.d.n * p.L.d.h * p.L.d.w, p.L.d.c, p.w_user,
+                      p.w8, p.L.d.k, p.L.d.r, p.L.d.s, pdl_enabled() ? 1 : 0, st);
+    if (e != cudaSuccess) return e;
+  }
   e = p.s.kind != TP_KIND_DIRECT ? tc_launch(p.tc, st) : direct_launch(p.dp, st);
   if (e != cudaSuccess) return e;
   if (p.nchw) {
@@ -524,7 +545,7 @@ static cudaError_t launch_plan(const ConvPlan& p, cudaStream_t st) {
 static void plan_geometry(const ConvPlan& p, int sm_granted, tp_measurement* m) {
   const dim3 g = p.s.kind != TP_KIND_DIRECT ? p.tc.grid : p.dp.grid;
   m->ctas = (int64_t)g.x * g.y * g.z;
-  m->threads_per_cta = p.s.threads;
+  m->threads_per_cta = p.s.kind != TP_KIND_DIRECT ? (int32_t)p.tc.block.x : p.s.threads;   // as launched
   m->ctas_per_sm = p.ctas_per_sm;
   m->waves = (int32_t)cdiv(m->ctas, (int64_t)sm_granted * std::max(1, p.ctas_per_sm));
   m->kind = p.s.kind;

@@ -230,8 +230,44 @@ static bool valid_stem(const Layer& L, int bm, int bn) {
   return bn <= std::max<int64_t>(32, np2(L.d.k));
 }
 
+// Strip kind for the C <= 8 gathered layers ("strip
+// kind"): x and w are padded to 8 channels (16-byte pixel rows) by a pre-pass
+// inside the call; a tile is BM output pixels of one output row; per filter
+// row r one TMA box per column phase (stride s_w in {1, 2}) brings the input
+// strip, and one MMA covers two taps of a phase: the no-swizzle K-major core
+// matrices of taps t and t + 1 are the strip and the strip one pixel (16 B)
+// later (LBO = 16 B).  Weights stay resident; two TMEM accumulators.
+bool strip_kind_eligible(const Layer& L) {
+  const tp_conv_desc& d = L.d;
+  return L.kind == TP_KIND_IGEMM_TC_GATHER && d.c <= 8 && (d.stride_w == 1 || d.stride_w == 2) && d.s <= 8 &&
+         d.r <= 8;
+}
+static const int kStripBM[] = {64, 128};
+static const int kStripBN[] = {32, 64, 128};
+static const int kStripStages[] = {2, 4, 6};
+static const int kStripTpc[] = {1, 2, 4, 8, 16};
+// Pixels of one phase box: BM + 2 ceil(T0 / 2) - 1 with T0 = ceil(S / s_w) taps
+// in phase 0 (the MMA of the last tap pair reads one row past an odd tap count).
+int64_t strip_box_px(const Layer& L, int bm) {
+  const int64_t t0 = cdiv(L.d.s, L.d.stride_w);
+  return bm + 2 * cdiv(t0, 2) - 1;
+}
+int64_t strip_stage_bytes(const Layer& L, int bm) {
+  return (int64_t)L.d.stride_w * cdiv(strip_box_px(L, bm) * 16, 128) * 128;
+}
+// Resident weights: per filter row, S taps + s_w zero taps of BN x 16 B.
+int64_t strip_weight_bytes(const Layer& L, int bn) {
+  return cdiv((int64_t)L.d.r * (L.d.s + L.d.stride_w) * bn * 16, 1024) * 1024;
+}
+static bool valid_strip(const Layer& L, int bm, int bn, int stages) {
+  if (bm > std::max<int64_t>(64, np2(L.Q))) return false;
+  if (bn > std::max<int64_t>(32, np2(L.d.k))) return false;
+  if ((int64_t)L.d.stride_w * strip_box_px(L, bm) > 256) return false;   // TMA box extent
+  return (int64_t)stages * strip_stage_bytes(L, bm) + strip_weight_bytes(L, bn) + 1024 <= kSmemLimit;
+}
+
 void fill_geometry(const Layer& L, tp_schedule* s) {
-  if (s->kind == TP_KIND_IGEMM_TC_STEM) {
+  if (s->kind == TP_KIND_IGEMM_TC_STEM || s->kind == TP_KIND_IGEMM_TC_STRIP) {
     s->grid_x = (int32_t)cdiv((int64_t)L.d.n * L.P * cdiv(L.Q, s->bm), std::max(1, s->tiles_per_cta));
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = 1;
@@ -288,6 +324,15 @@ static void enumerate(const Layer& L, F visit) {
         if (!valid_stem(L, bm, bn)) continue;
         tp_schedule s; std::memset(&s, 0, sizeof(s));
         s.kind = TP_KIND_IGEMM_TC_STEM; s.bm = bm; s.bn = bn; s.bk = (int32_t)stem_kp(L); s.stages = 2;
+        s.threads = 256; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
+        if (!visit(s)) return;
+      }
+    // ... then the strip kind.
+    if (strip_kind_eligible(L))
+      for (int bm : kStripBM) for (int bn : kStripBN) for (int st : kStripStages) for (int tpc : kStripTpc) {
+        if (!valid_strip(L, bm, bn, st)) continue;
+        tp_schedule s; std::memset(&s, 0, sizeof(s));
+        s.kind = TP_KIND_IGEMM_TC_STRIP; s.bm = bm; s.bn = bn; s.bk = 16; s.stages = st;
         s.threads = 256; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
         if (!visit(s)) return;
       }
@@ -360,6 +405,10 @@ bool schedule_in_space(const Layer& L, const tp_schedule& s) {
     return stem_kind_eligible(L) && in_(s.bm, kStemBM, 2) && in_(s.bn, kStemBN, 3) && s.bk == stem_kp(L) &&
            s.stages == 2 && s.threads == 256 && s.split_k == 1 && in_(s.tiles_per_cta, kStemTpc, 4) &&
            valid_stem(L, s.bm, s.bn);
+  if (s.kind == TP_KIND_IGEMM_TC_STRIP)
+    return strip_kind_eligible(L) && in_(s.bm, kStripBM, 2) && in_(s.bn, kStripBN, 3) && s.bk == 16 &&
+           in_(s.stages, kStripStages, 3) && s.threads == 256 && s.split_k == 1 &&
+           in_(s.tiles_per_cta, kStripTpc, 5) && valid_strip(L, s.bm, s.bn, s.stages);
   if (s.kind == TP_KIND_IGEMM_TF32X3)
     return tf32_kind_eligible(L) && in_(s.bm, kTcBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 32 &&
            in_(s.stages, kTf32Stages, 3) && s.threads == 256 && in_(s.split_k, kTcSplit, 4) &&

@@ -224,6 +224,18 @@ static __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t s
   return d;
 }
 
+// No-swizzle K-major descriptor (canonical layout ((8, m), (8, 2k)) of 8-row x
+// 16-byte core matrices): LBO = byte distance between the two core matrices
+// along K, SBO = byte distance between 8-row groups along M / N.  The strip
+// kind sets LBO = 16 B on A (tap t + 1 = the strip one pixel later).
+static __device__ __forceinline__ uint64_t make_sdesc_plain(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;   // layout type 0 (no swizzle) at [61, 64)
+  return d;
+}
+
 // Store 16 consecutive output channels [n0, n0+16) of row m.
 static __device__ __forceinline__ void store16(void* y, int64_t m, int K, int n0, const float (&v)[16], int out_f32) {
   if (out_f32) {

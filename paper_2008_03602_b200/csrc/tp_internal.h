@@ -39,6 +39,10 @@ bool row_kind_eligible(const Layer& L);                     // row-halo kind app
 bool mt_kind_eligible(const Layer& L);                      // multi-tile im2col kind applies
 bool tf32_kind_eligible(const Layer& L);
 bool stem_kind_eligible(const Layer& L);                    // stem kind applies (C < 8 gathered layers)
+bool strip_kind_eligible(const Layer& L);                   // strip kind applies (C <= 8 gathered layers)
+int64_t strip_box_px(const Layer& L, int bm);               // strip kind: pixels per phase box
+int64_t strip_stage_bytes(const Layer& L, int bm);          // strip kind: one ring stage (all phase boxes)
+int64_t strip_weight_bytes(const Layer& L, int bn);         // strip kind: resident weights
 int64_t stem_kp(const Layer& L);                            // stem kind: reduction padded to 64 (R S C)
 int64_t stem_patch_bytes(const Layer& L, int bm);                    // 3xTF32 tensor-core kind applies (fp32 dense)
 int64_t tf32_smem_bytes(int bm, int bn, int stages, int split);

@@ -96,6 +96,10 @@ struct TcArgs {
   int dep_wait;
   int dep_signal;
   int dep_early;               // flag chain: trigger the dependent launch at kernel entry
+  int strip_px;                // strip kind: 16-byte pixels per phase box
+  int strip_stage;             // strip kind: bytes of one ring stage (s_w phase boxes)
+  int strip_woff;              // strip kind: byte offset of the resident weights
+  int ystage2;                 // multi-tile kinds: two y staging buffers (TMA-store epilogue)
 };
 
 struct TcProblem {
@@ -117,6 +121,7 @@ struct TcProblem {
   int mt;          // 1: TP_KIND_IGEMM_TC_MT (im2col multi-tile)
   int tf32;        // 1: TP_KIND_IGEMM_TF32X3 (fp32 NHWC x, KRSC w; 3xTF32 split)
   int stem;        // 1: TP_KIND_IGEMM_TC_STEM (C < 8 stems: staged input patch, resident weights)
+  int strip;       // 1: TP_KIND_IGEMM_TC_STRIP (x, w padded to 8 channels in the workspace)
 };
 
 struct TcPlan {
@@ -173,6 +178,8 @@ cudaError_t launch_gather(const void* y, int layout_nhwc, int out_f32, int N, in
 cudaError_t launch_smid_probe(int ctas, int* smids, cudaStream_t st);
 cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int grid, cudaStream_t st);
 cudaError_t launch_l2_flush(void* buf, size_t bytes, int grid, cudaStream_t st);
+cudaError_t launch_pad_c8(const void* x, void* x8, int64_t npix, int C, const void* w, void* w8, int K, int R, int S,
+                          int pdl, cudaStream_t st);
 cudaError_t launch_empty_chain(int ctas, int threads, int* ctr, int wait, cudaStream_t st);
 cudaError_t launch_empty(int ctas, int threads, int pdl, cudaStream_t st);
 

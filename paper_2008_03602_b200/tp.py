@@ -27,7 +27,8 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 OK, EINVAL, EINVALID_CONFIG, ECAPACITY, ECUDA, EMISMATCH, EUNSUPPORTED = range(7)
-KIND_IGEMM_TC, KIND_DIRECT, KIND_IGEMM_TC_GATHER, KIND_IGEMM_TC_ROW, KIND_IGEMM_TC_MT, KIND_IGEMM_TF32X3, KIND_IGEMM_TC_STEM = 0, 1, 2, 3, 4, 5, 6
+(KIND_IGEMM_TC, KIND_DIRECT, KIND_IGEMM_TC_GATHER, KIND_IGEMM_TC_ROW, KIND_IGEMM_TC_MT, KIND_IGEMM_TF32X3,
+ KIND_IGEMM_TC_STEM, KIND_IGEMM_TC_STRIP) = range(8)
 NHWC, NCHW = 0, 1
 BF16, FP32 = 0, 1
 PART_FINE_GRAINED = 1

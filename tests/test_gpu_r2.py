@@ -431,3 +431,79 @@ def test_chain_run_mixed_kinds_and_timed_layer_counter_zeroed():
     m = tp.conv2d_run(b3_, k3[tp.KIND_IGEMM_TC][0], timing_cfg=tp.timing())
     torch.cuda.synchronize()
     assert m["status"] == 0 and int(b3_.ws.view(torch.int32).abs().sum()) == 0
+
+
+# ------------------------------------------------------------------ strip kind (C <= 8 stems, padded strips)
+STRIP_TINY = [mk(2, 3, 10, 70, 64, 3, 3, 1, 1, out=tp.FP32, epi=1),      # VGG conv1_1-like, 2 images
+              mk(1, 3, 23, 140, 64, 7, 7, 2, 3, out=tp.FP32, epi=1),     # R50 conv1-like (7x7 s2 p3)
+              mk(1, 3, 9, 132, 32, 3, 3, 2, 1, out=tp.FP32, epi=1),      # MobileNetV2 conv0-like (3x3 s2)
+              mk(1, 5, 6, 80, 40, 3, 3, 1, 1, out=tp.FP32, epi=1),       # C = 5, ragged N tile
+              mk(1, 3, 12, 20, 16, 3, 3, 1, 1, out=tp.FP32, epi=3),      # Q = 20 < BM, K = 16 < BN
+              mk(2, 4, 11, 37, 24, 5, 5, 2, 2, out=tp.FP32, epi=1),      # 5x5 s2 p2, odd W
+              mk(1, 6, 7, 30, 8, 3, 3, 1, 0, out=tp.FP32, epi=1),        # C = 6, pad 0, K = 8
+              mk(1, 3, 16, 64, 64, 3, 3, 1, 1, epi=3)]                   # bf16 output
+
+
+def _strip_scheds(d):
+    out = [s for s in (tp.space_get(d, i) for i in range(tp.space_size(d))) if s["kind"] == tp.KIND_IGEMM_TC_STRIP]
+    assert out, "layer has no strip schedules"
+    return out
+
+
+@pytest.mark.parametrize("d", STRIP_TINY, ids=lambda d: f"strip_{d['c']}x{d['h']}x{d['w']}_k{d['k']}_r{d['r']}s{d['stride_h']}_o{d['out_dtype']}")
+def test_strip_every_schedule_bit_exact_integer(d):
+    """O11 for the strip kind: every schedule (ragged last tile of each row,
+    zero-padded borders, both column phases of stride 2, odd tap counts paired
+    with the zero taps, several images, every tiles_per_cta) equals the oracle
+    bit for bit (within one bf16 rounding for bf16 output)."""
+    x, w, b = datagen.make_inputs(d, 71, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    bad = []
+    for s in _strip_scheds(d):
+        buf.poison()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        y = buf.output()
+        ok = np.array_equal(y, ref) if d["out_dtype"] == tp.FP32 else rel_err(y, ref) <= 2 ** -8
+        if not ok:
+            bad.append((s["space_index"], s["bm"], s["bn"], s["stages"], s["tiles_per_cta"]))
+    assert not bad, f"{len(bad)} strip schedules differ, first: {bad[:5]}"
+
+
+@pytest.mark.parametrize("sm_tuned", [1, 3, 7])
+def test_strip_balanced_spans_and_timed_bit_exact(sm_tuned):
+    """Multi-tile strip schedules frozen at a few SMs (ragged balanced spans),
+    timed (the last timed launch leaves y), in a 25% partition."""
+    d = STRIP_TINY[1]
+    part = tp.Partition.get(0.25)
+    x, w, b = datagen.make_inputs(d, 73, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b, part=part)
+    bad = []
+    for s in _strip_scheds(d):
+        if s["tiles_per_cta"] < 2:
+            continue
+        s = dict(s, sm_tuned=sm_tuned)
+        buf.poison()
+        m = tp.conv2d_run(buf, s, part, tp.timing(warmup=1, groups=1, n_min=2, target_group_us=1.0))
+        part.sync()
+        if m["status"] != 0 or not np.array_equal(buf.output(), ref):
+            bad.append((s["space_index"], s["tiles_per_cta"]))
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("cat,li,cfg", [("resnet50", 0, 2), ("mobilenetv2", 0, 5), ("vgg19_b16", 0, 4)],
+                         ids=["r50_conv1", "mbv2_conv0", "vgg_conv1_1"])
+def test_strip_full_size_vs_oracle(cat, li, cfg):
+    layers = wl.catalog(cat)
+    d = layers[li]
+    x, w, b = datagen.make_inputs(d, datagen.data_seed(cfg, li))
+    idx, ref = refs.load(cat, cfg, layers)[li]
+    buf = tp.LayerBuffers(d, x, w, b)
+    for s in _strip_scheds(d):
+        buf.y.fill_(0xFF)
+        torch.cuda.synchronize()
+        tp.conv2d_run(buf, s)
+        torch.cuda.synchronize()
+        assert rel_err(buf.gather(idx), ref) <= 2e-2, s

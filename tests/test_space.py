@@ -60,7 +60,8 @@ def test_direct_smem_depthwise_hand():
 
 
 def test_mobilenetv2_space_totals():
-    # Mirror totals with reading C25: direct 3628 + IGEMM_TC 6148 + gathered 48 + stem 8 = 9832;
+    # Mirror totals with reading C25: direct 3628 + IGEMM_TC 6148 + gathered 48 + stem 8 (+ 15 strip) = 9832
+    # base + appended kinds;
     # the SURVEY 8(a) a2 count (10,180, stem on the direct kind) clamps the depthwise channel tile at C
     # and so admits 20 more direct schedules: 9776 + 384 (stem's direct space) = 10,160 here.
     cat = wl.catalog("mobilenetv2")
@@ -69,7 +70,7 @@ def test_mobilenetv2_space_totals():
         for x in sp.enumerate_space(d):
             kinds[x["kind"]] = kinds.get(x["kind"], 0) + 1
     assert kinds == {sp.KIND_DIRECT: 3628, sp.KIND_IGEMM_TC: 6148, sp.KIND_IGEMM_TC_GATHER: 48,
-                     sp.KIND_IGEMM_TC_STEM: 8}
+                     sp.KIND_IGEMM_TC_STEM: 8, sp.KIND_IGEMM_TC_STRIP: 15}
     stem = [d for d in cat if sp.layer_kind(d) == sp.KIND_IGEMM_TC_GATHER]
     assert len(stem) == 1 and kinds[sp.KIND_DIRECT] + kinds[sp.KIND_IGEMM_TC] + _direct_count(stem[0]) == 10160
 
@@ -129,11 +130,12 @@ def test_stem_kind_hand_count():
     # BN <= max(32, np2(64)) -> {32, 64}; tiles_per_cta {2, 4, 8, 16}; the largest smem
     # (BM=128, BN=64) = 64*192*2 + 2*128*192*2 + 2 ceil(7*786*2/1024) KiB + 1 KiB (k table) + 128*64*4
     # (output staging) + 1024 = 24576 + 98304 + 22528 + 1024 + 32768 + 1024 = 180224 fits: 2 x 2 x 4 = 16,
-    # appended after the gathered tuples.
+    # appended right after the gathered tuples (the strip kind follows).
     d = wl.catalog("resnet50")[0]
     sps = sp.enumerate_space(d)
     st = [s for s in sps if s["kind"] == sp.KIND_IGEMM_TC_STEM]
-    assert len(st) == 16 and sps[-16:] == st and all(s["bk"] == 192 for s in st)
+    g = [s for s in sps if s["kind"] == sp.KIND_IGEMM_TC_GATHER]
+    assert len(st) == 16 and sps[len(g):len(g) + 16] == st and all(s["bk"] == 192 for s in st)
     x = [s for s in st if s["bm"] == 64 and s["bn"] == 32 and s["tiles_per_cta"] == 8][0]
     assert (x["grid_x"], x["grid_y"], x["grid_z"]) == (-(-(112 * 2) // 8), 2, 1)
     # VGG conv1_1 (C=3, 3x3 s1, Q=224, b16): KP = 64; eligible; MobileNetV2 conv0 (3x3 s2, Q=112): eligible
@@ -144,6 +146,30 @@ def test_stem_kind_hand_count():
     assert not sp.stem_eligible(wl.catalog("resnet50")[1])
     assert not sp.stem_eligible(dict(v, h=32, w=32))
     assert not sp.stem_eligible(dict(v, c=6, r=7, s=7))
+
+
+def test_strip_kind_hand_count():
+    # Strip kind, appended after the stem tuples.  Phase-box pixels:
+    # BM + 2 ceil(ceil(S / s_w) / 2) - 1; s_w x that <= 256 (TMA box extent).
+    # R50 conv1 (7x7 s2, K = 64, Q = 112): 4 taps in phase 0 -> BM + 3 px; BM = 128 -> 2 x 131 = 262 > 256,
+    #   so BM = 64 only (2 x 67 = 134); BN {32, 64}; stages {2, 4, 6}; tiles_per_cta {1, 2, 4, 8, 16}:
+    #   smem <= 6 x 2 x 1152 + 7 x 9 x 64 x 16 (64512 -> 63 KiB) + 1 KiB fits -> 1 x 2 x 3 x 5 = 30.
+    # VGG conv1_1 (3x3 s1, K = 64): BM + 3 px <= 256 for both BM -> 2 x 2 x 3 x 5 = 60.
+    # MobileNetV2 conv0 (3x3 s2, K = 32): phase 0 has 2 taps -> BM + 1 px; BM = 128 -> 258 > 256 -> 15.
+    for cat, n, bms in (("resnet50", 30, {64}), ("vgg19_b16", 60, {64, 128}), ("mobilenetv2", 15, {64})):
+        d = wl.catalog(cat)[0]
+        space = sp.enumerate_space(d)
+        st = [x for x in space if x["kind"] == sp.KIND_IGEMM_TC_STRIP]
+        assert len(st) == n and {x["bm"] for x in st} == bms and all(x["bk"] == 16 for x in st)
+        last_stem = max(i for i, x in enumerate(space) if x["kind"] == sp.KIND_IGEMM_TC_STEM)
+        assert space[last_stem + 1:last_stem + 1 + n] == st
+    x = [s for s in sp.enumerate_space(wl.catalog("resnet50")[0]) if s["kind"] == sp.KIND_IGEMM_TC_STRIP
+         and s["bn"] == 64 and s["tiles_per_cta"] == 4][0]
+    assert (x["grid_x"], x["grid_y"], x["grid_z"]) == (-(-(112 * 2) // 4), 1, 1)
+    # not eligible: C % 8 == 0 layers, stride 3 columns, filters wider than 8
+    v = wl.catalog("vgg19_b16")[0]
+    assert not sp.strip_eligible(wl.catalog("resnet50")[1])
+    assert not sp.strip_eligible(dict(v, stride_w=3)) and not sp.strip_eligible(dict(v, s=9, pad_w=4))
 
 
 def test_row_kind_hand_count_and_order():
@@ -248,7 +274,7 @@ def test_libtp_space_matches_mirror(d):
         assert s["kind"] == m["kind"]
         for f in (fields_dir if m["kind"] == sp.KIND_DIRECT else fields_tc + ("kind",)):
             assert s[f] == m[f], (f, m)
-        if m["kind"] in (sp.KIND_IGEMM_TC_ROW, sp.KIND_IGEMM_TC_MT):
+        if m["kind"] in (sp.KIND_IGEMM_TC_ROW, sp.KIND_IGEMM_TC_MT, sp.KIND_IGEMM_TC_STEM, sp.KIND_IGEMM_TC_STRIP):
             f = "tiles_per_cta"
             assert s[f] == m[f], (f, m)
         assert (s["grid_x"], s["grid_y"], s["grid_z"]) == (m["grid_x"], m["grid_y"], m["grid_z"])
