@@ -306,17 +306,15 @@ tp_status tp_cross_eval(const tp_conv_desc* d, const tp_schedule* tuned_at_p, tp
                         size_t ws_bytes, const tp_timing* timing, tp_measurement* out);
 
 /* Model-level run (reading C21): layers 0..n-1 run in order
- * inside `part` -- layer i+1 starts its reads only after layer i's outputs are
- * complete -- `reps` times back to back, captured as ONE CUDA graph.  Ordering
- * is a flag chain where both neighbours are TMA im2col launches (a global
- * arrival counter, acquire/release at gpu scope) and grid
- * completion (PDL griddepcontrol.wait) elsewhere, so layer i+1 may read layer
- * i's y (x[i+1] == y[i]).  Per-layer arrays of length n: descs, scheds (any
- * schedule of each layer's space), device pointers x, w, bias (may be NULL),
- * y, ws and ws_bytes as for tp_conv2d_run.  timing == NULL and out == NULL:
- * one asynchronous replay.  Otherwise warmup replays, then `groups` timed
- * replays; out->median_us = per-sequence latency (group time / reps),
- * n_per_group = reps.  Errors: as tp_conv2d_run for any layer. */
+ * inside `part` -- each launch waits for its predecessor's completion
+ * (programmatic dependent launch), so layer i+1 may read layer i's y
+ * (x[i+1] == y[i]) -- `reps` times back to back, captured as ONE CUDA graph.
+ * Per-layer arrays of length n: descs, scheds (any schedule of each layer's
+ * space), device pointers x, w, bias (may be NULL), y, ws and ws_bytes as for
+ * tp_conv2d_run.  timing == NULL and out == NULL: one asynchronous replay.
+ * Otherwise warmup replays, then `groups` timed replays; out->median_us =
+ * per-sequence latency (group time / reps), n_per_group = reps.  Errors: as
+ * tp_conv2d_run for any layer. */
 tp_status tp_chain_run(int32_t n_layers, const tp_conv_desc* descs, const tp_schedule* scheds, tp_partition* part,
                        const void* const* x, const void* const* w, const void* const* bias, void* const* y,
                        void* const* ws, const size_t* ws_bytes, int32_t reps, const tp_timing* timing,

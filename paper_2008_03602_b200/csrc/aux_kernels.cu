@@ -206,41 +206,6 @@ cudaError_t launch_pad_c8(const void* x, void* x8, int64_t npix, int C, const vo
                             npix, C, reinterpret_cast<const uint16_t*>(w), reinterpret_cast<uint4*>(w8), K, R, S);
 }
 
-// The empty kernel as a link of a flag chain (TcArgs::dep_*): wait for the
-// earlier launches' arrivals (acquire), let the next launch in, arrive (release).
-__global__ void empty_chain_kernel(int* ctr, int wait, int early) {
-  if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (threadIdx.x == 0) {
-    if (wait > 0) {
-      int v;
-      for (;;) {
-        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-        if (v >= wait) break;
-        __nanosleep(32);
-      }
-    } else {
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-    }
-  }
-  __syncthreads();
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ctr) : "memory");
-}
-
-cudaError_t launch_empty_chain(int ctas, int threads, int* ctr, int wait, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(threads);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  static const int early = getenv("TP_CHAIN_EARLY") ? atoi(getenv("TP_CHAIN_EARLY")) : 0;
-  return cudaLaunchKernelEx(&cfg, empty_chain_kernel, ctr, wait, early);
-}
-
 cudaError_t launch_empty(int ctas, int threads, int pdl, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctas);

@@ -79,7 +79,6 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   unsigned long long* trace =
       a.trace ? a.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * kTraceSlots
               : nullptr;
-  if (a.dep_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // Entry stamps stay in registers until the prologue is done: a global store
   // here would make the release fence below wait for it.
   unsigned long long tr_entry = 0, tr_gt = 0;
@@ -243,10 +242,8 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
     trace[60] = (unsigned long long)a.cluster_red;
   }
   // Every warp sleeps in the PDL wait rather than spinning on an mbarrier while
-  // the previous grid may still run on this SM (co-resident CTAs).  In a flag
-  // chain only the TMA producers wait (on the arrival counter): no other warp
-  // touches memory the predecessors write.
-  if (GATHER || a.dep_wait == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the previous grid may still run on this SM (co-resident CTAs).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (GATHER && warp != 1) {
     // ---------------- gather producers (all warps but the MMA warp) ----------------
@@ -333,12 +330,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   } else if (is_prod) {
     // ---------------- TMA producers: k-blocks j = prank (mod nprod), one elected lane each ----------------
     const uint32_t lead = elect_one();
-    if (a.dep_wait > 0) {
-      if (lead) dep_wait_acquire(a.dep_ctr, a.dep_wait);
-      __syncwarp();
-    } else {
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // Every operand this grid reads is now final: the next kernel in the
     // stream may be scheduled (programmatic dependent launch).
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -473,11 +465,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
           float t = __uint_as_float(raw[i]) + bv[i];
           v[i] = a.relu ? fmaxf(t, 0.0f) : t;
         }
-        if (a.dbg & 4) {   // experiments only: no y stores
-          if (v[0] == 12345.0f) store16(a.y, m, a.K, nb, v, a.out_f32);
-        } else {
-          store16(a.y, m, a.K, nb, v, a.out_f32);
-        }
+        store16(a.y, m, a.K, nb, v, a.out_f32);
       }
     } else if (a.cluster_red) {
       // Row segment -> the owner CTA's receive slot [split][row - owner_r0]:
@@ -521,7 +509,6 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       for (int j = 0; j < BN * EB / IB; ++j)
         tma_store_2d(&tmY, smem_raw + (size_t)j * BM * IB, nbase + j * (IB / EB), m0);
       tma_store_commit_wait();
-      if (a.dep_signal) tma_store_wait_all();   // the writes, not only the smem reads
     }
   }
   if (a.split_k > 1 && a.cluster_red) {
@@ -602,7 +589,6 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   tc_fence_before();
   __syncthreads();
   if (trace && threadIdx.x == 0) trace[3] = gtimer();
-  if (a.dep_signal && threadIdx.x == 0) dep_signal_release(a.dep_ctr);
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
@@ -1524,10 +1510,6 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     a.nprod = nprod_env < 1 ? 1 : nprod_env;   // producer warps cap (experiments: TP_NPROD)
   }
   a.w_early = 0;   // set per launch sequence by the runtime (time_plan / tuner phase B)
-  a.dep_ctr = nullptr;   // flag chain: set per launch by the runtime (timing graphs)
-  a.dep_wait = 0;
-  a.dep_signal = 0;
-  a.dep_early = 0;
   a.ystage2 = 0;
   a.strip_px = a.strip_stage = a.strip_woff = 0;
   a.a_tiled = a_tiled ? 1 : 0;

@@ -343,45 +343,14 @@ struct ConvPlan {
   int in_eb = 2, out_eb = 2;
   int kernels_per_call = 1;
   int ctas_per_sm = 1;
-  int* dep_ctr = nullptr;   // flag-chain counter in the workspace (tensor-core layers)
   void* x8 = nullptr;       // strip kind: channel-padded x / w (pre-pass outputs)
   void* w8 = nullptr;
   const void* w_user = nullptr;
 };
 
-// Flag chains: launches of the TMA im2col kind inside a
-// timed launch chain are ordered by a global arrival counter instead of grid
-// completion (TP_FLAGCHAIN=0 turns it off).  Only kinds whose every read of a
-// predecessor's output goes through TMA (L2, async proxy) take part.
-static bool flag_chain_enabled() {
-  // Off by default: measured slower than PDL grid completion (R50 b1 model sum
-  // 206.9 -> 225.3 us, empty-kernel link 0.96 -> 1.43 us).
-  static const bool on = pdl_enabled() && getenv("TP_FLAGCHAIN") && atoi(getenv("TP_FLAGCHAIN")) != 0;
-  return on;
-}
-static bool chain_capable(const ConvPlan& p) {
-  return flag_chain_enabled() && p.dep_ctr && !p.nchw && p.s.kind == TP_KIND_IGEMM_TC;
-}
-static cudaError_t launch_plan(const ConvPlan& p, cudaStream_t st);
-// Launch j (0-based) of a flag chain of this plan: j = 0 waits for its
-// predecessor with griddepcontrol.wait as usual; j > 0 waits until the j
-// earlier launches' CTAs have all arrived.  Every launch arrives once per CTA.
-static int plan_ctas(const ConvPlan& p) { return (int)(p.tc.grid.x * p.tc.grid.y * p.tc.grid.z); }
-static cudaError_t launch_plan_signal(const ConvPlan& p, cudaStream_t st, int wait_target) {
-  ConvPlan q = p;
-  q.tc.args.dep_ctr = p.dep_ctr;
-  q.tc.args.dep_signal = 1;
-  q.tc.args.dep_wait = wait_target;
-  static const int early = getenv("TP_CHAIN_EARLY") ? atoi(getenv("TP_CHAIN_EARLY")) : 0;
-  q.tc.args.dep_early = early;
-  return launch_plan(q, st);
-}
-static cudaError_t launch_plan_chain(const ConvPlan& p, cudaStream_t st, int j) {
-  return launch_plan_signal(p, st, j * plan_ctas(p));
-}
 
 struct WsLayout {
-  size_t counters = 0, dep = 0, partials = 0, xbuf = 0, ybuf = 0, x8 = 0, w8 = 0, total = 0;
+  size_t counters = 0, partials = 0, xbuf = 0, ybuf = 0, x8 = 0, w8 = 0, total = 0;
 };
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -396,9 +365,6 @@ static WsLayout ws_layout(const Layer& L, const tp_schedule& s) {
   if (L.kind != TP_KIND_DIRECT) {
     const int64_t max_tiles = cdiv(L.M, 64) * cdiv(L.d.k, 32);
     w.counters = off; off = align256(off + (size_t)max_tiles * 4);
-    // flag-chain arrival counter of timed launch chains (TcArgs::dep_ctr), also
-    // at a schedule-independent offset; zero between calls
-    w.dep = off; off = align256(off + 4);
   }
   if ((s.kind == TP_KIND_IGEMM_TC || s.kind == TP_KIND_IGEMM_TC_GATHER) && s.split_k > 1) {
     const int64_t tiles = cdiv(L.M, s.bm) * cdiv(L.d.k, s.bn);
@@ -488,7 +454,6 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     }
     tp_status st = tc_prepare(pb, &plan->tc);
     if (st != TP_OK) return st;
-    plan->dep_ctr = reinterpret_cast<int*>(wsb + wl.dep);
     plan->ctas_per_sm = tc_occupancy(plan->tc);
     // Multi-tile kinds: when the frozen grid has more CTA columns than the
     // tuned partition holds at once, the resident CTAs take balanced tile spans
@@ -584,10 +549,8 @@ struct TunerScratch {
   int64_t* g_idx = nullptr;    // gate check-point indices / values (reused: cudaMalloc and
   double* g_vals = nullptr;    // cudaFree per call cost up to 100s of ms on some hosts)
   size_t g_cap = 0;
-  int* dep = nullptr;          // flag-chain counter of the floor measurement
   EventPool pa, pb;
   ~TunerScratch() {
-    if (dep) cudaFree(dep);
     if (d) cudaFree(d);
     if (h) cudaFreeHost(h);
     if (g_idx) cudaFree(g_idx);
@@ -602,18 +565,15 @@ static TunerScratch& scratch_of(tp_partition* p) {
 
 // Caller holds the partition lock and has its context current.
 // `launch(st)` enqueues one call (kpc kernels) on st.
-// `launch(st, seq)`: seq = -1 a standalone launch; seq >= 0 its position in a
-// captured group.  chain_ctr != nullptr: the group is a flag chain whose
-// counter is reset before every group (outside the timed events) and after.
 template <class Launch>
 static tp_status time_launches(tp_partition* part, Launch launch, int kpc, const tp_timing& tm, EventPool& pool,
-                               tp_measurement* out, int* chain_ctr = nullptr) {
+                               tp_measurement* out) {
   cudaStream_t st = part->stream;
   const bool cold = tm.flush_l2 != 0;
   auto flush = [&]() { return launch_l2_flush(part->flush_buf, part->flush_bytes, 148 * 4, st); };
   for (int i = 0; i < std::max(0, tm.warmup); ++i) {
     if (cold) TP_CK(flush());
-    TP_CK(launch(st, -1));
+    TP_CK(launch(st));
   }
   const int groups = std::max(1, tm.groups);
   std::vector<double> per;   // per-launch microseconds, one entry per group
@@ -625,7 +585,7 @@ static tp_status time_launches(tp_partition* part, Launch launch, int kpc, const
       for (int i = 0; i < n; ++i) {
         TP_CK(flush());
         TP_CK(cudaEventRecord(pool.ev[2 * (g * n + i)], st));
-        TP_CK(launch(st, -1));
+        TP_CK(launch(st));
         TP_CK(cudaEventRecord(pool.ev[2 * (g * n + i) + 1], st));
       }
     TP_CK(cudaStreamSynchronize(st));
@@ -644,7 +604,7 @@ static tp_status time_launches(tp_partition* part, Launch launch, int kpc, const
     TP_CK(pool.ensure(2 * (size_t)groups + 2));
     const int n0 = std::max(1, tm.n_min);
     TP_CK(cudaEventRecord(pool.ev[0], st));
-    for (int i = 0; i < n0; ++i) TP_CK(launch(st, -1));
+    for (int i = 0; i < n0; ++i) TP_CK(launch(st));
     TP_CK(cudaEventRecord(pool.ev[1], st));
     TP_CK(cudaEventSynchronize(pool.ev[1]));
     float ms0 = 0;
@@ -657,7 +617,7 @@ static tp_status time_launches(tp_partition* part, Launch launch, int kpc, const
       cudaGraph_t graph = nullptr;
       TP_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       cudaError_t ce = cudaSuccess;
-      for (int i = 0; i < n && ce == cudaSuccess; ++i) ce = launch(st, chain_ctr ? i : -1);
+      for (int i = 0; i < n && ce == cudaSuccess; ++i) ce = launch(st);
       cudaError_t ee = cudaStreamEndCapture(st, &graph);
       g_launches -= (int64_t)n * kpc;   // capture does not launch
       if (ce != cudaSuccess || ee != cudaSuccess) {
@@ -670,17 +630,15 @@ static tp_status time_launches(tp_partition* part, Launch launch, int kpc, const
       TP_CK(ie);
     }
     for (int g = 0; g < groups; ++g) {
-      if (exec && chain_ctr) TP_CK(cudaMemsetAsync(chain_ctr, 0, sizeof(int), st));
       TP_CK(cudaEventRecord(pool.ev[2 + 2 * g], st));
       if (exec) {
         TP_CK(cudaGraphLaunch(exec, st));
         g_launches += (int64_t)n * kpc;
       } else {
-        for (int i = 0; i < n; ++i) TP_CK(launch(st, -1));
+        for (int i = 0; i < n; ++i) TP_CK(launch(st));
       }
       TP_CK(cudaEventRecord(pool.ev[3 + 2 * g], st));
     }
-    if (exec && chain_ctr) TP_CK(cudaMemsetAsync(chain_ctr, 0, sizeof(int), st));
     cudaError_t se = cudaStreamSynchronize(st);
     if (exec) cudaGraphExecDestroy(exec);
     TP_CK(se);
@@ -717,14 +675,8 @@ static tp_status time_plan(tp_partition* part, const ConvPlan& plan, const tp_ti
   ConvPlan early = plan;
   early.tc.args.w_early = (w_early_enabled() && !tm.flush_l2) ? 1 : 0;
   int count = 0;
-  const bool chain = chain_capable(plan) && tm.use_graph && !tm.flush_l2;
-  return time_launches(
-      part,
-      [&](cudaStream_t st, int seq) {
-        const ConvPlan& p = count++ == 0 ? plan : early;
-        return seq >= 0 ? launch_plan_chain(p, st, seq) : launch_plan(p, st);
-      },
-      plan.kernels_per_call, tm, pool, out, chain ? plan.dep_ctr : nullptr);
+  return time_launches(part, [&](cudaStream_t st) { return launch_plan(count++ == 0 ? plan : early, st); },
+                       plan.kernels_per_call, tm, pool, out);
 }
 
 // ---------------------------------------------------------------- correctness gate (a10)
@@ -1051,15 +1003,13 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       // a kernel that never writes the weights (TcArgs::w_early).
       c.plan.tc.args.w_early = w_early_enabled() ? 1 : 0;
       cudaError_t e = cudaSuccess;
-      const bool chain = chain_capable(c.plan) && tm.use_graph;
       for (int k = 0; k < warm && e == cudaSuccess; ++k) e = launch_plan(c.plan, st);
       const auto te1 = std::chrono::steady_clock::now();
       if (e == cudaSuccess && tm.use_graph) {
         cudaGraph_t graph = nullptr;
         e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
         cudaError_t ce = cudaSuccess;
-        for (int k = 0; k < c.n && ce == cudaSuccess && e == cudaSuccess; ++k)
-          ce = chain ? launch_plan_chain(c.plan, st, k) : launch_plan(c.plan, st);
+        for (int k = 0; k < c.n && ce == cudaSuccess && e == cudaSuccess; ++k) ce = launch_plan(c.plan, st);
         if (e == cudaSuccess) {
           cudaError_t ee = cudaStreamEndCapture(st, &graph);
           g_launches -= (int64_t)c.n * c.plan.kernels_per_call;   // capture does not launch
@@ -1104,8 +1054,7 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
       }
       cudaEvent_t* ev = pb.ev.data() + (size_t)c.slot * 2 * groups;
       for (int g = 0; g < c.groups && e == cudaSuccess; ++g) {
-        if (chain && c.exec) e = cudaMemsetAsync(c.plan.dep_ctr, 0, sizeof(int), st);
-        if (e == cudaSuccess) e = cudaEventRecord(ev[2 * g], st);
+        e = cudaEventRecord(ev[2 * g], st);
         if (e == cudaSuccess) {
           if (c.exec) {
             e = cudaGraphLaunch(c.exec, st);
@@ -1116,7 +1065,6 @@ static tp_status measure_candidates(const Layer& L, tp_partition* part, const in
         }
         if (e == cudaSuccess) e = cudaEventRecord(ev[2 * g + 1], st);
       }
-      if (e == cudaSuccess && chain && c.exec) e = cudaMemsetAsync(c.plan.dep_ctr, 0, sizeof(int), st);
       if (e != cudaSuccess) {
         c.m.status = TP_ECUDA;
         set_error(std::string("timing enqueue: ") + cudaGetErrorString(e));
@@ -1414,22 +1362,13 @@ tp_status tp_partition_floor(tp_partition* part, int32_t ctas, int32_t threads, 
   CtxGuard g(p);
   EventPool pool;
   const int pdl = pdl_enabled() ? 1 : 0;
-  // With flag chains on, the floor is an empty kernel chained the same way
-  // (every CTA waits for the earlier launches' arrivals, then arrives).
-  TunerScratch& sc = scratch_of(p);
-  const bool chain = flag_chain_enabled() && tm.use_graph && !tm.flush_l2;
-  if (chain && !sc.dep) {
-    TP_CK(cudaMalloc(&sc.dep, 256));
-    TP_CK(cudaMemset(sc.dep, 0, 256));
-  }
   st = time_launches(
       p,
-      [&](cudaStream_t s, int seq) {
+      [&](cudaStream_t s) {
         g_launches += 1;
-        return seq >= 0 ? launch_empty_chain(ctas, threads, sc.dep, seq * ctas, s)
-                        : launch_empty(ctas, threads, pdl, s);
+        return launch_empty(ctas, threads, pdl, s);
       },
-      1, tm, pool, out, chain ? sc.dep : nullptr);
+      1, tm, pool, out);
   out->ctas = ctas;
   out->threads_per_cta = threads;
   out->sm_requested = p->sm_requested;
@@ -1711,11 +1650,6 @@ tp_status tp_chain_run(int32_t n_layers, const tp_conv_desc* descs, const tp_sch
   if (st != TP_OK) return st;
   std::lock_guard<std::mutex> lk(p->mu);
   CtxGuard g(p);
-  TunerScratch& sc = scratch_of(p);
-  if (!sc.dep) {
-    TP_CK(cudaMalloc(&sc.dep, 256));
-    TP_CK(cudaMemset(sc.dep, 0, 256));
-  }
   std::vector<ConvPlan> plans(n_layers);
   for (int32_t i = 0; i < n_layers; ++i) {
     Layer L;
@@ -1724,29 +1658,18 @@ tp_status tp_chain_run(int32_t n_layers, const tp_conv_desc* descs, const tp_sch
     st = make_plan(L, scheds[i], x[i], w[i], bias ? bias[i] : nullptr, y[i], ws[i], ws_bytes[i], &plans[i],
                    p->sm_granted);
     if (st != TP_OK) return st;
-    plans[i].dep_ctr = sc.dep;
   }
-  // One graph: reps x the layer sequence.  A chain-capable launch whose
-  // predecessor also arrives on the counter waits for all arrivals so far;
-  // any other launch waits for its predecessor's completion (griddepcontrol).
+  // One graph: reps x the layer sequence; each launch waits for its
+  // predecessor's completion (programmatic dependent launch, griddepcontrol).
   cudaStream_t s = p->stream;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
-  int cum = 0, launches = 0;
-  bool prev_signals = false;
+  int launches = 0;
   for (int32_t r = 0; r < reps && e == cudaSuccess; ++r)
     for (int32_t i = 0; i < n_layers && e == cudaSuccess; ++i) {
-      const ConvPlan& pl = plans[i];
-      if (chain_capable(pl)) {
-        e = launch_plan_signal(pl, s, prev_signals ? cum : 0);
-        cum += plan_ctas(pl);
-        prev_signals = true;
-      } else {
-        e = launch_plan(pl, s);
-        prev_signals = false;
-      }
-      launches += pl.kernels_per_call;
+      e = launch_plan(plans[i], s);
+      launches += plans[i].kernels_per_call;
     }
   cudaError_t ee = cudaStreamEndCapture(s, &graph);
   g_launches -= launches;
@@ -1759,14 +1682,12 @@ tp_status tp_chain_run(int32_t n_layers, const tp_conv_desc* descs, const tp_sch
     return TP_ECUDA;
   }
   auto replay = [&]() -> cudaError_t {
-    cudaError_t r = cudaMemsetAsync(sc.dep, 0, sizeof(int), s);
-    if (r == cudaSuccess) r = cudaGraphLaunch(exec, s);
+    cudaError_t r = cudaGraphLaunch(exec, s);
     if (r == cudaSuccess) g_launches += launches;
     return r;
   };
   if (!timing && !out) {
     e = replay();
-    if (e == cudaSuccess) e = cudaMemsetAsync(sc.dep, 0, sizeof(int), s);
   } else {
     const tp_timing tm = timing ? *timing : default_timing();
     EventPool pool;
@@ -1774,13 +1695,11 @@ tp_status tp_chain_run(int32_t n_layers, const tp_conv_desc* descs, const tp_sch
     for (int i = 0; i < std::max(0, tm.warmup) && e == cudaSuccess; ++i) e = replay();
     std::vector<double> per;
     for (int gi = 0; gi < std::max(1, tm.groups) && e == cudaSuccess; ++gi) {
-      e = cudaMemsetAsync(sc.dep, 0, sizeof(int), s);
-      if (e == cudaSuccess) e = cudaEventRecord(pool.ev[2 * gi], s);
+      e = cudaEventRecord(pool.ev[2 * gi], s);
       if (e == cudaSuccess) e = cudaGraphLaunch(exec, s);
       if (e == cudaSuccess) g_launches += launches;
       if (e == cudaSuccess) e = cudaEventRecord(pool.ev[2 * gi + 1], s);
     }
-    if (e == cudaSuccess) e = cudaMemsetAsync(sc.dep, 0, sizeof(int), s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     for (int gi = 0; gi < std::max(1, tm.groups) && e == cudaSuccess; ++gi) {
       float ms = 0;

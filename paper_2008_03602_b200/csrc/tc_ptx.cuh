@@ -127,26 +127,6 @@ static __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, cons
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
-// Flag chain (TcArgs::dep_*): wait for the predecessors' arrivals, then order
-// the async-proxy (TMA) reads of their outputs after the generic acquire.
-static __device__ __forceinline__ void dep_wait_acquire(const int* ctr, int target) {
-  int v;
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    if (v >= target) break;
-    __nanosleep(32);
-  }
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-// Called by one thread after a CTA barrier that follows every thread's global
-// writes (and, for TMA stores, cp.async.bulk.wait_group 0 by the issuing thread).
-static __device__ __forceinline__ void dep_signal_release(int* ctr) {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(ctr) : "memory");
-}
-static __device__ __forceinline__ void tma_store_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
 static __device__ __forceinline__ void tma_store_commit_wait() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

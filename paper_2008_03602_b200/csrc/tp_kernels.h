@@ -87,15 +87,6 @@ struct TcArgs {
   int w_early;                 // 1: weight (B) boxes of the first ring pass are issued before
                                //    griddepcontrol.wait -- only when the preceding kernel in the
                                //    stream is a launch of this plan (weights are layer constants)
-  // Flag-chained launches ("flag chain"): a chain of launches of
-  // libtp kernels whose ordering is carried by a global arrival counter instead of
-  // grid completion.  dep_wait > 0: the TMA producers wait until *dep_ctr >= dep_wait
-  // (acquire, gpu scope) instead of griddepcontrol.wait; dep_signal: every CTA adds 1 to
-  // *dep_ctr (release, gpu scope) once all of its global writes are complete.
-  int* dep_ctr;
-  int dep_wait;
-  int dep_signal;
-  int dep_early;               // flag chain: trigger the dependent launch at kernel entry
   int strip_px;                // strip kind: 16-byte pixels per phase box
   int strip_stage;             // strip kind: bytes of one ring stage (s_w phase boxes)
   int strip_woff;              // strip kind: byte offset of the resident weights
@@ -180,7 +171,6 @@ cudaError_t launch_copy(const void* src, void* dst, size_t bytes, int grid, cuda
 cudaError_t launch_l2_flush(void* buf, size_t bytes, int grid, cudaStream_t st);
 cudaError_t launch_pad_c8(const void* x, void* x8, int64_t npix, int C, const void* w, void* w8, int K, int R, int S,
                           int pdl, cudaStream_t st);
-cudaError_t launch_empty_chain(int ctas, int threads, int* ctr, int wait, cudaStream_t st);
 cudaError_t launch_empty(int ctas, int threads, int pdl, cudaStream_t st);
 
 }  // namespace tp

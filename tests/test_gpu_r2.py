@@ -354,7 +354,7 @@ def test_no_out_of_bounds_writes_every_schedule(d):
     assert not bad, f"{len(bad)} failures, first: {bad[:5]}"
 
 
-# ------------------------------------------------------------------ flag-chained launches (model-level run)
+# ------------------------------------------------------------------ model-level run (tp_chain_run)
 def _chain_pair(c=8, hw=20, k1=8, k2=16):
     a = mk(1, c, hw, hw, k1, 3, 3, 1, 1, epi=2)                       # bf16 out: the next layer's input
     b = mk(1, k1, hw, hw, k2, 1, 1, 1, 0, out=tp.FP32, epi=0)         # reads a's y
@@ -397,10 +397,9 @@ def test_chain_run_next_layer_reads_previous_output(reps):
 
 
 def test_chain_run_mixed_kinds_and_timed_layer_counter_zeroed():
-    """A chain mixing kinds that take part in the flag chain (TMA im2col) and
-    kinds that use grid completion (direct depthwise, row-halo) keeps the
-    producer -> consumer order; a timed tp_conv2d_run of a chain-capable
-    schedule leaves its workspace arrival counter at zero."""
+    """A chain mixing kinds (TMA im2col, row-halo, direct depthwise) keeps the
+    producer -> consumer order; a timed tp_conv2d_run leaves the workspace
+    zeroed."""
     c = 64
     d1 = mk(1, c, 8, 60, c, 3, 3, 1, 1, epi=2)                         # row-halo + TMA kinds
     d2 = mk(1, c, 8, 60, c, 3, 3, 1, 1, g=c, epi=2)                    # depthwise direct (bf16)
