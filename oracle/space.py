@@ -196,15 +196,16 @@ def strip_eligible(d: dict) -> bool:
 
 
 def _valid_strip(d: dict, bm: int, bn: int, stages: int, tiles_per_cta: int) -> bool:
-    # one ring stage = s_w phase boxes of (bm + 2 ceil(T0 / 2) - 1) 16-byte pixels, each rounded
-    # up to 128 B, where T0 = ceil(S / s_w) taps fall in phase 0; resident weights: R rows of
-    # (S + s_w) taps x bn rows x 16 B, rounded up to 1 KiB; + 1 KiB of barriers
+    # one ring stage = the strip of (bm + 2 ceil(T0 / 2) - 1) 16-byte pixels (T0 = ceil(S / s_w)
+    # taps in phase 0): with s_w = 1 whole 512-byte boxes, with s_w = 2 one box per phase rounded
+    # up to 128 B; resident weights: R rows of (S + s_w) taps x bn rows x 16 B, rounded up to
+    # 1 KiB; + 1 KiB of barriers
     P, Q = out_pq(d)
     sw = d["stride_w"]
     px = bm + 2 * _cdiv(_cdiv(d["s"], sw), 2) - 1
     if sw * px > 256:                # a TMA box spans at most 256 elements per dimension
         return False
-    stage = sw * _cdiv(px * 16, 128) * 128
+    stage = _cdiv(px * 16, 512) * 512 if sw == 1 else sw * _cdiv(px * 16, 128) * 128
     weights = _cdiv(d["r"] * (d["s"] + sw) * bn * 16, 1024) * 1024
     if stages * stage + weights + 1024 > SMEM_LIMIT:
         return False

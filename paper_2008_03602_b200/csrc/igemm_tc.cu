@@ -621,6 +621,9 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 // core matrices along K 16 B apart (A) and s_w BN 16 B apart (weights laid out
 // [r][s][n][8] in shared memory, loaded once; the s_w zero taps after each
 // row's S taps pair with an odd tap count).
+#ifndef TP_MT_WAIT
+#define TP_MT_WAIT mbar_wait_sleep
+#endif
 template <int BM, int BN, int BK, int KM>
 __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
@@ -636,7 +639,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
   // STRIP: runtime stage size (phase boxes only; the weights are resident)
   const uint32_t A_STAGE = STRIP ? (uint32_t)a.strip_stage : (ROW ? A_STRIP : A_SUB * NSUB);
   const uint32_t B_STAGE = STRIP ? 0u : (ROW ? 3 * B_TAP : B_SUB * NSUB);
-  const uint32_t A_BYTES = STRIP ? (uint32_t)(a.sw * a.strip_px * 16)
+  const uint32_t A_BYTES = STRIP ? (a.sw == 1 ? (uint32_t)a.strip_stage : (uint32_t)(a.sw * a.strip_px * 16))
                                  : (ROW ? (BM + 2) * 128 : A_SUB * NSUB);   // expect_tx of the A part
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
@@ -679,18 +682,43 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     trace[62] = sm;
   }
 
-  // ROW: tile = BM pixels of one output row (q-block t % nqb of row t / nqb);
+  // ROW / STRIP: tile = BM pixels of one output row (q-block t % nqb of row t / nqb);
   // im2col: tile = BM consecutive output pixels m0 = t * BM (rows past M masked).
-  auto tile_coords = [&](int t, int& q0, int& p0, int& n0, int& mrow0, int& mvalid) {
+  // A CTA's tiles are consecutive: the cursor is set once (divisions) and then
+  // advanced with compares (ncu: the per-tile divisions were ~6% of the strip
+  // kernel's instructions).
+  struct TileCursor { int qb, p, n, m0; };
+  auto cursor_at = [&](int t) {
+    TileCursor c{0, 0, 0, 0};
     if constexpr (ROW || STRIP) {
-      const int qb = t % a.nqb, row = t / a.nqb;
-      q0 = qb * BM;
-      p0 = row % a.P;
-      n0 = row / a.P;
-      mrow0 = row * a.Q + q0;
+      const int row = t / a.nqb;
+      c.qb = t - row * a.nqb;
+      c.p = row % a.P;
+      c.n = row / a.P;
+    } else {
+      c.m0 = t * BM;
+    }
+    return c;
+  };
+  auto cursor_next = [&](TileCursor& c) {
+    if constexpr (ROW || STRIP) {
+      if (++c.qb == a.nqb) {
+        c.qb = 0;
+        if (++c.p == a.P) { c.p = 0; ++c.n; }
+      }
+    } else {
+      c.m0 += BM;
+    }
+  };
+  auto tile_coords = [&](const TileCursor& c, int& q0, int& p0, int& n0, int& mrow0, int& mvalid) {
+    if constexpr (ROW || STRIP) {
+      q0 = c.qb * BM;
+      p0 = c.p;
+      n0 = c.n;
+      mrow0 = (n0 * a.P + p0) * a.Q + q0;
       mvalid = a.Q - q0 < BM ? a.Q - q0 : BM;
     } else {
-      const int m0 = t * BM;
+      const int m0 = c.m0;
       q0 = m0 % a.Q;
       const int t0 = m0 / a.Q;
       p0 = t0 % a.P;
@@ -740,12 +768,21 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       uint8_t* sb = b_tiles + (size_t)stage * B_STAGE;
       if (parts & 4) mbar_arrive_expect_tx_p(full + stage, A_BYTES + B_STAGE, lead);
       if constexpr (STRIP) {
-        // filter row r: one strip per column phase (the weights are resident)
-        const uint32_t pb = (uint32_t)a.strip_stage / (uint32_t)a.sw;
-        for (int f = 0; f < a.sw; ++f)
-          if (parts & 1)
-            tma_load_tile_4d_p(sa + f * pb, &tmA, full + stage, 0, q0 * a.sw - a.pw + f, p0 * a.sh - a.ph + r, n0,
-                               lead);
+        // filter row r: one strip per column phase (the weights are resident).
+        // s_w = 1: the strip is contiguous in the padded row, loaded as 512-byte
+        // boxes of a (W*8, H, N) view -- a box of 16-byte rows costs the TMA
+        // engine one request per row (measured: the ring then starves the MMA).
+        if (parts & 1) {
+          if (a.sw == 1) {
+            for (int j = 0; j < a.strip_px; j += 32)
+              tma_load_tile_3d_p(sa + j * 16, &tmA, full + stage, (q0 - a.pw + j) * 8, p0 * a.sh - a.ph + r, n0, lead);
+          } else {
+            const uint32_t pb = (uint32_t)a.strip_stage / (uint32_t)a.sw;
+            for (int f = 0; f < a.sw; ++f)
+              tma_load_tile_4d_p(sa + f * pb, &tmA, full + stage, 0, q0 * a.sw - a.pw + f, p0 * a.sh - a.ph + r, n0,
+                                 lead);
+          }
+        }
       } else if constexpr (ROW) {
         // (channel block cb, filter row r): the input strip + the three taps
         if (parts & 1) tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
@@ -800,16 +837,19 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     }
     int stage = 0;
     uint32_t phase = 0;
+    TileCursor cur = cursor_at(tile0);
     for (int i = 0; i < ntl; ++i) {
       int q0, p0, n0, mrow0, mvalid;
-      tile_coords(tile0 + i, q0, p0, n0, mrow0, mvalid);
+      tile_coords(cur, q0, p0, n0, mrow0, mvalid);
+      cursor_next(cur);
       int cb = 0, r = 0, sx = 0;
       for (int kb = 0; kb < kpt; ++kb) {
-        mbar_wait(empty + stage, phase ^ 1u);
+        TP_MT_WAIT(empty + stage, phase ^ 1u);
         issue(stage, cb, r, sx, q0, p0, n0, mrow0, (i == 0 && kb < npre) ? 1 : 7);
         advance(cb, r, sx);
         if (++stage == stages) { stage = 0; phase ^= 1u; }
       }
+      if (trace && lane == 0 && i < 8) trace[4 + i] = gtimer();    // tile i's loads issued
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: two accumulators, alternating per tile ----------------
@@ -820,18 +860,18 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     int stage = 0;
     uint32_t phase = 0;
     if constexpr (STRIP) {
-      mbar_wait(wfull, 0);
+      TP_MT_WAIT(wfull, 0);
       tc_fence_after();
     }
     for (int i = 0; i < ntl; ++i) {
       const int buf = i & 1;
       if (i >= 2) {
-        mbar_wait(tempty + buf, (uint32_t)(((i - 2) >> 1) & 1));
+        TP_MT_WAIT(tempty + buf, (uint32_t)(((i - 2) >> 1) & 1));
         tc_fence_after();
       }
       const uint32_t dcol = tmem_base + (uint32_t)(buf * BN);
       for (int kb = 0; kb < kpt; ++kb) {
-        mbar_wait(full + stage, phase);
+        TP_MT_WAIT(full + stage, phase);
         tc_fence_after();
         const uint64_t ad = adesc0 + ((uint32_t)(stage * A_STAGE) >> 4);
         const uint64_t bd = bdesc0 + ((uint32_t)(stage * B_STAGE) >> 4);
@@ -867,6 +907,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
         if (++stage == stages) { stage = 0; phase ^= 1u; }
       }
       tc_commit_p(tfull + buf, lead);
+      if (trace && lane == 0 && i < 8) trace[12 + i] = gtimer();   // tile i's MMAs issued
     }
   }
 
@@ -891,14 +932,27 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     // [M][K] for multi-tile im2col tiles -- and store it with TMA from one thread.
     const int n_epi = n_epi_warps * 32;
     const int issuer = split_roles ? 64 : 0;
+    // Bias of the CTA's BN columns staged once in shared memory (inside the
+    // barrier block: BN <= 128 floats fit after the barriers), read after this
+    // grid's PDL wait like every other operand; BN = 256 keeps per-chunk loads.
+    constexpr bool kBiasSmem = BN <= 128;
+    float* sbias = reinterpret_cast<float*>(smem_raw + a.bar_off + 256);
+    if constexpr (kBiasSmem) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int j = (int)threadIdx.x - (split_roles ? 64 : 0); j < BN; j += n_epi)
+        sbias[j] = (a.has_bias && nbase + j < a.K) ? __ldg(a.bias + nbase + j) : 0.0f;
+      asm volatile("bar.sync 3, %0;" ::"r"(n_epi) : "memory");
+    }
     uint8_t* stg = smem_raw + a.recv_off;
     const uint32_t EB = a.out_f32 ? 4u : 2u;
     const uint32_t IB = BN * EB < 128u ? BN * EB : 128u;
     const uint32_t ystage = (uint32_t)BM * BN * EB;   // bytes of one staged tile
+    TileCursor cur = cursor_at(tile0);
     for (int i = 0; i < ntl; ++i) {
       const int buf = i & 1;
       int q0, p0, n0, mrow0, mvalid;
-      tile_coords(tile0 + i, q0, p0, n0, mrow0, mvalid);
+      tile_coords(cur, q0, p0, n0, mrow0, mvalid);
+      cursor_next(cur);
       // a.ystage2: two staging buffers alternate, so only the store of tile i - 2
       // must have read this one (one bulk group may stay in flight)
       uint8_t* stg_t = stg + (a.ystage2 ? (size_t)buf * ystage : 0);
@@ -913,18 +967,27 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       }
       float bv[16];
       const int nb0 = nbase + c_begin;
+      if constexpr (kBiasSmem) {
 #pragma unroll
-      for (int g = 0; g < 16; g += 4) {
-        if (a.has_bias && nb0 + g + 4 <= a.K) {
-          const float4 f = __ldg(reinterpret_cast<const float4*>(a.bias + nb0 + g));
+        for (int g = 0; g < 16; g += 4) {
+          const float4 f = *reinterpret_cast<const float4*>(sbias + c_begin + g);
           bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
-        } else {
-          bv[g] = bv[g + 1] = bv[g + 2] = bv[g + 3] = 0.0f;
+        }
+      } else {
+#pragma unroll
+        for (int g = 0; g < 16; g += 4) {
+          if (a.has_bias && nb0 + g + 4 <= a.K) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(a.bias + nb0 + g));
+            bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
+          } else {
+            bv[g] = bv[g + 1] = bv[g + 2] = bv[g + 3] = 0.0f;
+          }
         }
       }
       __syncwarp();
-      mbar_wait(tfull + buf, (uint32_t)((i >> 1) & 1));
+      TP_MT_WAIT(tfull + buf, (uint32_t)((i >> 1) & 1));
       tc_fence_after();
+      if (trace && (int)threadIdx.x == issuer && i < 8) trace[28 + i] = gtimer();   // tile i's accumulator ready
       for (int c = c_begin; c < c_end; c += 16) {
         uint32_t raw[16];
         tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + c), raw);
@@ -932,7 +995,10 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
         if (c > c_begin) {
 #pragma unroll
           for (int g = 0; g < 16; g += 4) {
-            if (a.has_bias && nb + g + 4 <= a.K) {
+            if constexpr (kBiasSmem) {
+              const float4 f = *reinterpret_cast<const float4*>(sbias + c + g);
+              bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
+            } else if (a.has_bias && nb + g + 4 <= a.K) {
               const float4 f = __ldg(reinterpret_cast<const float4*>(a.bias + nb + g));
               bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
             } else {
@@ -1003,6 +1069,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + buf);
+      if (trace && (int)threadIdx.x == issuer && i < 8) trace[20 + i] = gtimer();   // tile i drained (issuer warp)
       if (a.y_tma) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync 2, %0;" ::"r"(n_epi) : "memory");
@@ -1112,15 +1179,27 @@ static tp_status strip_prepare(const TcProblem& pb, TcPlan* plan) {
   const int sw = pb.sw;
   const int t0 = (pb.S + sw - 1) / sw;
   const int px = pb.bm + 2 * ((t0 + 1) / 2) - 1;
-  const int phase_bytes = (px * 16 + 127) / 128 * 128;
+  // s_w = 1: whole 512-byte boxes (32 pixels each); s_w = 2: one strided box per phase
+  const int phase_bytes = sw == 1 ? (px * 16 + 511) / 512 * 512 : (px * 16 + 127) / 128 * 128;
   {
-    cuuint64_t dims[4] = {8, (cuuint64_t)pb.W, (cuuint64_t)pb.H, (cuuint64_t)pb.N};
-    cuuint64_t strides[3] = {16, (cuuint64_t)pb.W * 16, (cuuint64_t)pb.H * pb.W * 16};
-    cuuint32_t box[4] = {8, (cuuint32_t)(sw * px), 1, 1};
-    cuuint32_t es[4] = {1, (cuuint32_t)sw, 1, 1};
-    CUresult r = drv.encodeTiled(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.x), dims,
-                                 strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    if (sw == 1) {   // padded rows as (W*8, H, N): 256-element (512-byte) boxes along the row
+      cuuint64_t dims[3] = {(cuuint64_t)pb.W * 8, (cuuint64_t)pb.H, (cuuint64_t)pb.N};
+      cuuint64_t strides[2] = {(cuuint64_t)pb.W * 16, (cuuint64_t)pb.H * pb.W * 16};
+      cuuint32_t box[3] = {256, 1, 1};
+      cuuint32_t es[3] = {1, 1, 1};
+      r = drv.encodeTiled(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pb.x), dims, strides, box,
+                          es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      cuuint64_t dims[4] = {8, (cuuint64_t)pb.W, (cuuint64_t)pb.H, (cuuint64_t)pb.N};
+      cuuint64_t strides[3] = {16, (cuuint64_t)pb.W * 16, (cuuint64_t)pb.H * pb.W * 16};
+      cuuint32_t box[4] = {8, (cuuint32_t)(sw * px), 1, 1};
+      cuuint32_t es[4] = {1, (cuuint32_t)sw, 1, 1};
+      r = drv.encodeTiled(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.x), dims, strides, box,
+                          es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (r != CUDA_SUCCESS) {
       set_error("tensor map (strip A) failed (" + std::to_string((int)r) + ")");
       return TP_ECUDA;

@@ -252,7 +252,10 @@ int64_t strip_box_px(const Layer& L, int bm) {
   const int64_t t0 = cdiv(L.d.s, L.d.stride_w);
   return bm + 2 * cdiv(t0, 2) - 1;
 }
+// s_w = 1: the strip is loaded as whole 512-byte boxes; s_w = 2: one box per
+// column phase, each rounded up to 128 bytes.
 int64_t strip_stage_bytes(const Layer& L, int bm) {
+  if (L.d.stride_w == 1) return cdiv(strip_box_px(L, bm) * 16, 512) * 512;
   return (int64_t)L.d.stride_w * cdiv(strip_box_px(L, bm) * 16, 128) * 128;
 }
 // Resident weights: per filter row, S taps + s_w zero taps of BN x 16 B.

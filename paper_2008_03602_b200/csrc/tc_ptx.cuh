@@ -32,6 +32,19 @@ static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
       "r"(parity)
       : "memory");
 }
+// Same wait with a suspend-time hint: the thread sleeps until the phase
+// completes (or the hint elapses) instead of re-issuing try_wait, leaving the
+// issue slots to the warps doing work (multi-tile kinds: ncu showed ~30% of the
+// stall samples and a large share of the instructions in spin loops).
+static __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TP_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra TP_WAITS_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 static __device__ __forceinline__ void tma_load_im2col_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c,
                                                    int32_t w, int32_t h, int32_t n, uint16_t off_w,
                                                    uint16_t off_h) {
@@ -96,6 +109,15 @@ static __device__ __forceinline__ void tma_load_tile_2d_p(void* dst, const CUten
       "@q cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4}], [%2];\n\t}" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(lead)
+      : "memory");
+}
+static __device__ __forceinline__ void tma_load_tile_3d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                   int32_t c1, int32_t c2, uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %6, 0;\n\t"
+      "@q cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(lead)
       : "memory");
 }
 static __device__ __forceinline__ void tc_mma_p(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
