@@ -628,7 +628,9 @@ def run_extras(args, tp, refs, shard, datagen, wl, part, bufs, units, checks, me
         rows = []
         for row in cx["layers"]:
             rl = row["diag_roofline"][str(q)]
-            rows.append({"layer": row["layer"], "best_us": round(row["matrix_us"][str(q)][str(q)], 3),
+            rows.append({"layer": row["layer"], "space_index": row["best_schedule"][str(q)]["space_index"],
+                         "kind": row["best_schedule"][str(q)]["kind"],
+                         "best_us": round(row["matrix_us"][str(q)][str(q)], 3),
                          "binding": rl["binding"], "binding_roof_us": round(rl["roof_us"][rl["binding"] + "_us"], 3),
                          "binding_roof_frac": round(rl["frac_of_binding_roof"], 3),
                          "tensor_frac": round(rl["tensor_frac"], 4), "hbm_frac": round(rl["hbm_frac"], 4)})

@@ -66,7 +66,14 @@ enum { TP_EPI_BIAS = 1, TP_EPI_RELU = 2 };
  * are gathered into shared memory by CUDA-core warps over the flattened
  * (r, s, c) axis (bf16, g = 1, C % 8 != 0: the C = 3 stems). */
 enum { TP_KIND_IGEMM_TC = 0, TP_KIND_DIRECT = 1, TP_KIND_IGEMM_TC_GATHER = 2, TP_KIND_IGEMM_TC_ROW = 3,
-       TP_KIND_IGEMM_TC_MT = 4, TP_KIND_IGEMM_TF32X3 = 5, TP_KIND_IGEMM_TC_STEM = 6, TP_KIND_IGEMM_TC_STRIP = 7 };
+       TP_KIND_IGEMM_TC_MT = 4, TP_KIND_IGEMM_TF32X3 = 5, TP_KIND_IGEMM_TC_STEM = 6, TP_KIND_IGEMM_TC_STRIP = 7,
+       TP_KIND_IGEMM_TC_ROWW = 8 };
+/* IGEMM_TC_ROWW ("row-halo, resident weights"): appended after the IGEMM_TC_ROW
+ * tuples of row-halo layers with C = 64.  The nine taps' BN x 64 weight tiles
+ * are loaded once per CTA; the ring carries input strips only.  Knobs BM
+ * {64, 128}, BN {32..256}, stages (strips in flight) {2, 4, 6, 8},
+ * tiles_per_cta {2, 4, 8, 16}; bk = 64, threads = 256, split_k = 1; grid as
+ * IGEMM_TC_ROW. */
 /* IGEMM_TC_STRIP ("strip"): appended after the gathered (and stem) tuples of
  * gathered layers with C <= 8, stride_w in {1, 2}, R, S <= 8.  A pre-pass inside
  * the call pads x to NHWC with 8 channels and w to [K][R][S][8] (16-byte pixel

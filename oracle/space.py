@@ -27,6 +27,7 @@ KIND_IGEMM_TC_MT = 4
 KIND_IGEMM_TF32X3 = 5
 KIND_IGEMM_TC_STEM = 6
 KIND_IGEMM_TC_STRIP = 7
+KIND_IGEMM_TC_ROWW = 8
 DTYPE_BF16 = 0
 DTYPE_FP32 = 1
 SMEM_LIMIT = 232448          # 227 KiB usable per CTA on sm_100a
@@ -37,6 +38,7 @@ ROW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (1, 2, 3)
              ("tiles_per_cta", (1, 2, 4, 8, 16)))
 MT_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("tiles_per_cta", (2, 4, 8)))
 STEM_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128)), ("tiles_per_cta", (2, 4, 8, 16)))
+ROWW_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 4, 6, 8)), ("tiles_per_cta", (2, 4, 8, 16)))
 STRIP_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128)), ("stages", (2, 4, 6)), ("tiles_per_cta", (1, 2, 4, 8, 16)))
 TF32_KNOBS = (("bm", (64, 128)), ("bn", (32, 64, 128, 256)), ("stages", (2, 3, 4)), ("split_k", (1, 2, 4, 8)))
 DIRECT_KNOBS = (("threads", (64, 128, 256, 512)), ("tile_q", (1, 2, 4)), ("vec_k", (1, 2, 4, 8)),
@@ -188,6 +190,21 @@ def _valid_stem(d: dict, bm: int, bn: int, tiles_per_cta: int) -> bool:
     return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))
 
 
+def roww_eligible(d: dict) -> bool:
+    """Row-halo kind with resident weights: row-halo layers with C = 64."""
+    return row_eligible(d) and d["c"] == 64
+
+
+def _valid_roww(d: dict, bm: int, bn: int, stages: int, tiles_per_cta: int) -> bool:
+    # stages input strips of (bm + 2) x 128 B (each rounded up to 1 KiB) + the nine taps' weight
+    # tiles bn x 128 B + 1 KiB of barriers
+    P, Q = out_pq(d)
+    strip = _cdiv((bm + 2) * 128, 1024) * 1024
+    if stages * strip + 9 * bn * 128 + 1024 > SMEM_LIMIT:
+        return False
+    return bm <= _np2(Q) and bn <= max(32, _np2(d["k"]))
+
+
 def strip_eligible(d: dict) -> bool:
     """Strip kind: gathered layers with C <= 8, column
     stride 1 or 2 and filters of at most 8 x 8."""
@@ -255,6 +272,13 @@ def enumerate_space(d: dict) -> list[dict]:
                          space_index=len(out))
                 s.update(geometry(d, s))
                 out.append(s)
+    if roww_eligible(d):         # after the row-halo tuples; bk = 64, threads = 256, split_k = 1
+        for combo in itertools.product(*[v for _, v in ROWW_KNOBS]):
+            if _valid_roww(d, *combo):
+                s = dict(zip([k for k, _ in ROWW_KNOBS], combo), bk=64, threads=256, split_k=1,
+                         kind=KIND_IGEMM_TC_ROWW, space_index=len(out))
+                s.update(geometry(d, s))
+                out.append(s)
     if tf32_eligible(d):         # appended after the direct tuples; bk = 32, threads = 256, split_k = 1
         for combo in itertools.product(*[v for _, v in TF32_KNOBS]):
             if _valid_tf32(d, *combo):
@@ -293,7 +317,7 @@ def geometry(d: dict, s: dict) -> dict:
         g = (_cdiv(_cdiv(d["n"] * P * Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
     elif s.get("kind") in (KIND_IGEMM_TC_STEM, KIND_IGEMM_TC_STRIP):
         g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
-    elif s.get("kind") == KIND_IGEMM_TC_ROW:
+    elif s.get("kind") in (KIND_IGEMM_TC_ROW, KIND_IGEMM_TC_ROWW):
         g = (_cdiv(d["n"] * P * _cdiv(Q, s["bm"]), s["tiles_per_cta"]), _cdiv(d["k"], s["bn"]), 1)
     elif s.get("kind", layer_kind(d)) in (KIND_IGEMM_TC, KIND_IGEMM_TC_GATHER, KIND_IGEMM_TF32X3):
         M = d["n"] * P * Q

@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
   constexpr uint32_t B_TAP = BN * 128;
   // STRIP: runtime stage size (phase boxes only; the weights are resident)
   const uint32_t A_STAGE = STRIP ? (uint32_t)a.strip_stage : (ROW ? A_STRIP : A_SUB * NSUB);
-  const uint32_t B_STAGE = STRIP ? 0u : (ROW ? 3 * B_TAP : B_SUB * NSUB);
+  const uint32_t B_STAGE = (STRIP || (ROW && a.roww)) ? 0u : (ROW ? 3 * B_TAP : B_SUB * NSUB);
   const uint32_t A_BYTES = STRIP ? (a.sw == 1 ? (uint32_t)a.strip_stage : (uint32_t)(a.sw * a.strip_px * 16))
                                  : (ROW ? (BM + 2) * 128 : A_SUB * NSUB);   // expect_tx of the A part
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
   uint64_t* tempty = tfull + 2;         // [2]
   uint64_t* wfull = tempty + 2;         // STRIP: resident weights landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
-  uint8_t* w_res = smem_raw + a.strip_woff;   // STRIP: [r][S + s_w taps][BN][16 B]
+  uint8_t* w_res = smem_raw + a.strip_woff;   // STRIP: [r][S + s_w taps][BN][16 B]; ROW + roww: [r][s][BN][128 B]
   const uint32_t w_row = STRIP ? (uint32_t)((a.S + a.sw) * BN * 16) : 0u;
 
   const int tpc = a.tpc;
@@ -766,7 +766,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     auto issue = [&](int stage, int cb, int r, int sx, int q0, int p0, int n0, int m0, int parts) {
       uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
       uint8_t* sb = b_tiles + (size_t)stage * B_STAGE;
-      if (parts & 4) mbar_arrive_expect_tx_p(full + stage, A_BYTES + B_STAGE, lead);
+      if (parts & 4) mbar_arrive_expect_tx_p(full + stage, A_BYTES + ((parts & 2) ? B_STAGE : 0u), lead);
       if constexpr (STRIP) {
         // filter row r: one strip per column phase (the weights are resident).
         // s_w = 1: the strip is contiguous in the padded row, loaded as 512-byte
@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       } else if constexpr (ROW) {
         // (channel block cb, filter row r): the input strip + the three taps
         if (parts & 1) tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
-        if (parts & 2) {
+        if ((parts & 2) && !a.roww) {
 #pragma unroll
           for (int ss = 0; ss < 3; ++ss)
             tma_load_tile_4d_p(sb + ss * B_TAP, &tmB, full + stage, cb * 64, ss, r, nbase, lead);
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     };
     // w_early: the weight boxes of the first tile's first ring pass go out
     // before the PDL wait (weights are layer constants; see TcArgs::w_early).
-    const int npre = (!STRIP && a.w_early && ntl > 0) ? (kpt < stages ? kpt : stages) : 0;
+    const int npre = (!STRIP && !(ROW && a.roww) && a.w_early && ntl > 0) ? (kpt < stages ? kpt : stages) : 0;
     {
       int cb = 0, r = 0, sx = 0;
       for (int kb = 0; kb < npre; ++kb) {
@@ -834,6 +834,13 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       // resident weights: one box (8 channels, BN rows, S taps) per filter row
       mbar_arrive_expect_tx_p(wfull, (uint32_t)(a.R * a.S * BN * 16), lead);
       for (int r = 0; r < a.R; ++r) tma_load_tile_4d_p(w_res + (size_t)r * w_row, &tmB, wfull, 0, nbase, 0, r, lead);
+    } else if constexpr (ROW) {
+      if (a.roww) {   // resident weights (C = 64): the nine taps, once
+        mbar_arrive_expect_tx_p(wfull, 9u * B_TAP, lead);
+        for (int r = 0; r < 3; ++r)
+          for (int ss = 0; ss < 3; ++ss)
+            tma_load_tile_4d_p(w_res + (size_t)(r * 3 + ss) * B_TAP, &tmB, wfull, 0, ss, r, nbase, lead);
+      }
     }
     int stage = 0;
     uint32_t phase = 0;
@@ -845,7 +852,12 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       int cb = 0, r = 0, sx = 0;
       for (int kb = 0; kb < kpt; ++kb) {
         TP_MT_WAIT(empty + stage, phase ^ 1u);
-        issue(stage, cb, r, sx, q0, p0, n0, mrow0, (i == 0 && kb < npre) ? 1 : 7);
+        // Resident weights: when the ring has exactly one stage per k-block of a
+        // tile, k-block kb always lands in stage kb, so the weight boxes of the
+        // first tile stay valid and later tiles load the input side only
+        // (row-halo kind with C = 64: 123 -> 50 KB of L2 -> SMEM traffic per tile).
+        const bool w_resident = !STRIP && stages == kpt && i > 0;
+        issue(stage, cb, r, sx, q0, p0, n0, mrow0, (i == 0 && kb < npre) ? 1 : (w_resident ? 5 : 7));
         advance(cb, r, sx);
         if (++stage == stages) { stage = 0; phase ^= 1u; }
       }
@@ -855,11 +867,12 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     // ---------------- MMA issuer: two accumulators, alternating per tile ----------------
     const uint32_t lead = elect_one();
     const uint64_t adesc0 = STRIP ? make_sdesc_plain(smem_u32(a_tiles), 16u, 128u) : make_sdesc(smem_u32(a_tiles), SWZ);
+    const bool wres = STRIP || (ROW && a.roww);
     const uint64_t bdesc0 = STRIP ? make_sdesc_plain(smem_u32(w_res), (uint32_t)(a.sw * BN * 16), 128u)
-                                  : make_sdesc(smem_u32(b_tiles), SWZ);
+                                  : make_sdesc(smem_u32(wres ? w_res : b_tiles), SWZ);
     int stage = 0;
     uint32_t phase = 0;
-    if constexpr (STRIP) {
+    if (wres) {
       TP_MT_WAIT(wfull, 0);
       tc_fence_after();
     }
@@ -874,7 +887,9 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
         TP_MT_WAIT(full + stage, phase);
         tc_fence_after();
         const uint64_t ad = adesc0 + ((uint32_t)(stage * A_STAGE) >> 4);
-        const uint64_t bd = bdesc0 + ((uint32_t)(stage * B_STAGE) >> 4);
+        // roww: the weights of filter row kb (C = 64: one channel block) are resident
+        const uint64_t bd = (ROW && a.roww) ? bdesc0 + ((uint32_t)(kb * 3 * B_TAP) >> 4)
+                                            : bdesc0 + ((uint32_t)(stage * B_STAGE) >> 4);
         if constexpr (STRIP) {
           // filter row kb: per phase f, tap pairs (t, t + 1), t even; tap s = f + s_w t
           const uint32_t pb = (uint32_t)a.strip_stage / (uint32_t)a.sw;
@@ -1603,7 +1618,10 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   plan->block = dim3(pb.threads);
   // Multi-tile kinds with tiles_per_cta > 1: two more drain warps, so each TMEM
   // lane quadrant has two (the knob stays 256 threads; TP_EPI8=0 turns it off).
-  if ((pb.row || pb.mt) && a.tpc > 1 && pb.threads == 256 && pb.bn >= 128 && mt_epi8()) plan->block = dim3(320);
+  // (BN = 64 with two CTAs per SM lost a CTA to the extra registers; the resident-weight
+  //  row kind runs one CTA per SM, so it always takes the eight drain warps.)
+  if ((pb.row || pb.mt) && a.tpc > 1 && pb.threads == 256 && (pb.bn >= 128 || pb.roww) && mt_epi8())
+    plan->block = dim3(320);
   // Split-K reduces through DSMEM inside a (1, 1, split_k) cluster when the
   // context can co-schedule such clusters; otherwise (e.g. a green context
   // split without SM co-scheduling) through the global workspace.
@@ -1620,6 +1638,13 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   }
   a.bar_off = (int)tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, a.cluster_red != 0, pb.row != 0);
   a.recv_off = (int)tc_ring_bytes(pb.bm, pb.bn, pb.bk, pb.stages, pb.row != 0);
+  a.roww = 0;
+  if (pb.roww) {   // [strip ring][nine resident weight taps][barriers]
+    a.roww = 1;
+    a.strip_woff = (int)((size_t)pb.stages * (((size_t)(pb.bm + 2) * 128 + 1023) / 1024 * 1024));
+    a.bar_off = a.strip_woff + 9 * pb.bn * 128;
+    a.recv_off = a.strip_woff;
+  }
   a.tab_off = a.bar_off + 1024;
   plan->smem = (size_t)a.tab_off + (pb.gather ? (size_t)pb.bm * 16 + (size_t)a.kblocks * pb.bk * 8 : 0);
   if (pb.row || pb.mt) {

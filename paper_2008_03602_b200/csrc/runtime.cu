@@ -438,7 +438,8 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     pb.ws_counters = s.split_k > 1 ? reinterpret_cast<int*>(wsb + wl.counters) : nullptr;
     pb.ws_partial = s.split_k > 1 ? reinterpret_cast<float*>(wsb + wl.partials) : nullptr;
     pb.gather = s.kind == TP_KIND_IGEMM_TC_GATHER ? 1 : 0;
-    pb.row = s.kind == TP_KIND_IGEMM_TC_ROW ? 1 : 0;
+    pb.row = (s.kind == TP_KIND_IGEMM_TC_ROW || s.kind == TP_KIND_IGEMM_TC_ROWW) ? 1 : 0;
+    pb.roww = s.kind == TP_KIND_IGEMM_TC_ROWW ? 1 : 0;
     pb.tpc = s.tiles_per_cta;
     pb.mt = s.kind == TP_KIND_IGEMM_TC_MT ? 1 : 0;
     pb.tf32 = s.kind == TP_KIND_IGEMM_TF32X3 ? 1 : 0;
@@ -461,7 +462,7 @@ static tp_status make_plan(const Layer& L, const tp_schedule& s_in, const void* 
     // partition once frozen, sm_tuned -- reading C15 -- else this partition's).
     {
       static const bool no_slots = getenv("TP_NO_SLOTS") && atoi(getenv("TP_NO_SLOTS")) != 0;
-      const bool multi = s.kind == TP_KIND_IGEMM_TC_ROW || s.kind == TP_KIND_IGEMM_TC_MT ||
+      const bool multi = s.kind == TP_KIND_IGEMM_TC_ROW || s.kind == TP_KIND_IGEMM_TC_ROWW || s.kind == TP_KIND_IGEMM_TC_MT ||
                          s.kind == TP_KIND_IGEMM_TC_STEM || s.kind == TP_KIND_IGEMM_TC_STRIP;
       const int sms = s.sm_tuned > 0 ? s.sm_tuned : sm_count;
       // Resident CTAs per SM: the occupancy calculator, capped by TMEM (512

@@ -163,6 +163,20 @@ static bool valid_mt(const Layer& L, int bm, int bn, int stages) {
   return 64 <= std::max<int64_t>(16, np2(L.d.c));
 }
 
+// Row-halo kind with resident weights (C = 64 layers): the 3 x 3 taps' BN x 64
+// weight tiles are loaded once per CTA and the ring carries input strips only,
+// so it can run several tiles ahead of the MMA (the strips of the large VGG
+// layers come from HBM; weight reloads were most of the L2 -> SMEM traffic).
+bool roww_kind_eligible(const Layer& L) { return row_kind_eligible(L) && L.d.c == 64; }
+static const int kRowwStages[] = {2, 4, 6, 8};
+static const int kRowwTpc[] = {2, 4, 8, 16};
+int64_t row_strip_bytes(int bm) { return (((int64_t)(bm + 2) * 128) + 1023) / 1024 * 1024; }
+static bool valid_roww(const Layer& L, int bm, int bn, int stages) {
+  if ((int64_t)stages * row_strip_bytes(bm) + 9 * (int64_t)bn * 128 + 1024 > kSmemLimit) return false;
+  if (bm > np2(L.Q)) return false;
+  return bn <= std::max<int64_t>(32, np2(L.d.k));
+}
+
 static const int kRowBM[] = {64, 128};
 static const int kRowStages[] = {1, 2, 3};
 static const int kRowTpc[] = {1, 2, 4, 8, 16};
@@ -280,7 +294,7 @@ void fill_geometry(const Layer& L, tp_schedule* s) {
     s->grid_x = (int32_t)cdiv(cdiv(L.M, s->bm), std::max(1, s->tiles_per_cta));
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = 1;
-  } else if (s->kind == TP_KIND_IGEMM_TC_ROW) {
+  } else if (s->kind == TP_KIND_IGEMM_TC_ROW || s->kind == TP_KIND_IGEMM_TC_ROWW) {
     s->grid_x = (int32_t)cdiv((int64_t)L.d.n * L.P * cdiv(L.Q, s->bm), std::max(1, s->tiles_per_cta));
     s->grid_y = (int32_t)cdiv(L.d.k, s->bn);
     s->grid_z = 1;
@@ -321,6 +335,15 @@ static void enumerate(const Layer& L, F visit) {
           s.threads = th; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
           if (!visit(s)) return;
         }
+    // ... then the row-halo kind with resident weights (C = 64).
+    if (roww_kind_eligible(L))
+      for (int bm : kRowBM) for (int bn : kTcBN) for (int st : kRowwStages) for (int tpc : kRowwTpc) {
+        if (!valid_roww(L, bm, bn, st)) continue;
+        tp_schedule s; std::memset(&s, 0, sizeof(s));
+        s.kind = TP_KIND_IGEMM_TC_ROWW; s.bm = bm; s.bn = bn; s.bk = 64; s.stages = st;
+        s.threads = 256; s.split_k = 1; s.tiles_per_cta = tpc; s.space_index = idx++;
+        if (!visit(s)) return;
+      }
     // Gathered stems append the stem kind (after every gathered tuple).
     if (stem_kind_eligible(L))
       for (int bm : kStemBM) for (int bn : kStemBN) for (int tpc : kStemTpc) {
@@ -404,6 +427,10 @@ bool schedule_in_space(const Layer& L, const tp_schedule& s) {
     return row_kind_eligible(L) && in_(s.bm, kRowBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 64 &&
            in_(s.stages, kRowStages, 3) && in_(s.threads, kTcThreads, 2) && s.split_k == 1 &&
            in_(s.tiles_per_cta, kRowTpc, 5) && valid_row(L, s.bm, s.bn, s.stages, s.threads, s.tiles_per_cta);
+  if (s.kind == TP_KIND_IGEMM_TC_ROWW)
+    return roww_kind_eligible(L) && in_(s.bm, kRowBM, 2) && in_(s.bn, kTcBN, 4) && s.bk == 64 &&
+           in_(s.stages, kRowwStages, 4) && s.threads == 256 && s.split_k == 1 &&
+           in_(s.tiles_per_cta, kRowwTpc, 4) && valid_roww(L, s.bm, s.bn, s.stages);
   if (s.kind == TP_KIND_IGEMM_TC_STEM)
     return stem_kind_eligible(L) && in_(s.bm, kStemBM, 2) && in_(s.bn, kStemBN, 3) && s.bk == stem_kp(L) &&
            s.stages == 2 && s.threads == 256 && s.split_k == 1 && in_(s.tiles_per_cta, kStemTpc, 4) &&

@@ -36,6 +36,8 @@ int64_t direct_smem_bytes(const Layer& L, int threads, int tile_q, int vec_k, in
 int64_t tc_smem_bytes(int bm, int bn, int bk, int stages);
 int64_t tcg_table_bytes(const Layer& L, int bm, int bk);   // gather kind: pixel + k tables
 bool row_kind_eligible(const Layer& L);                     // row-halo kind applies
+bool roww_kind_eligible(const Layer& L);                    // row-halo kind with resident weights (C = 64)
+int64_t row_strip_bytes(int bm);                            // row-halo kinds: one input strip (1 KiB multiple)
 bool mt_kind_eligible(const Layer& L);                      // multi-tile im2col kind applies
 bool tf32_kind_eligible(const Layer& L);
 bool stem_kind_eligible(const Layer& L);                    // stem kind applies (C < 8 gathered layers)

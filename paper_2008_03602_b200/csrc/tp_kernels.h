@@ -91,6 +91,7 @@ struct TcArgs {
   int strip_stage;             // strip kind: bytes of one ring stage (s_w phase boxes)
   int strip_woff;              // strip kind: byte offset of the resident weights
   int ystage2;                 // multi-tile kinds: two y staging buffers (TMA-store epilogue)
+  int roww;                    // row-halo kind: weights resident at strip_woff (ring = strips only)
 };
 
 struct TcProblem {
@@ -113,6 +114,7 @@ struct TcProblem {
   int tf32;        // 1: TP_KIND_IGEMM_TF32X3 (fp32 NHWC x, KRSC w; 3xTF32 split)
   int stem;        // 1: TP_KIND_IGEMM_TC_STEM (C < 8 stems: staged input patch, resident weights)
   int strip;       // 1: TP_KIND_IGEMM_TC_STRIP (x, w padded to 8 channels in the workspace)
+  int roww;        // 1: TP_KIND_IGEMM_TC_ROWW (row-halo with resident weights; row = 1 too)
 };
 
 struct TcPlan {

@@ -28,7 +28,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 OK, EINVAL, EINVALID_CONFIG, ECAPACITY, ECUDA, EMISMATCH, EUNSUPPORTED = range(7)
 (KIND_IGEMM_TC, KIND_DIRECT, KIND_IGEMM_TC_GATHER, KIND_IGEMM_TC_ROW, KIND_IGEMM_TC_MT, KIND_IGEMM_TF32X3,
- KIND_IGEMM_TC_STEM, KIND_IGEMM_TC_STRIP) = range(8)
+ KIND_IGEMM_TC_STEM, KIND_IGEMM_TC_STRIP, KIND_IGEMM_TC_ROWW) = range(9)
 NHWC, NCHW = 0, 1
 BF16, FP32 = 0, 1
 PART_FINE_GRAINED = 1

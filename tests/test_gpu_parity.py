@@ -403,7 +403,7 @@ def test_multitile_tma_store_epilogue_in_partition(d):
     bad, n = [], 0
     for i in range(tp.space_size(d)):
         s = tp.space_get(d, i)
-        if s["kind"] not in (tp.KIND_IGEMM_TC_ROW, tp.KIND_IGEMM_TC_MT):
+        if s["kind"] not in (tp.KIND_IGEMM_TC_ROW, tp.KIND_IGEMM_TC_ROWW, tp.KIND_IGEMM_TC_MT):
             continue
         n += 1
         buf.poison()
@@ -433,7 +433,7 @@ def test_multitile_balanced_spans_bit_exact(d, sm_tuned):
     bad, n = [], 0
     for i in range(tp.space_size(d)):
         s = tp.space_get(d, i)
-        if s["kind"] not in (tp.KIND_IGEMM_TC_ROW, tp.KIND_IGEMM_TC_MT, tp.KIND_IGEMM_TC_STEM) or \
+        if s["kind"] not in (tp.KIND_IGEMM_TC_ROW, tp.KIND_IGEMM_TC_ROWW, tp.KIND_IGEMM_TC_MT, tp.KIND_IGEMM_TC_STEM) or \
                 s["tiles_per_cta"] < 2:
             continue
         s = dict(s, sm_tuned=sm_tuned)

@@ -98,7 +98,7 @@ def test_space_counts_and_order():
         rest = [d for d in cat if sp.layer_kind(d) != sp.KIND_IGEMM_TC_GATHER]
         assert len(stems) == 1 and stems[0]["c"] == 3
         n_rest = sum(1 for d in rest for x in sp.enumerate_space(d)
-                     if x["kind"] not in (sp.KIND_IGEMM_TC_ROW, sp.KIND_IGEMM_TC_MT))
+                     if x["kind"] not in (sp.KIND_IGEMM_TC_ROW, sp.KIND_IGEMM_TC_ROWW, sp.KIND_IGEMM_TC_MT))
         assert n_rest + _direct_count(stems[0]) == total
     d = wl.catalog("resnet50")[2]
     s = sp.enumerate_space(d)
@@ -146,6 +146,24 @@ def test_stem_kind_hand_count():
     assert not sp.stem_eligible(wl.catalog("resnet50")[1])
     assert not sp.stem_eligible(dict(v, h=32, w=32))
     assert not sp.stem_eligible(dict(v, c=6, r=7, s=7))
+
+
+def test_roww_kind_hand_count():
+    # Row-halo kind with resident weights (C = 64 row-halo layers), appended right after the row-halo
+    # tuples.  VGG conv1_2 (Q = 224, K = 64): BM {64, 128}, BN {32, 64}, stages {2, 4, 6, 8},
+    # tiles_per_cta {2, 4, 8, 16}; the largest (BM 128, BN 64, 8 strips): 8 x 17 KiB + 9 x 64 x 128 + 1 KiB
+    # = 139264 + 73728 + 1024 = 214016 fits -> 2 x 2 x 4 x 4 = 64.  conv2_1 (K = 128): BN = 128 weights are
+    # 147456 B, so with BM = 128 (17 KiB strips) only 2 or 4 stages fit (6 x 17408 + 147456 + 1024 > 232448):
+    # BN 32/64 -> 2 x 2 x 4 x 4 = 64, BN 128 -> (BM 64: 9 KiB strips, all 4 stages; BM 128: 2) x 4 = 24 -> 88.
+    v = wl.catalog("vgg19_b16")
+    for d, n in ((v[1], 64), (v[2], 88)):
+        space = sp.enumerate_space(d)
+        rw = [x for x in space if x["kind"] == sp.KIND_IGEMM_TC_ROWW]
+        row = [i for i, x in enumerate(space) if x["kind"] == sp.KIND_IGEMM_TC_ROW]
+        assert len(rw) == n and space[row[-1] + 1:row[-1] + 1 + n] == rw
+        assert all(x["bk"] == 64 and x["threads"] == 256 and x["split_k"] == 1 for x in rw)
+    assert not sp.roww_eligible(v[3])             # conv2_2: C = 128
+    assert [d["name"] for d in wl.catalog("resnet50") if sp.roww_eligible(d)] == ["r50.l1.b0.c2"]   # Q = 56, C = 64
 
 
 def test_strip_kind_hand_count():
