@@ -524,6 +524,20 @@ def main():
                                       "peak, measured empty-kernel launch floor) / sum of their tuned latencies",
                  "traffic_capture": cap})
 
+    # ---------------- measured model latency: the 53 layers as one graph (reading C21, f2) ----------------
+    model_chain = None
+    if args.workload == "resnet50":
+        names = {d["name"]: li for li, d in enumerate(layers)}
+        seq = [names[n] for n in wl.resnet50_sequence()]
+        if all((0, li) in best for li in seq):
+            mc = tp.chain_run([bufs[(0, li)] for li in seq],
+                              [tp.space_get(layers[li], best[(0, li)]["space_index"]) for li in seq], part, reps=4,
+                              timing_cfg=tp.timing())
+            model_chain = {"layers": len(seq), "median_us": round(mc["median_us"], 2),
+                           "min_us": round(mc["min_us"], 2), "sum_of_layer_latencies_us": round(lat_sum, 2),
+                           "note": "tp_chain_run: the 53 ResNet-50 convs in execution order (each its own operands) "
+                                   "captured as one CUDA graph with PDL between launches, 4 passes per timed group"}
+
     # ---------------- extras (N = 1): the rest of the metric on this box, clocks sampled ----------------
     extras = None
     if world == 1 and not args.no_extras and args.workload == "resnet50":
@@ -570,7 +584,7 @@ def main():
                        "gate": "fp64 oracle points (refs/, 4096 per layer) at 2e-2 / 1e-5",
                        "parallelism": f"candidate-shard x{world}"},
             "latency_us": {"model_sum_tuned": round(lat_sum, 2), "at_fraction": args.fraction,
-                           "per_layer": per_layer},
+                           "model_chain": model_chain, "per_layer": per_layer},
             "candidates_ok": n_ok, "candidates_total": len(recs),
             "raced_frac": round(shard.raced_frac(recs), 4),
             "gpu_busy_frac": round(busy / (el_ms / steps), 3),

@@ -102,3 +102,19 @@ def layer_dict(entry, dtype: int, relu: bool = True, bias: bool = True, layout: 
 def catalog(name: str, relu: bool = True, bias: bool = True) -> list[dict]:
     entries, dtype = CATALOGS[name]
     return [layer_dict(e, dtype, relu, bias) for e in entries]
+
+
+def resnet50_sequence() -> list[str]:
+    """The 53 conv layers of ResNet-50 v1.5 in execution order, as unique-layer
+    names of RESNET50 (each bottleneck block runs c1, c2, c3, then the
+    downsample projection of its first block; torchvision's forward order)."""
+    seq = ["r50.conv1"]
+    for stage, blocks in (("l1", 3), ("l2", 4), ("l3", 6), ("l4", 3)):
+        for b in range(blocks):
+            if b == 0:
+                seq += [f"r50.{stage}.b0.c1", f"r50.{stage}.b0.c2", f"r50.{stage}.b0.c3"]
+                seq.append("r50.l1.b0.c3" if stage == "l1" else f"r50.{stage}.b0.ds")
+            else:
+                c3 = "r50.l1.b0.c3" if stage == "l1" else f"r50.{stage}.b0.c3"
+                seq += [f"r50.{stage}.b1.c1", "r50.l1.b0.c2" if stage == "l1" else f"r50.{stage}.b1.c2", c3]
+    return seq

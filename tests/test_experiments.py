@@ -86,3 +86,14 @@ def test_pd_check_flags_a_diagonal_above_its_column():
     # the same gap is noise when the cells' CV is 2%: eps = 0.06 and 10.0 <= 9.5 x 1.06
     assert ex.pd_check([row({(0.1, 0.1): 10.0, (1.0, 0.1): 9.5, (0.1, 1.0): 5.0, (1.0, 1.0): 4.0}, 0.02)],
                        fr)["pass"]
+
+
+def test_resnet50_sequence_matches_multiplicities():
+    import collections
+    seq = wl.resnet50_sequence()
+    cnt = collections.Counter(seq)
+    assert len(seq) == 53 and seq[0] == "r50.conv1"
+    assert all(cnt[d["name"]] == d["mult"] for d in wl.catalog("resnet50"))
+    # each stage's first block ends with its downsample projection (torchvision order)
+    assert seq[1:5] == ["r50.l1.b0.c1", "r50.l1.b0.c2", "r50.l1.b0.c3", "r50.l1.b0.c3"]
+    assert seq[seq.index("r50.l4.b0.c1") + 3] == "r50.l4.b0.ds"
