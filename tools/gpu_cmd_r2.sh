@@ -1,4 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider > gpurun_out/r2_gpu_all3.log 2>&1; tail -3 gpurun_out/r2_gpu_all3.log
-timeout 1500 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r2_bench3.json 2> gpurun_out/r2_bench3.err; tail -c 300 gpurun_out/r2_bench3.err
-timeout 600 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/r2_ref3.json 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1; tail -3 gpurun_out/r2_smoke.log
+for i in 511 515; do python tools/mt_trace.py vgg19_b16 vgg.64.224.1 $i 0.25; done > gpurun_out/r2_mt_trace5.log 2>&1
+cat gpurun_out/r2_mt_trace5.log
