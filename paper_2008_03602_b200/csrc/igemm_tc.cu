@@ -628,7 +628,9 @@ template <int BM, int BN, int BK, int KM>
 __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
                                                        const __grid_constant__ CUtensorMap tmY, TcArgs a) {
-  constexpr bool ROW = KM == 1, STRIP = KM == 2;
+  // KM 3 = the row-halo kind's CTA-pair form: a separate instantiation, since a kernel
+  // containing cta_group::2 instructions must be launched with clusters of 2.
+  constexpr bool ROW = KM == 1 || KM == 3, STRIP = KM == 2, PAIR = KM == 3;
   static_assert(!ROW || BK == 64, "row-halo k-blocks are 64 channels");
   constexpr int SUBK = BK < 64 ? BK : 64;
   constexpr int NSUB = BK / SUBK;
@@ -643,10 +645,19 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
                                  : (ROW ? (BM + 2) * 128 : A_SUB * NSUB);   // expect_tx of the A part
   constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
+  // CTA pair (ROW + roww + a.pair2): one cta_group::2 MMA of 2 BM rows x BN over the
+  // (2, 1, 1) cluster -- each CTA holds its own tile's strips (A rows) and half of
+  // the weight rows (BN / 2 per tap); rank 0 issues, both TMEMs receive their rows.
+  constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                              ((uint32_t)((2 * BM) >> 4) << 24);
+  constexpr uint32_t B_TAP_HALF = (BN / 2) * 128;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int stages = a.stages;
+  constexpr bool pair = PAIR;
+  const uint32_t prank = pair ? cluster_ctarank() : 0u;
+  const uint32_t w_tap = pair ? B_TAP_HALF : B_TAP;   // resident weight bytes per tap in this CTA
   uint8_t* a_tiles = smem_raw;
   uint8_t* b_tiles = a_tiles + (size_t)stages * A_STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + a.bar_off);
@@ -661,7 +672,15 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
   const int tpc = a.tpc;
   const bool split_roles = tpc > 1;     // warps 2..7 drain while warps 0/1 run ahead
   int tile0, ntl;
-  tile_span(a.ntiles, tpc, a.slots, tile0, ntl);
+  if (pair) {
+    // cluster c runs pair steps u in [c tpc, c tpc + tpc); step u = tiles 2u (rank 0), 2u + 1 (rank 1);
+    // both CTAs of a cluster get the same count (they return together or not at all)
+    const int npairs = (a.ntiles + 1) / 2, u0 = (int)(blockIdx.x >> 1) * tpc;
+    ntl = npairs - u0 < tpc ? npairs - u0 : tpc;
+    tile0 = 2 * u0 + (int)prank;
+  } else {
+    tile_span(a.ntiles, tpc, a.slots, tile0, ntl);
+  }
   if (ntl <= 0) return;                 // past the resident slots (whole CTA, before any barrier)
   const int nbase = blockIdx.y * BN;
   const int kpt = a.kblocks;            // k-blocks per tile = (C / 64) * 3
@@ -731,7 +750,11 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
     for (int i = 0; i < stages; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, (uint32_t)n_epi_warps); }
+    // pair: the leader's tempty counts both CTAs' drain warps (they arrive remotely)
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull + i, 1);
+      mbar_init(tempty + i, (uint32_t)(pair ? 2 * n_epi_warps : n_epi_warps));
+    }
     mbar_init(wfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmA);
@@ -748,14 +771,22 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(ncols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (pair) {   // the same warp of both CTAs, the same columns
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(ncols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(ncols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (pair) cluster_sync_all();   // both CTAs' barriers exist before any cross-CTA signal
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   if (trace && threadIdx.x == 0) trace[1] = gtimer();
 
@@ -766,7 +797,12 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     auto issue = [&](int stage, int cb, int r, int sx, int q0, int p0, int n0, int m0, int parts) {
       uint8_t* sa = a_tiles + (size_t)stage * A_STAGE;
       uint8_t* sb = b_tiles + (size_t)stage * B_STAGE;
-      if (parts & 4) mbar_arrive_expect_tx_p(full + stage, A_BYTES + ((parts & 2) ? B_STAGE : 0u), lead);
+      if (parts & 4) {
+        if (!pair)
+          mbar_arrive_expect_tx_p(full + stage, A_BYTES + ((parts & 2) ? B_STAGE : 0u), lead);
+        else if (prank == 0)   // the leader's barrier counts both CTAs' strips
+          mbar_arrive_expect_tx_p(full + stage, 2 * A_BYTES, lead);
+      }
       if constexpr (STRIP) {
         // filter row r: one strip per column phase (the weights are resident).
         // s_w = 1: the strip is contiguous in the padded row, loaded as 512-byte
@@ -785,7 +821,12 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
         }
       } else if constexpr (ROW) {
         // (channel block cb, filter row r): the input strip + the three taps
-        if (parts & 1) tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
+        if (parts & 1) {
+          if (pair)
+            tma_load_tile_4d_pair_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
+          else
+            tma_load_tile_4d_p(sa, &tmA, full + stage, cb * 64, q0 - 1, p0 + r - 1, n0, lead);
+        }
         if ((parts & 2) && !a.roww) {
 #pragma unroll
           for (int ss = 0; ss < 3; ++ss)
@@ -836,10 +877,18 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       for (int r = 0; r < a.R; ++r) tma_load_tile_4d_p(w_res + (size_t)r * w_row, &tmB, wfull, 0, nbase, 0, r, lead);
     } else if constexpr (ROW) {
       if (a.roww) {   // resident weights (C = 64): the nine taps, once
-        mbar_arrive_expect_tx_p(wfull, 9u * B_TAP, lead);
-        for (int r = 0; r < 3; ++r)
-          for (int ss = 0; ss < 3; ++ss)
-            tma_load_tile_4d_p(w_res + (size_t)(r * 3 + ss) * B_TAP, &tmB, wfull, 0, ss, r, nbase, lead);
+        if (!pair) {
+          mbar_arrive_expect_tx_p(wfull, 9u * B_TAP, lead);
+          for (int r = 0; r < 3; ++r)
+            for (int ss = 0; ss < 3; ++ss)
+              tma_load_tile_4d_p(w_res + (size_t)(r * 3 + ss) * B_TAP, &tmB, wfull, 0, ss, r, nbase, lead);
+        } else {      // each CTA its half of the weight rows, counted on the leader's barrier
+          if (prank == 0) mbar_arrive_expect_tx_p(wfull, 9u * B_TAP, lead);
+          for (int r = 0; r < 3; ++r)
+            for (int ss = 0; ss < 3; ++ss)
+              tma_load_tile_4d_pair_p(w_res + (size_t)(r * 3 + ss) * B_TAP_HALF, &tmB, wfull, 0, ss, r,
+                                      nbase + (int)prank * (BN / 2), lead);
+        }
       }
     }
     int stage = 0;
@@ -849,6 +898,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       int q0, p0, n0, mrow0, mvalid;
       tile_coords(cur, q0, p0, n0, mrow0, mvalid);
       cursor_next(cur);
+      if (pair) cursor_next(cur);
       int cb = 0, r = 0, sx = 0;
       for (int kb = 0; kb < kpt; ++kb) {
         TP_MT_WAIT(empty + stage, phase ^ 1u);
@@ -863,7 +913,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       }
       if (trace && lane == 0 && i < 8) trace[4 + i] = gtimer();    // tile i's loads issued
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && prank == 0) {
     // ---------------- MMA issuer: two accumulators, alternating per tile ----------------
     const uint32_t lead = elect_one();
     const uint64_t adesc0 = STRIP ? make_sdesc_plain(smem_u32(a_tiles), 16u, 128u) : make_sdesc(smem_u32(a_tiles), SWZ);
@@ -888,7 +938,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
         tc_fence_after();
         const uint64_t ad = adesc0 + ((uint32_t)(stage * A_STAGE) >> 4);
         // roww: the weights of filter row kb (C = 64: one channel block) are resident
-        const uint64_t bd = (ROW && a.roww) ? bdesc0 + ((uint32_t)(kb * 3 * B_TAP) >> 4)
+        const uint64_t bd = (ROW && a.roww) ? bdesc0 + ((uint32_t)(kb * 3 * w_tap) >> 4)
                                             : bdesc0 + ((uint32_t)(stage * B_STAGE) >> 4);
         if constexpr (STRIP) {
           // filter row kb: per phase f, tap pairs (t, t + 1), t even; tap s = f + s_w t
@@ -902,13 +952,24 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
                        lead);
           }
         } else if constexpr (ROW) {
+          const uint32_t tap = a.roww ? w_tap : B_TAP;
+          if (pair) {
 #pragma unroll
-          for (int ss = 0; ss < 3; ++ss)
+            for (int ss = 0; ss < 3; ++ss)
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              tc_mma_p(dcol, ad + ((uint32_t)(ss * 128 + kk * 32) >> 4),
-                       bd + ((uint32_t)(ss * B_TAP + kk * 32) >> 4), IDESC, (kb > 0 || ss > 0 || kk > 0) ? 1u : 0u,
-                       lead);
+              for (int kk = 0; kk < 4; ++kk)
+                tc_mma_pair_p(dcol, ad + ((uint32_t)(ss * 128 + kk * 32) >> 4),
+                              bd + ((uint32_t)(ss * tap + kk * 32) >> 4), IDESC2,
+                              (kb > 0 || ss > 0 || kk > 0) ? 1u : 0u, lead);
+          } else {
+#pragma unroll
+            for (int ss = 0; ss < 3; ++ss)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                tc_mma_p(dcol, ad + ((uint32_t)(ss * 128 + kk * 32) >> 4),
+                         bd + ((uint32_t)(ss * tap + kk * 32) >> 4), IDESC, (kb > 0 || ss > 0 || kk > 0) ? 1u : 0u,
+                         lead);
+          }
         } else {
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
@@ -918,10 +979,10 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
                      (kb > 0 || kk > 0) ? 1u : 0u, lead);
           }
         }
-        tc_commit_p(empty + stage, lead);
+        if (pair) tc_commit_pair_p(empty + stage, lead); else tc_commit_p(empty + stage, lead);
         if (++stage == stages) { stage = 0; phase ^= 1u; }
       }
-      tc_commit_p(tfull + buf, lead);
+      if (pair) tc_commit_pair_p(tfull + buf, lead); else tc_commit_p(tfull + buf, lead);
       if (trace && lane == 0 && i < 8) trace[12 + i] = gtimer();   // tile i's MMAs issued
     }
   }
@@ -968,6 +1029,10 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       int q0, p0, n0, mrow0, mvalid;
       tile_coords(cur, q0, p0, n0, mrow0, mvalid);
       cursor_next(cur);
+      if (pair) {
+        cursor_next(cur);
+        if (tile0 + 2 * i >= a.ntiles) mvalid = 0;   // odd tile count: rank 1's last tile is empty
+      }
       // a.ystage2: two staging buffers alternate, so only the store of tile i - 2
       // must have read this one (one bulk group may stay in flight)
       uint8_t* stg_t = stg + (a.ystage2 ? (size_t)buf * ystage : 0);
@@ -1083,7 +1148,12 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + buf);
+      if (lane == 0) {
+        if (pair)
+          mbar_arrive_remote(tempty + buf, 0);   // the leader's MMA thread waits for both CTAs
+        else
+          mbar_arrive(tempty + buf);
+      }
       if (trace && (int)threadIdx.x == issuer && i < 8) trace[20 + i] = gtimer();   // tile i drained (issuer warp)
       if (a.y_tma) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1109,7 +1179,15 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
   tc_fence_before();
   __syncthreads();
   if (trace && threadIdx.x == 0) trace[3] = gtimer();
-  if (warp == 2) {
+  if (pair) {
+    // the leader's MMAs wrote this CTA's TMEM and its drain warps arrived on the
+    // leader's barriers: both CTAs are done with each other before the free
+    cluster_sync_all();
+    if (warp == 2) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols) : "memory");
+    }
+  } else if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols) : "memory");
   }
@@ -1122,6 +1200,9 @@ template <int BM, int BN, int MODE>
 static KernelFn pick_bk(int bk) {
   if constexpr (MODE == 4) {
     if constexpr (BN <= 128) return bk == 16 ? igemm_mt_kernel<BM, BN, 16, 2> : nullptr;
+    return nullptr;
+  } else if constexpr (MODE == 5) {   // row-halo, resident weights, CTA pair (BM = 128)
+    if constexpr (BM == 128 && BN <= 128) return bk == 64 ? igemm_mt_kernel<BM, BN, 64, 3> : nullptr;
     return nullptr;
   } else if constexpr (MODE == 2) {
     return bk == 64 ? igemm_mt_kernel<BM, BN, 64, 1> : nullptr;
@@ -1146,7 +1227,8 @@ static KernelFn pick_bk(int bk) {
 static KernelFn pick_tc(int bm, int bn, int bk, int mode) {
 #define TP_TC_CASE(M_, N_)                                                                       \
   if (bm == M_ && bn == N_)                                                                      \
-    return mode == 4 ? pick_bk<M_, N_, 4>(bk)                                                    \
+    return mode == 5 ? pick_bk<M_, N_, 5>(bk)                                                    \
+                     : mode == 4 ? pick_bk<M_, N_, 4>(bk)                                        \
                      : mode == 3 ? pick_bk<M_, N_, 3>(bk)                                        \
                      : (mode == 2 ? pick_bk<M_, N_, 2>(bk)                                       \
                                   : (mode == 1 ? pick_bk<M_, N_, 1>(bk) : pick_bk<M_, N_, 0>(bk)));
@@ -1175,6 +1257,11 @@ static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red, b
 
 static bool ystage2_enabled() {
   static const bool on = !(getenv("TP_YSTAGE2") && atoi(getenv("TP_YSTAGE2")) == 0);
+  return on;
+}
+
+static bool roww_pair_enabled() {
+  static const bool on = getenv("TP_ROWW2") && atoi(getenv("TP_ROWW2")) != 0;
   return on;
 }
 
@@ -1490,7 +1577,9 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     cuuint64_t b_dims[4] = {(cuuint64_t)pb.C, (cuuint64_t)pb.S, (cuuint64_t)pb.R, (cuuint64_t)pb.K};
     cuuint64_t b_strides[3] = {(cuuint64_t)pb.C * 2, (cuuint64_t)pb.S * pb.C * 2,
                                (cuuint64_t)pb.R * pb.S * pb.C * 2};
-    cuuint32_t b_box[4] = {64, 1, 1, (cuuint32_t)pb.bn};
+    // CTA pair (resident-weight row kind): each CTA loads half of the BN weight rows
+    const bool pair2 = pb.roww && pb.bm == 128 && pb.bn <= 128 && roww_pair_enabled();
+    cuuint32_t b_box[4] = {64, 1, 1, (cuuint32_t)(pair2 ? pb.bn / 2 : pb.bn)};
     r = drv.encodeTiled(&plan->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.w), b_dims, b_strides,
                         b_box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1616,6 +1705,7 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
                              (unsigned)pb.split_k);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
   plan->block = dim3(pb.threads);
+  plan->cluster_x = 1;
   // Multi-tile kinds with tiles_per_cta > 1: two more drain warps, so each TMEM
   // lane quadrant has two (the knob stays 256 threads; TP_EPI8=0 turns it off).
   // (BN = 64 with two CTAs per SM lost a CTA to the extra registers; the resident-weight
@@ -1639,11 +1729,20 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.bar_off = (int)tc_bar_off(pb.bm, pb.bn, pb.bk, pb.stages, a.cluster_red != 0, pb.row != 0);
   a.recv_off = (int)tc_ring_bytes(pb.bm, pb.bn, pb.bk, pb.stages, pb.row != 0);
   a.roww = 0;
+  a.pair2 = 0;
   if (pb.roww) {   // [strip ring][nine resident weight taps][barriers]
     a.roww = 1;
+    a.pair2 = (pb.bm == 128 && pb.bn <= 128 && roww_pair_enabled()) ? 1 : 0;   // CTA pair: half the weight rows each
     a.strip_woff = (int)((size_t)pb.stages * (((size_t)(pb.bm + 2) * 128 + 1023) / 1024 * 1024));
-    a.bar_off = a.strip_woff + 9 * pb.bn * 128;
+    a.bar_off = a.strip_woff + 9 * pb.bn * (a.pair2 ? 64 : 128);
     a.recv_off = a.strip_woff;
+    if (a.pair2) {   // (2, 1, 1) clusters; cluster c runs tile pairs [c tpc, c tpc + tpc)
+      const int npairs = (a.ntiles + 1) / 2;
+      plan->grid.x = 2u * (unsigned)((npairs + a.tpc - 1) / a.tpc);
+      plan->cluster_x = 2;
+      plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, 64, 5));
+      if (!plan->fn) { set_error("no CTA-pair row instantiation for this BM x BN"); return TP_EINVALID_CONFIG; }
+    }
   }
   a.tab_off = a.bar_off + 1024;
   plan->smem = (size_t)a.tab_off + (pb.gather ? (size_t)pb.bm * 16 + (size_t)a.kblocks * pb.bk * 8 : 0);
@@ -1708,7 +1807,13 @@ cudaError_t tc_launch(const TcPlan& plan, cudaStream_t stream) {
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
-  if (plan.cluster_z > 1) {
+  if (plan.cluster_x > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)plan.cluster_x;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  } else if (plan.cluster_z > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
     attr[na].val.clusterDim.x = 1;
     attr[na].val.clusterDim.y = 1;

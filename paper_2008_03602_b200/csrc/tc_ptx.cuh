@@ -160,6 +160,56 @@ static __device__ __forceinline__ void tc_commit_p(uint64_t* bar, uint32_t lead)
       "r"(lead)
       : "memory");
 }
+// ---- CTA pair (cta_group::2): one 256-row MMA over two SMs of a TPC ----
+// Both CTAs of the (2, 1, 1) cluster load their own half; the TMA completes its
+// bytes on CTA 0's mbarrier (bit 24 of the shared::cluster address selects the
+// peer; cleared = rank 0), which the leader's MMA thread waits on.
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
+static __device__ __forceinline__ void tma_load_tile_4d_pair_p(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                               int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                                               uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %7, 0;\n\t"
+      "@q cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(lead)
+      : "memory");
+}
+static __device__ __forceinline__ void tc_mma_pair_p(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                     uint32_t accumulate, uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@q tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(lead)
+      : "memory");
+}
+// Commit the leader's MMAs to the barrier at the same offset in both CTAs.
+static __device__ __forceinline__ void tc_commit_pair_p(uint64_t* bar, uint32_t lead) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %2;\n\t}"
+      ::"r"(smem_u32(bar)), "r"(lead), "h"((uint16_t)3)
+      : "memory");
+}
+// Arrive on the barrier at this offset in cluster CTA `rank` (release, cluster scope).
+static __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+static __device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+static __device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 static __device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));

@@ -92,6 +92,7 @@ struct TcArgs {
   int strip_woff;              // strip kind: byte offset of the resident weights
   int ystage2;                 // multi-tile kinds: two y staging buffers (TMA-store epilogue)
   int roww;                    // row-halo kind: weights resident at strip_woff (ring = strips only)
+  int pair2;                   // roww, BM = 128: CTA pair, cta_group::2 MMAs of 256 rows ((2,1,1) cluster)
 };
 
 struct TcProblem {
@@ -125,6 +126,7 @@ struct TcPlan {
   dim3 grid, block;
   size_t smem = 0;
   int cluster_z = 1;
+  int cluster_x = 1;   // roww CTA pairs: (2, 1, 1) clusters
 };
 
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan);

@@ -506,3 +506,45 @@ def test_strip_full_size_vs_oracle(cat, li, cfg):
         tp.conv2d_run(buf, s)
         torch.cuda.synchronize()
         assert rel_err(buf.gather(idx), ref) <= 2e-2, s
+
+
+# ------------------------------------------------------------------ row-halo with resident weights (kind 8)
+ROWW_TINY = [mk(2, 64, 5, 130, 48, 3, 3, 1, 1, out=tp.FP32, epi=1),    # BM 128 fits (Q = 130), 20 tiles
+             mk(1, 64, 5, 100, 40, 3, 3, 1, 1, out=tp.FP32, epi=1),    # one q-block per row: 5 tiles (odd)
+             mk(1, 64, 6, 60, 64, 3, 3, 1, 1, epi=3)]                  # bf16 output, BM 64 only
+
+
+@pytest.mark.parametrize("d", ROWW_TINY, ids=lambda d: f"roww_{d['n']}x{d['h']}x{d['w']}_k{d['k']}_o{d['out_dtype']}")
+def test_roww_every_schedule_bit_exact_integer(d):
+    """Every resident-weight row-halo schedule (and, with TP_ROWW2=1 in the
+    environment, its CTA-pair cta_group::2 form for BM = 128) equals the oracle
+    (bit for bit with fp32 output, within one bf16 rounding otherwise), also
+    with the geometry frozen at a few SMs and in a 25% partition."""
+    x, w, b = datagen.make_inputs(d, 81, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    part = tp.Partition.get(0.25)
+    buf = tp.LayerBuffers(d, x, w, b, part=part)
+    scheds = kinds_of(d).get(tp.KIND_IGEMM_TC_ROWW, [])
+    assert scheds
+    bad = []
+    for s in scheds:
+        for sm_tuned in (0, 3):
+            buf.poison()
+            tp.conv2d_run(buf, dict(s, sm_tuned=sm_tuned), part)
+            part.sync()
+            y = buf.output()
+            ok = np.array_equal(y, ref) if d["out_dtype"] == tp.FP32 else rel_err(y, ref) <= 2 ** -8
+            if not ok:
+                bad.append((s["space_index"], s["bm"], s["bn"], s["stages"], s["tiles_per_cta"], sm_tuned))
+    assert not bad, f"{len(bad)} schedules differ, first: {bad[:5]}"
+
+
+def test_roww_cta_pair_variant_bit_exact():
+    """The CTA-pair (cta_group::2, 256-row MMA) form of the resident-weight
+    row-halo kind is an experiment switched on by TP_ROWW2=1 (read once per
+    process): run the resident-weight bit-exact test in a child process with it."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_r2.py", "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", "test_roww_every_schedule_bit_exact_integer"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=900, env=dict(os.environ, TP_ROWW2="1"))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "3 passed" in r.stdout
