@@ -1512,6 +1512,45 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   a.recv_off = (a.tab_off + kp * 4 + 1023) / 1024 * 1024;
   a.bar_off = a.recv_off + (int)stg;
   {
+    // Wide path (TcArgs::wide): when s_w C_w = 8 for some C_w in {2, 4, 8} >= C,
+    // input row segments are widened to C_w-element (16 / s_w-byte) pixels in a
+    // ring of NS = R + 2 s_h slots and read by the MMAs in place.  Layout:
+    // [B, K_P' = 64 ceil(R K_r / 64)][ring slots, output staging -- or the raw
+    // weights while they are repacked][4 R raw row buffers][barriers | bias at +512].
+    static const int dbg = getenv("TP_STEM_DBG") ? atoi(getenv("TP_STEM_DBG")) : 0;
+    a.dbg = dbg;
+    // Used for spans of >= 4 tiles (TP_STEM_WIDE: 0 never, 2 always): the ring
+    // pays off once consecutive tiles share input rows; for 1-2 tiles per CTA
+    // the im2col tile starts sooner (ResNet-50 conv1 at 100%: 7.9 us im2col vs
+    // 11.6 us ring; VGG-19 conv1_1 b16 at 25%, 16 tiles per CTA: 131 vs 89-92 us).
+    static const int wide_env = getenv("TP_STEM_WIDE") ? atoi(getenv("TP_STEM_WIDE")) : 1;
+    const int cw = (pb.sw == 1 || pb.sw == 2 || pb.sw == 4) ? 8 / pb.sw : 0;
+    a.wide = 0;
+    const int ns = pb.R + 2 * pb.sh;
+    if ((wide_env == 2 || (wide_env == 1 && a.tpc >= 4)) && cw > 0 && pb.C <= cw && ns <= 16) {
+      const int spad = (pb.S * cw + 15) / 16 * 16 / cw;
+      const int kr = spad * cw, kpn = (pb.R * kr + 63) / 64 * 64;
+      const int pcolsw = (pb.bm - 1) * pb.sw + spad;
+      const int wrow = (pcolsw * cw * 2 + 15) / 16 * 16;
+      const size_t ring = ((size_t)ns * wrow + 1023) / 1024 * 1024;
+      const size_t stg = (size_t)pb.bm * pb.bn * (pb.out_f32 ? 4 : 2);
+      const size_t wreg = std::max(ring + stg, ((size_t)pb.bn * kg * 2 + 1023) / 1024 * 1024);
+      const size_t bbytes = (size_t)pb.bn * kpn * 2;
+      const int rrow = (a.prow * 2 + 15) / 16 * 16;
+      const int nraw = 4 * pb.R;   // raw rows of the tiles being widened and copied ahead (kPDT = 2)
+      const size_t raw = ((size_t)nraw * rrow + 1023) / 1024 * 1024;
+      const size_t total = bbytes + wreg + raw + 512 + (size_t)pb.bn * 4;
+      if (kpn <= 256 && total <= 232448) {
+        a.wide = cw; a.kr = kr; a.pcolsw = pcolsw; a.wrow = wrow; a.nslots = ns; a.rrow = rrow; a.nraw = nraw;
+        a.bk = kpn;
+        a.recv_off = (int)(bbytes + ring);
+        a.patch_off = (int)(bbytes + wreg);
+        a.tab_off = a.patch_off + (int)raw;
+        a.bar_off = a.tab_off;
+      }
+    }
+  }
+  {
     static const bool no_ytma = getenv("TP_NO_YTMA") && atoi(getenv("TP_NO_YTMA")) != 0;
     const int eb = pb.out_f32 ? 4 : 2;
     const int ib = pb.bn * eb < 128 ? pb.bn * eb : 128;
@@ -1534,7 +1573,7 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);
   plan->block = dim3(256);
   plan->cluster_z = 1;
-  plan->smem = (size_t)a.bar_off + 128 + (size_t)pb.bn * 4;   // + the staged bias (inside the budget's 1 KiB)
+  plan->smem = (size_t)a.bar_off + (a.wide ? 512 : 128) + (size_t)pb.bn * 4;   // + the staged bias
   cudaError_t e = ensure_smem_attr(plan->fn, plan->smem);
   if (e != cudaSuccess) {
     set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));

@@ -263,6 +263,19 @@ static __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[1
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 32 consecutive TMEM columns of this warp's lane quadrant, one load + one wait.
+static __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[16], uint32_t (&u)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+        "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // Shared-memory matrix descriptor, K-major, swizzled (sm100 format: start>>4
 // [0,14), LBO>>4 [16,30) (unused for swizzled K-major, =1), SBO>>4 [32,46) =
 // 8 rows * row pitch, version 1 at [46,48), layout type at [61,64)).
@@ -286,6 +299,29 @@ static __device__ __forceinline__ uint64_t make_sdesc_plain(uint32_t saddr, uint
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1u << 46;   // layout type 0 (no swizzle) at [61, 64)
   return d;
+}
+
+// Two fp32 values -> packed bf16x2 (RNE, lo in the low half), ReLU fused into the
+// conversion (cvt .relu: max(rne(x), 0) == rne(max(x, 0)), rounding is monotone).
+template <bool RELU>
+static __device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t r;
+  if constexpr (RELU)
+    asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  else
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// 16 fp32 accumulator words + bias -> 8 packed bf16x2 words (paired adds, FADD2).
+template <bool RELU>
+static __device__ __forceinline__ void bias_pack16(const uint32_t (&raw)[16], const float (&bv)[16], uint32_t (&pk)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 t = __fadd2_rn(make_float2(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1])),
+                                make_float2(bv[2 * j], bv[2 * j + 1]));
+    pk[j] = cvt_bf16x2<RELU>(t.x, t.y);
+  }
 }
 
 // Store 16 consecutive output channels [n0, n0+16) of row m.

@@ -75,13 +75,19 @@ struct TcArgs {
   int cluster_red;             // 1: split-K reduced through DSMEM in a (1,1,split_k) cluster
   int bar_off;                 // byte offset of the mbarriers in dynamic shared memory
   int recv_off;                // byte offset of the split-K receive buffer (cluster path)
-  int dbg;                     // TP_DEBUG_TC env (experiments only): bit0 skip A TMA, bit1 skip B TMA
+  int dbg;                     // TP_DEBUG_TC env (experiments only): bit0 skip A TMA, bit1 skip B TMA;
+                               //   stem kind (TP_STEM_DBG): bit0 no patch copies, bit1 no weight repack, bit2 no widening
   int a_tiled;                 // 1: A is a tiled [M][C] map (1x1 / stride 1 / pad 0 layers), not im2col
   int nprod;                   // igemm_tc: cap on TMA producer warps (4 = all available)
   int y_tma;                   // igemm_tc split 1: epilogue staged in the ring smem, TMA 2-D store of y
   int R, pcols, patch_off;     // stem kind: filter rows, patch pixels per row, patch offset in smem
   int prow, pbuf, pc_async;    // stem kind: patch row pitch (elements), bytes per patch buffer, cp.async path
   int pdist;                   // stem kind: patch prefetch distance in tiles (1 or 2; pdist + 1 buffers)
+  int wide, wrow, nslots, rrow, nraw, pcolsw, kr;   // stem kind, wide path (wide = C_w > 0, s_w C_w = 8):
+                               //   input row segments widened to C_w-element pixels in a ring of nslots
+                               //   slots (pitch wrow bytes, pcolsw pixels), nraw raw rows rrow bytes apart;
+                               //   reduction order k = r K_r + s C_w + c, K_r = S_pad C_w a multiple of
+                               //   16; tiles column-major; 0 = im2col tile, k = (r, s, c)
   int psh;                     // stem kind: elements a patch row starts before its first input
                                //   element ((pw C) & 1; (-pw C) mod 8 in the 16-byte mode pc_async = 2)
   int w_early;                 // 1: weight (B) boxes of the first ring pass are issued before

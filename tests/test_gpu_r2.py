@@ -548,3 +548,16 @@ def test_roww_cta_pair_variant_bit_exact():
                        timeout=900, env=dict(os.environ, TP_ROWW2="1"))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "3 passed" in r.stdout
+
+
+@pytest.mark.parametrize("mode", ["0", "2"], ids=["im2col_only", "ring_only"])
+def test_stem_both_paths_every_schedule(mode):
+    """The stem kind builds its A operand two ways -- an im2col tile per tile, or
+    (spans of >= 4 tiles) a ring of widened input rows read in place by the MMAs.
+    TP_STEM_WIDE (read once per process) forces one path for every schedule: rerun
+    the every-schedule bit-exact and full-size stem tests in a child process."""
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-q", "-x", "-p", "no:cacheprovider",
+                        "-k", "stem_every_schedule or stem_full_size or stem_vgg"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=900, env=dict(os.environ, TP_STEM_WIDE=mode))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
