@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -1036,15 +1037,6 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       // a.ystage2: two staging buffers alternate, so only the store of tile i - 2
       // must have read this one (one bulk group may stay in flight)
       uint8_t* stg_t = stg + (a.ystage2 ? (size_t)buf * ystage : 0);
-      if (a.y_tma) {   // the store that last used this staging buffer must have read it
-        if ((int)threadIdx.x == issuer) {
-          if (a.ystage2)
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          else
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
-        asm volatile("bar.sync 2, %0;" ::"r"(n_epi) : "memory");
-      }
       float bv[16];
       const int nb0 = nbase + c_begin;
       if constexpr (kBiasSmem) {
@@ -1065,10 +1057,58 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
         }
       }
       __syncwarp();
-      TP_MT_WAIT(tfull + buf, (uint32_t)((i >> 1) & 1));
+      // The issuer's warp polls the accumulator barrier (its issuer thread also
+      // makes sure the store that last used this staging buffer has read it);
+      // the named barrier releases the other drain warps, which would otherwise
+      // spend issue slots polling.
+      if (((int)threadIdx.x >> 5) == (issuer >> 5)) {
+        if (a.y_tma && (int)threadIdx.x == issuer) {
+          if (a.ystage2)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        TP_MT_WAIT(tfull + buf, (uint32_t)((i >> 1) & 1));
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(n_epi) : "memory");
       tc_fence_after();
       if (trace && (int)threadIdx.x == issuer && i < 8) trace[28 + i] = gtimer();   // tile i's accumulator ready
-      for (int c = c_begin; c < c_end; c += 16) {
+      if constexpr (kBiasSmem) {
+        if (!a.out_f32 && a.y_tma) {
+          // bf16 + TMA store: compile-time staging geometry, ReLU chosen once per tile
+          constexpr uint32_t IBf = BN * 2 < 128 ? BN * 2 : 128, SWM = IBf / 16 - 1;
+          const uint32_t xr = ((((uint32_t)row * IBf) >> 7) & SWM) << 4;
+          uint8_t* rowp = stg_t + (size_t)row * IBf;
+          const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN);
+          auto drain = [&](auto relu_c) {
+            constexpr bool RELU = decltype(relu_c)::value;
+            for (int c = c_begin; c < c_end; c += 16) {
+              uint32_t raw[16];
+              tmem_ld16(tb + (uint32_t)c, raw);
+              float bw[16];
+#pragma unroll
+              for (int g = 0; g < 16; g += 4) {
+                const float4 f = *reinterpret_cast<const float4*>(sbias + c + g);
+                bw[g] = f.x; bw[g + 1] = f.y; bw[g + 2] = f.z; bw[g + 3] = f.w;
+              }
+              uint32_t pk[8];
+              bias_pack16<RELU>(raw, bw, pk);
+              if (row_ok) {
+#pragma unroll
+                for (int qq = 0; qq < 2; ++qq) {
+                  const uint32_t cb = (uint32_t)(c + 8 * qq) * 2u, j = cb / IBf, cin = cb % IBf;
+                  *reinterpret_cast<uint4*>(rowp + (size_t)j * BM * IBf + (cin ^ xr)) =
+                      make_uint4(pk[4 * qq], pk[4 * qq + 1], pk[4 * qq + 2], pk[4 * qq + 3]);
+                }
+              }
+            }
+          };
+          if (a.relu) drain(std::integral_constant<bool, true>());
+          else drain(std::integral_constant<bool, false>());
+        }
+      }
+      const bool fast_done = kBiasSmem && !a.out_f32 && a.y_tma;
+      for (int c = c_begin; c < c_end && !fast_done; c += 16) {
         uint32_t raw[16];
         tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + c), raw);
         const int nb = nbase + c;
