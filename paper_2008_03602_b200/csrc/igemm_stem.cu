@@ -36,12 +36,17 @@ namespace tp {
 // Wide path helpers (C_w = 8 / s_w channels per widened pixel, compile-time).
 // One widened pixel u of a raw row (elements u C + c, c < C; zero past C and
 // past the raw columns).
-template <int CW, int CC>   // CC: compile-time C (0: runtime C)
+template <int CW, int CC, bool ONES>   // CC: compile-time C (0: runtime C); ONES: TcArgs::bias_mma
 __device__ __forceinline__ void widen_px(const uint16_t* raw, uint8_t* wrow, int u, int pcols, int sh1, int C_rt) {
   const int C = CC > 0 ? CC : C_rt;
   uint32_t wv[CW / 2];
 #pragma unroll
-  for (int q = 0; q < CW / 2; ++q) wv[q] = 0u;
+  for (int q = 0; q < CW / 2; ++q) {   // bf16 1.0 on the bias channels C..C+2
+    uint32_t w = 0u;
+    if (ONES && 2 * q >= C && 2 * q < C + 3) w |= 0x3F80u;
+    if (ONES && 2 * q + 1 >= C && 2 * q + 1 < C + 3) w |= 0x3F800000u;
+    wv[q] = w;
+  }
   if (u < pcols) {
     const uint16_t* src = raw + sh1 + u * C;
 #pragma unroll
@@ -65,7 +70,7 @@ __device__ __forceinline__ void wide_wchunk(const uint16_t* src, uint32_t (&v)[4
   }
 }
 
-template <int BM, int BN>
+template <int BM, int BN, bool WIDE>   // WIDE: the ring path (TcArgs::wide), else the im2col tile
 __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
                                                          const __grid_constant__ CUtensorMap tmY, TcArgs a) {   // (no tensor maps: same launch signature as igemm_tc)
   constexpr uint32_t A_SUB = BM * 128, B_SUB = BN * 128;   // one 64-element (128-B) k column block
@@ -136,7 +141,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   // k table: k = (r, s, c) -> offset of x[r][s + m s_w][c] in the patch for pixel m = 0; -1 = padding.
-  for (int k = threadIdx.x; k < KP && !a.wide; k += blockDim.x) {
+  for (int k = threadIdx.x; k < KP && !WIDE; k += blockDim.x) {
     int v = -1;
     if (k < a.Kg) {
       const int c = k % C, rs = k / C, s = rs % a.S, r = rs / a.S;
@@ -186,12 +191,28 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
         for (int idx = pt; idx < BN * CH && !(a.dbg & 2); idx += kProd) {
           const int n = idx % BN, ch = idx / BN, k0 = ch * 8;
           uint32_t v[4] = {0u, 0u, 0u, 0u};
-          if (a.wide) {
+          if constexpr (WIDE) {
             // k = r K_r + s C_w + c (K_r = S_pad C_w): zero for s >= S, c >= C
             const int r = k0 / a.kr, s0 = (k0 - r * a.kr) >> (a.wide == 8 ? 3 : (a.wide == 4 ? 2 : 1));
             if (a.wide == 8) wide_wchunk<8>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
             else if (a.wide == 4) wide_wchunk<4>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
             else wide_wchunk<2>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
+            if (a.bias_mma && k0 == 0) {
+              // bias = b1 + b2 + b3 exactly (three bf16 parts of the fp32 value) on
+              // pixel s = 0, channels C..C+2 (C_w = 8: chunk 0 is that pixel)
+              const float bf = (a.has_bias && n < nrows) ? __ldg(a.bias + nbase + n) : 0.0f;
+              const __nv_bfloat16 b1 = __float2bfloat16_rn(bf);
+              const float r1 = bf - __bfloat162float(b1);
+              const __nv_bfloat16 b2 = __float2bfloat16_rn(r1);
+              const __nv_bfloat16 b3 = __float2bfloat16_rn(r1 - __bfloat162float(b2));
+              const uint32_t p1 = __bfloat16_as_ushort(b1), p2 = __bfloat16_as_ushort(b2), p3 = __bfloat16_as_ushort(b3);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const int j = c - C;
+                const uint32_t pv = j == 0 ? p1 : (j == 1 ? p2 : p3);
+                if (j >= 0 && j < 3) v[c >> 1] |= pv << ((c & 1) * 16);
+              }
+            }
           } else {
             const int lim = n < nrows ? a.Kg - k0 : 0;   // elements j < lim of the chunk are W[n][k0 + j]
             const uint16_t* src = wst + n * a.Kg + k0;
@@ -267,7 +288,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     // Patches run a.pdist tiles ahead through pdist + 1 buffers (one cp.async
     // group per tile, empty past the last tile, so that "wait until pdist
     // groups are pending" always means "tile i's patch has landed").
-    if (a.wide) {
+    if constexpr (WIDE) {
       // ---- wide path: a ring of widened input rows ----
       // Tiles run column-major (q-block outer, output row inner), so tile i + 1
       // (next output row, same q-block) shares R - s_h input rows with tile i:
@@ -377,13 +398,18 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
           const uint16_t* rawr = reinterpret_cast<const uint16_t*>(rawb + (size_t)rk * a.rrow);
           uint8_t* wr = slots + (size_t)sk * a.wrow;
           if (a.wide == 8) {
-            if (C == 3) widen_px<8, 3>(rawr, wr, u, a.pcols, sh1, C);
-            else widen_px<8, 0>(rawr, wr, u, a.pcols, sh1, C);
+            if (C == 3) {
+              if (a.bias_mma) widen_px<8, 3, true>(rawr, wr, u, a.pcols, sh1, C);
+              else widen_px<8, 3, false>(rawr, wr, u, a.pcols, sh1, C);
+            } else {
+              if (a.bias_mma) widen_px<8, 0, true>(rawr, wr, u, a.pcols, sh1, C);
+              else widen_px<8, 0, false>(rawr, wr, u, a.pcols, sh1, C);
+            }
           } else if (a.wide == 4) {
-            if (C == 3) widen_px<4, 3>(rawr, wr, u, a.pcols, sh1, C);
-            else widen_px<4, 0>(rawr, wr, u, a.pcols, sh1, C);
+            if (C == 3) widen_px<4, 3, false>(rawr, wr, u, a.pcols, sh1, C);
+            else widen_px<4, 0, false>(rawr, wr, u, a.pcols, sh1, C);
           } else {
-            widen_px<2, 0>(rawr, wr, u, a.pcols, sh1, C);
+            widen_px<2, 0, false>(rawr, wr, u, a.pcols, sh1, C);
           }
           u += kProd;
           while (u >= pw8 && k < nnew) { u -= pw8; ++k; }
@@ -499,7 +525,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     const bool slp = !(a.dbg & 8);
     if (slp) mbar_wait_sleep(b_full, 0); else mbar_wait(b_full, 0);
     const uint64_t bdesc0 = make_sdesc(smem_u32(b_s), 128);
-    if (a.wide) {
+    if constexpr (WIDE) {
       // Wide path: tile i (column-major order) reads input rows gstart .. gstart + R - 1
       // of the ring; A for MMA kk = (filter row r, half h) is a no-swizzle K-major
       // view of slot (gstart + r) % NS at byte 32 h of the q-block's segment --
@@ -552,7 +578,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
         if (trace && lane == 0 && i < 8) trace[12 + i] = (unsigned long long)clock64();
       }
     }
-    for (int i = 0; i < ntl && !a.wide; ++i) {
+    for (int i = 0; i < ntl && !WIDE; ++i) {
       const int b = i & 1;
       if (slp) mbar_wait_sleep(a_full + b, (uint32_t)(i >> 1) & 1u);
       else mbar_wait(a_full + b, (uint32_t)(i >> 1) & 1u);
@@ -585,7 +611,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     const uint32_t IB = BN * EB < 128u ? BN * EB : 128u;
     // Bias of the CTA's BN columns staged once (zero past K and without a
     // bias); ReLU as a max against 0 (or -inf without ReLU).
-    float* bias_s = reinterpret_cast<float*>(smem_raw + a.bar_off + (a.wide ? 512 : 128));
+    float* bias_s = reinterpret_cast<float*>(smem_raw + a.bar_off + (WIDE ? 512 : 128));
     for (int j = (int)threadIdx.x - 128; j < BN; j += 128)
       bias_s[j] = (a.has_bias && nbase + j < a.K) ? __ldg(a.bias + nbase + j) : 0.0f;
     asm volatile("bar.sync 2, 128;" ::: "memory");
@@ -593,12 +619,12 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     // tile (q-block, output row), advanced per tile: q-block fastest, or (wide
     // path) column-major -- output row fastest
     const int NPe = a.ntiles / a.nqb;
-    int e_qb = a.wide ? tile0 / NPe : tile0 % a.nqb;
-    int e_prw = a.wide ? tile0 - e_qb * NPe : tile0 / a.nqb;
+    int e_qb = WIDE ? tile0 / NPe : tile0 % a.nqb;
+    int e_prw = WIDE ? tile0 - e_qb * NPe : tile0 / a.nqb;
     for (int i = 0; i < ntl; ++i) {
       const int b = i & 1;
       const int qb = e_qb, prw = e_prw;
-      if (a.wide) {
+      if constexpr (WIDE) {
         if (++e_prw == NPe) { e_prw = 0; ++e_qb; }
       } else if (++e_qb == a.nqb) {
         e_qb = 0;
@@ -619,35 +645,32 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       tc_fence_after();
       if (trace && threadIdx.x == 128 && i < 8) trace[28 + i] = (unsigned long long)clock64();
       if (!a.out_f32 && a.y_tma) {
-        // bf16 + TMA store (the stems' case): compile-time staging geometry, 32
-        // columns per TMEM load, ReLU chosen once per tile.
+        // bf16 + TMA store (the stems' case): compile-time staging geometry, ReLU
+        // and the bias-in-MMA form chosen once per tile.
         constexpr uint32_t IBf = BN * 2 < 128 ? BN * 2 : 128, SWM = IBf / 16 - 1;
         const uint32_t xr = ((((uint32_t)row * IBf) >> 7) & SWM) << 4;
         uint8_t* rowp = stg + (size_t)row * IBf;
         const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(b * BN);
-        auto drain = [&](auto relu_c) {
-          constexpr bool RELU = decltype(relu_c)::value;
+        auto drain = [&](auto relu_c, auto fold_c) {
+          constexpr bool RELU = decltype(relu_c)::value, FOLD = decltype(fold_c)::value;
 #pragma unroll
-          for (int c = 0; c < BN; c += 32) {
-            uint32_t r0[16], r1[16];
-            tmem_ld32(tb + (uint32_t)c, r0, r1);
-            uint32_t pk[16];
-            float bv[16];
+          for (int c = 0; c < BN; c += 16) {
+            uint32_t raw[16], pk[8];
+            tmem_ld16(tb + (uint32_t)c, raw);
+            if constexpr (FOLD) {
+              pack16<RELU>(raw, pk);
+            } else {
+              float bv[16];
 #pragma unroll
-            for (int g = 0; g < 16; g += 4) {
-              const float4 f = *reinterpret_cast<const float4*>(bias_s + c + g);
-              bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
+              for (int g = 0; g < 16; g += 4) {
+                const float4 f = *reinterpret_cast<const float4*>(bias_s + c + g);
+                bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
+              }
+              bias_pack16<RELU>(raw, bv, pk);
             }
-            bias_pack16<RELU>(r0, bv, *reinterpret_cast<uint32_t(*)[8]>(pk));
-#pragma unroll
-            for (int g = 0; g < 16; g += 4) {
-              const float4 f = *reinterpret_cast<const float4*>(bias_s + c + 16 + g);
-              bv[g] = f.x; bv[g + 1] = f.y; bv[g + 2] = f.z; bv[g + 3] = f.w;
-            }
-            bias_pack16<RELU>(r1, bv, *reinterpret_cast<uint32_t(*)[8]>(pk + 8));
             if (row_ok) {
 #pragma unroll
-              for (int qq = 0; qq < 4; ++qq) {
+              for (int qq = 0; qq < 2; ++qq) {
                 const uint32_t cb = (uint32_t)(c + 8 * qq) * 2u, j = cb / IBf, cin = cb % IBf;
                 *reinterpret_cast<uint4*>(rowp + (size_t)j * BM * IBf + (cin ^ xr)) =
                     make_uint4(pk[4 * qq], pk[4 * qq + 1], pk[4 * qq + 2], pk[4 * qq + 3]);
@@ -655,8 +678,15 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
             }
           }
         };
-        if (a.relu) drain(std::integral_constant<bool, true>());
-        else drain(std::integral_constant<bool, false>());
+        using T = std::integral_constant<bool, true>;
+        using F = std::integral_constant<bool, false>;
+        if (WIDE && a.bias_mma) {
+          if constexpr (WIDE) {
+            if (a.relu) drain(T(), T()); else drain(F(), T());
+          }
+        } else {
+          if (a.relu) drain(T(), F()); else drain(F(), F());
+        }
       }
 #pragma unroll
       for (int c = 0; c < BN && !(!a.out_f32 && a.y_tma); c += 16) {
@@ -758,9 +788,11 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   }
 }
 
-const void* pick_stem(int bm, int bn) {
+const void* pick_stem(int bm, int bn, bool wide) {
 #define TP_STEM_CASE(M_, N_) \
-  if (bm == M_ && bn == N_) return reinterpret_cast<const void*>(igemm_stem_kernel<M_, N_>);
+  if (bm == M_ && bn == N_)    \
+    return wide ? reinterpret_cast<const void*>(igemm_stem_kernel<M_, N_, true>) \
+                : reinterpret_cast<const void*>(igemm_stem_kernel<M_, N_, false>);
   TP_STEM_CASE(64, 32) TP_STEM_CASE(64, 64) TP_STEM_CASE(64, 128)
   TP_STEM_CASE(128, 32) TP_STEM_CASE(128, 64) TP_STEM_CASE(128, 128)
 #undef TP_STEM_CASE

@@ -1582,6 +1582,8 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
       const size_t total = bbytes + wreg + raw + 512 + (size_t)pb.bn * 4;
       if (kpn <= 256 && total <= 232448) {
         a.wide = cw; a.kr = kr; a.pcolsw = pcolsw; a.wrow = wrow; a.nslots = ns; a.rrow = rrow; a.nraw = nraw;
+        static const bool no_fold = getenv("TP_STEM_FOLD") && atoi(getenv("TP_STEM_FOLD")) == 0;
+        a.bias_mma = (!no_fold && cw == 8 && pb.C <= 5 && !pb.out_f32) ? 1 : 0;
         a.bk = kpn;
         a.recv_off = (int)(bbytes + ring);
         a.patch_off = (int)(bbytes + wreg);
@@ -1607,7 +1609,7 @@ static tp_status stem_prepare(const TcProblem& pb, TcPlan* plan) {
                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
       a.y_tma = 1;
   }
-  plan->fn = pick_stem(pb.bm, pb.bn);
+  plan->fn = pick_stem(pb.bm, pb.bn, a.wide != 0);
   if (!plan->fn) { set_error("no igemm_stem instantiation for this BM x BN"); return TP_EINVALID_CONFIG; }
   plan->grid = dim3((unsigned)((a.ntiles + a.tpc - 1) / a.tpc), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u);
   if (pb.grid_x) plan->grid = dim3(pb.grid_x, pb.grid_y, pb.grid_z);

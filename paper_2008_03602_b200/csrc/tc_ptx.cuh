@@ -324,6 +324,13 @@ static __device__ __forceinline__ void bias_pack16(const uint32_t (&raw)[16], co
   }
 }
 
+// 16 fp32 accumulator words -> 8 packed bf16x2 words (bias already in the accumulator).
+template <bool RELU>
+static __device__ __forceinline__ void pack16(const uint32_t (&raw)[16], uint32_t (&pk)[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) pk[j] = cvt_bf16x2<RELU>(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1]));
+}
+
 // Store 16 consecutive output channels [n0, n0+16) of row m.
 static __device__ __forceinline__ void store16(void* y, int64_t m, int K, int n0, const float (&v)[16], int out_f32) {
   if (out_f32) {

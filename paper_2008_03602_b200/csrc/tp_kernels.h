@@ -83,6 +83,9 @@ struct TcArgs {
   int R, pcols, patch_off;     // stem kind: filter rows, patch pixels per row, patch offset in smem
   int prow, pbuf, pc_async;    // stem kind: patch row pitch (elements), bytes per patch buffer, cp.async path
   int pdist;                   // stem kind: patch prefetch distance in tiles (1 or 2; pdist + 1 buffers)
+  int bias_mma;                // stem kind, wide path with C_w - C >= 3: the bias enters the MMA as three
+                               //   bf16 parts (exact sum) on constant-one channels C..C+2 of the (r, s) =
+                               //   (0, 0) tap; the epilogue only converts
   int wide, wrow, nslots, rrow, nraw, pcolsw, kr;   // stem kind, wide path (wide = C_w > 0, s_w C_w = 8):
                                //   input row segments widened to C_w-element pixels in a ring of nslots
                                //   slots (pitch wrow bytes, pcolsw pixels), nraw raw rows rrow bytes apart;
@@ -137,7 +140,7 @@ struct TcPlan {
 
 tp_status tc_prepare(const TcProblem& pb, TcPlan* plan);
 const void* pick_tf32(int bm, int bn);   // igemm_tf32.cu
-const void* pick_stem(int bm, int bn);   // igemm_stem.cu
+const void* pick_stem(int bm, int bn, bool wide);   // igemm_stem.cu
 cudaError_t tc_launch(const TcPlan& plan, cudaStream_t stream);
 int tc_occupancy(const TcPlan& plan);
 size_t tc_dyn_smem(int bm, int bn, int bk, int stages);
