@@ -48,11 +48,14 @@ __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long l
 //   TMA would produce (the C = 3 stems, where a pixel row is 6 bytes and
 //   neither TMA mode applies).
 template <int BM, int BN, int BK, int MODE>
-__global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(256, 2) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
                                                        const __grid_constant__ CUtensorMap tmY, TcArgs a) {
   constexpr bool GATHER = MODE == 1;
-  static_assert(MODE == 0 || MODE == 1, "MODE 2 (row-halo) is igemm_row_kernel");
+  static_assert(MODE == 0 || MODE == 1 || MODE == 6, "modes 2-5 are igemm_mt_kernel");
+  // MODE 0 / 6: TMA-fed split_k == 1 / split_k > 1 instantiations (each launch runs
+  // only its own epilogue; smaller code per launch), MODE 1 (gathered): either.
+  const bool sk1 = MODE == 0 ? true : (MODE == 6 ? false : a.split_k == 1);
   // Compile-time tile geometry: one swizzle row holds SUBK channels (32/64/128 B).
   constexpr int SUBK = BK < 64 ? BK : 64;
   constexpr int NSUB = BK / SUBK;
@@ -417,7 +420,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
 #pragma unroll
     for (int i = 0; i < 16; ++i) bv[i] = bias_next[i];
     if (c + 16 < c_end) load_bias16(nb + 16, bias_next);
-    if (a.split_k == 1 && a.y_tma) {
+    if (sk1 && a.y_tma) {
       // Stage the tile in the (now idle) ring in the swizzled layout of the y
       // tensor map's box (IB-byte rows, BN / (IB / EB) boxes side by side); rows
       // past M and columns past K are clipped by the TMA store.
@@ -458,7 +461,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
           }
         }
       }
-    } else if (a.split_k == 1) {
+    } else if (sk1) {
       if (m_ok && nb < a.K) {
         float v[16];
 #pragma unroll
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
   }
 
   if (!GATHER && trace && threadIdx.x == 0) trace[69] = gtimer();
-  if (a.split_k == 1 && a.y_tma) {
+  if (sk1 && a.y_tma) {
     // generic-proxy smem writes -> visible to the TMA engine; one thread stores.
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       tma_store_commit_wait();
     }
   }
-  if (a.split_k > 1 && a.cluster_red) {
+  if (!sk1 && a.cluster_red) {
     // Owner side: the threads whose row this CTA owns wait for the other
     // splits' slices, sum all split_k slices in split order (deterministic),
     // add bias, ReLU, store.  Same thread <-> row mapping as the send pass.
@@ -550,7 +553,7 @@ __global__ void __launch_bounds__(256) igemm_tc_kernel(const __grid_constant__ C
       }
     }
     if (trace && threadIdx.x == 0) trace[67] = gtimer();
-  } else if (a.split_k > 1) {
+  } else if (!sk1) {
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1254,6 +1257,7 @@ static KernelFn pick_bk(int bk) {
       case 128: return igemm_mt_kernel<BM, BN, 128, 0>;
     }
   } else {
+    static_assert(MODE == 0 || MODE == 1 || MODE == 6, "igemm_tc_kernel modes");
     switch (bk) {
       case 16: return igemm_tc_kernel<BM, BN, 16, MODE>;
       case 32: return igemm_tc_kernel<BM, BN, 32, MODE>;
@@ -1267,7 +1271,8 @@ static KernelFn pick_bk(int bk) {
 static KernelFn pick_tc(int bm, int bn, int bk, int mode) {
 #define TP_TC_CASE(M_, N_)                                                                       \
   if (bm == M_ && bn == N_)                                                                      \
-    return mode == 5 ? pick_bk<M_, N_, 5>(bk)                                                    \
+    return mode == 6 ? pick_bk<M_, N_, 6>(bk)                                                    \
+                     : mode == 5 ? pick_bk<M_, N_, 5>(bk)                                        \
                      : mode == 4 ? pick_bk<M_, N_, 4>(bk)                                        \
                      : mode == 3 ? pick_bk<M_, N_, 3>(bk)                                        \
                      : (mode == 2 ? pick_bk<M_, N_, 2>(bk)                                       \
@@ -1778,7 +1783,8 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   a.strip_px = a.strip_stage = a.strip_woff = 0;
   a.a_tiled = a_tiled ? 1 : 0;
   a.y_tma = y_tma;
-  plan->fn = reinterpret_cast<const void*>(pick_tc(pb.bm, pb.bn, pb.bk, pb.mt ? 3 : (pb.row ? 2 : (pb.gather ? 1 : 0))));
+  plan->fn = reinterpret_cast<const void*>(
+      pick_tc(pb.bm, pb.bn, pb.bk, pb.mt ? 3 : (pb.row ? 2 : (pb.gather ? 1 : (pb.split_k > 1 ? 6 : 0)))));
   if (!plan->fn) { set_error("no igemm_tc instantiation for this BM x BN x BK"); return TP_EINVALID_CONFIG; }
   plan->grid = (pb.row || pb.mt)
                    ? dim3((unsigned)((a.ntiles + a.tpc - 1) / a.tpc), (unsigned)((pb.K + pb.bn - 1) / pb.bn), 1u)
