@@ -424,7 +424,20 @@ __global__ void __launch_bounds__(256, 2) igemm_tc_kernel(const __grid_constant_
       // Stage the tile in the (now idle) ring in the swizzled layout of the y
       // tensor map's box (IB-byte rows, BN / (IB / EB) boxes side by side); rows
       // past M and columns past K are clipped by the TMA store.
-      if (row_ok) {
+      if (row_ok && !a.out_f32) {
+        // bf16: paired bias adds and one RNE pack per pair, ReLU in the conversion
+        constexpr uint32_t IBf = BN * 2 < 128 ? BN * 2 : 128, SWM = IBf / 16 - 1;
+        uint32_t pk[8];
+        if (a.relu) bias_pack16<true>(raw, bv, pk);
+        else bias_pack16<false>(raw, bv, pk);
+        const uint32_t xr = ((((uint32_t)row * IBf) >> 7) & SWM) << 4;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t cb = (uint32_t)(c + 8 * q) * 2u, j = cb / IBf, cin = cb % IBf;
+          *reinterpret_cast<uint4*>(smem_raw + (size_t)j * BM * IBf + (size_t)row * IBf + (cin ^ xr)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+      } else if (row_ok) {
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -462,7 +475,12 @@ __global__ void __launch_bounds__(256, 2) igemm_tc_kernel(const __grid_constant_
         }
       }
     } else if (sk1) {
-      if (m_ok && nb < a.K) {
+      if (m_ok && nb < a.K && !a.out_f32) {
+        uint32_t pk[8];
+        if (a.relu) bias_pack16<true>(raw, bv, pk);
+        else bias_pack16<false>(raw, bv, pk);
+        store16_pk(a.y, m, a.K, nb, pk);
+      } else if (m_ok && nb < a.K) {
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -542,7 +560,14 @@ __global__ void __launch_bounds__(256, 2) igemm_tc_kernel(const __grid_constant_
             v[i] += t.x; v[i + 1] += t.y; v[i + 2] += t.z; v[i + 3] += t.w;
           }
         }
-        if (nb < a.K) {
+        if (nb < a.K && !a.out_f32) {
+          uint32_t raw[16], pk[8];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) raw[i] = __float_as_uint(v[i]);
+          if (a.relu) bias_pack16<true>(raw, bv, pk);
+          else bias_pack16<false>(raw, bv, pk);
+          store16_pk(a.y, m, a.K, nb, pk);
+        } else if (nb < a.K) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float t = v[i] + bv[i];

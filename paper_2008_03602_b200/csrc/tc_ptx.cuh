@@ -331,6 +331,13 @@ static __device__ __forceinline__ void pack16(const uint32_t (&raw)[16], uint32_
   for (int j = 0; j < 8; ++j) pk[j] = cvt_bf16x2<RELU>(__uint_as_float(raw[2 * j]), __uint_as_float(raw[2 * j + 1]));
 }
 
+// Store 16 packed bf16 output channels [n0, n0+16) of row m (two 16-byte stores).
+static __device__ __forceinline__ void store16_pk(void* y, int64_t m, int K, int n0, const uint32_t (&pk)[8]) {
+  uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(y) + m * K + n0);
+  if (n0 + 8 <= K) p[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  if (n0 + 16 <= K) p[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+}
+
 // Store 16 consecutive output channels [n0, n0+16) of row m.
 static __device__ __forceinline__ void store16(void* y, int64_t m, int K, int n0, const float (&v)[16], int out_f32) {
   if (out_f32) {
