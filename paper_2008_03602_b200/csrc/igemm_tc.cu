@@ -521,10 +521,21 @@ __global__ void __launch_bounds__(256, 2) igemm_tc_kernel(const __grid_constant_
   }
 
   if (!GATHER && trace && threadIdx.x == 0) trace[69] = gtimer();
-  if (sk1 && a.y_tma) {
-    // generic-proxy smem writes -> visible to the TMA engine; one thread stores.
+  // Every warp's last tcgen05.ld is done: release TMEM now, before the TMA
+  // store, the split-K reduction and the exit (in a chain of dependent launches
+  // a dealloc issued after the output stores cost ~0.1 us per launch:
+  // tools/micro/launch_gap.cu, variants 6 and 7).
+  if (sk1 && a.y_tma)   // generic-proxy smem writes -> visible to the TMA engine
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
+                 : "memory");
+  }
+  if (sk1 && a.y_tma) {
+    // one thread stores the staged tile
     if (threadIdx.x == 0) {
       const int EB = a.out_f32 ? 4 : 2;
       const int IB = BN * EB < 128 ? BN * EB : 128;
@@ -615,14 +626,7 @@ __global__ void __launch_bounds__(256, 2) igemm_tc_kernel(const __grid_constant_
   }
 
   if (!GATHER && trace && threadIdx.x == 0) trace[70] = gtimer();
-  tc_fence_before();
-  __syncthreads();
   if (trace && threadIdx.x == 0) trace[3] = gtimer();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
-                 : "memory");
-  }
 }
 
 // ------------------------------------------------------------- multi-tile kernel
