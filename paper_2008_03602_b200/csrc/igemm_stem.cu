@@ -776,7 +776,6 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
         }
       }
     }
-    if (a.y_tma && threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -786,6 +785,9 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols)
                  : "memory");
   }
+  // the last tile's store must have read the staging buffer before the CTA
+  // exits (waited after the TMEM release, which it does not need)
+  if (a.y_tma && threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 const void* pick_stem(int bm, int bn, bool wide) {

@@ -1289,7 +1289,6 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
         }
       }
     }
-    if (a.y_tma && (int)threadIdx.x == issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
 
   tc_fence_before();
@@ -1307,6 +1306,10 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols) : "memory");
   }
+  // the last tile's store must have read the staging buffer before the CTA
+  // exits (waited after the TMEM release, which it does not need)
+  if (a.y_tma && (int)threadIdx.x == (split_roles ? 64 : 0))
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------- host side
