@@ -48,7 +48,7 @@ __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long l
 //   TMA would produce (the C = 3 stems, where a pixel row is 6 bytes and
 //   neither TMA mode applies).
 template <int BM, int BN, int BK, int MODE>
-__global__ void __launch_bounds__(256, 2) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) igemm_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
                                                        const __grid_constant__ CUtensorMap tmY, TcArgs a) {
   constexpr bool GATHER = MODE == 1;

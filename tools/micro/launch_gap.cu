@@ -7,6 +7,9 @@
 //   7 = 6 with the dealloc before the y stores
 //   8 = 5 with alloc and dealloc both before the PDL wait (TMEM not held in the body)
 //   9 = 5 with the dealloc before the y stores
+//  10 = 3 with the 8 KB written by one bulk copy (cp.async.bulk smem -> global), wait_group.read
+//  11 = 10 with wait_group 0 (writes complete) before the exit
+//  12 = 3 with 2 KB per CTA, 13 = 3 with 32 KB per CTA
 // usage: launch_gap [ctas=100] [threads=256]     Build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o launch_gap launch_gap.cu
 #include <cuda_runtime.h>
@@ -19,6 +22,7 @@ __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvt
 template <int V>
 __global__ void __launch_bounds__(256) k(const uint4* __restrict__ x, uint4* __restrict__ y) {
   __shared__ uint32_t slot;
+  __shared__ __align__(128) uint4 stg[512];
   const bool tmem = V == 2 || V == 5 || V == 6 || V == 7 || V == 9;
   if ((V == 6 || V == 7 || V == 8) && threadIdx.x < 32) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(su32(&slot)) : "memory");
@@ -48,7 +52,27 @@ __global__ void __launch_bounds__(256) k(const uint4* __restrict__ x, uint4* __r
     const uint32_t base = slot;
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(base) : "memory");
   }
-  if (V == 3 || V >= 5) {   // 8 KB per CTA
+  if (V == 10 || V == 11) {
+    stg[threadIdx.x] = acc;
+    stg[threadIdx.x + blockDim.x] = acc;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint4* yp = y + (size_t)blockIdx.x * blockDim.x * 2;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 8192;" ::"l"(yp), "r"(su32(stg)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (V == 10) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+  }
+  if (V == 12) {   // 2 KB per CTA
+    if (threadIdx.x < 128) y[(size_t)blockIdx.x * 128 + threadIdx.x] = acc;
+  }
+  if (V == 13) {   // 32 KB per CTA
+    uint4* yp = y + (size_t)blockIdx.x * blockDim.x * 8;
+    for (int j = 0; j < 8; ++j) yp[threadIdx.x + j * blockDim.x] = acc;
+  }
+  if (V == 3 || (V >= 5 && V <= 9)) {   // 8 KB per CTA
     uint4* yp = y + (size_t)blockIdx.x * blockDim.x * 2;
     yp[threadIdx.x] = acc;
     yp[threadIdx.x + blockDim.x] = acc;
@@ -102,7 +126,7 @@ int main(int argc, char** argv) {
   const int ctas = argc > 1 ? atoi(argv[1]) : 100, threads = argc > 2 ? atoi(argv[2]) : 256;
   uint4 *x, *y;
   cudaMalloc(&x, (size_t)ctas * threads * 16);
-  cudaMalloc(&y, (size_t)ctas * threads * 32);
+  cudaMalloc(&y, (size_t)ctas * threads * 128);
   cudaMemset(x, 0, (size_t)ctas * threads * 16);
   cudaStream_t st;
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
@@ -118,6 +142,10 @@ int main(int argc, char** argv) {
   printf("7 = 6, dealloc early    %.3f\n", period<7>(ctas, threads, x, y, st, n));
   printf("8 = TMEM before wait only %.3f\n", period<8>(ctas, threads, x, y, st, n));
   printf("9 = 5, dealloc early    %.3f\n", period<9>(ctas, threads, x, y, st, n));
+  printf("10 = 8 KB bulk, read    %.3f\n", period<10>(ctas, threads, x, y, st, n));
+  printf("11 = 8 KB bulk, done    %.3f\n", period<11>(ctas, threads, x, y, st, n));
+  printf("12 = 2 KB stores        %.3f\n", period<12>(ctas, threads, x, y, st, n));
+  printf("13 = 32 KB stores       %.3f\n", period<13>(ctas, threads, x, y, st, n));
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return 0;
