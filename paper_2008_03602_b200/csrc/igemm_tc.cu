@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) igemm_tc_kernel(const 
 #define TP_MT_WAIT mbar_wait_sleep
 #endif
 template <int BM, int BN, int BK, int KM>
-__global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
+__global__ void __launch_bounds__(KM == 1 ? 352 : 320) igemm_mt_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
                                                        const __grid_constant__ CUtensorMap tmY, TcArgs a) {
   // KM 3 = the row-halo kind's CTA-pair form: a separate instantiation, since a kernel
@@ -764,7 +764,11 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
   const uint32_t ncols = (uint32_t)(split_roles ? 2 * BN : BN) <= 32 ? 32u : (uint32_t)(split_roles ? 2 * BN : BN);
   // tpc > 1: warps 2.. drain -- 8 of them (two per TMEM lane quadrant) when the
   // block has 320 threads, else 6 (quadrants 2 and 3 get two warps, 0 and 1 one).
-  const bool epi8 = blockDim.x == 320;
+  const bool epi8 = blockDim.x >= 320;
+  // 352 threads (N = 64 tiles): warp 10 is a second MMA issuer taking the odd
+  // tiles -- one thread issues an N = 64 MMA every ~52-56 cycles, two reach the
+  // shared-memory operand rate (~48; tools/micro/mma_issue.cu).
+  const bool mma2 = blockDim.x == 352;
   const int n_epi_warps = split_roles ? (epi8 ? 8 : 6) : (int)(blockDim.x >> 5);
   unsigned long long* trace =
       a.trace ? a.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots : nullptr;
@@ -990,9 +994,12 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       }
       if (trace && lane == 0 && i < 8) trace[4 + i] = gtimer();    // tile i's loads issued
     }
-  } else if (warp == 1 && prank == 0) {
+  } else if ((warp == 1 || (mma2 && warp == 10)) && prank == 0) {
     // ---------------- MMA issuer: two accumulators, alternating per tile ----------------
+    // (mma2: warp 1 issues the even tiles into accumulator 0, warp 10 the odd
+    // tiles into accumulator 1; each finds its ring position from the tile index)
     const uint32_t lead = elect_one();
+    const int i_first = (mma2 && warp == 10) ? 1 : 0, i_step = mma2 ? 2 : 1;
     const uint64_t adesc0 = STRIP ? make_sdesc_plain(smem_u32(a_tiles), 16u, 128u) : make_sdesc(smem_u32(a_tiles), SWZ);
     const bool wres = STRIP || (ROW && a.roww);
     const uint64_t bdesc0 = STRIP ? make_sdesc_plain(smem_u32(w_res), (uint32_t)(a.sw * BN * 16), 128u)
@@ -1003,8 +1010,13 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
       TP_MT_WAIT(wfull, 0);
       tc_fence_after();
     }
-    for (int i = 0; i < ntl; ++i) {
+    for (int i = i_first; i < ntl; i += i_step) {
       const int buf = i & 1;
+      if (mma2) {
+        const int g = i * kpt;
+        stage = g % stages;
+        phase = (uint32_t)((g / stages) & 1);
+      }
       if (i >= 2) {
         TP_MT_WAIT(tempty + buf, (uint32_t)(((i - 2) >> 1) & 1));
         tc_fence_after();
@@ -1065,7 +1077,7 @@ __global__ void __launch_bounds__(320) igemm_mt_kernel(const __grid_constant__ C
   }
 
   // ---------------- epilogue ----------------
-  if (!split_roles || warp >= 2) {
+  if (!split_roles || (warp >= 2 && !(mma2 && warp == 10))) {
     const int quad = warp & 3;
     int c_begin, c_end;
     if (split_roles) {               // warps 2..7 -> quadrants 2,3,0,1,2,3 (+ 8,9 -> 0,1 with epi8)
@@ -1875,6 +1887,15 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   //  row kind runs one CTA per SM, so it always takes the eight drain warps.)
   if ((pb.row || pb.mt) && a.tpc > 1 && pb.threads == 256 && (pb.bn >= 128 || pb.roww) && mt_epi8())
     plan->block = dim3(320);
+  // N = 64 resident-weight row tiles: a second MMA-issuing warp (TP_MMA2=0: off)
+  {
+    static const bool no_mma2 = getenv("TP_MMA2") && atoi(getenv("TP_MMA2")) == 0;
+    // the two issuers wait on the ring by phase parity: each one's stages must
+    // stay within one ring pass of the oldest unfinished fill (stages >= 2 k-blocks per tile)
+    if (!no_mma2 && plan->block.x == 320 && pb.row && pb.roww && pb.bn == 64 && !roww_pair_enabled() &&
+        a.stages >= 2 * a.kblocks)
+      plan->block = dim3(352);
+  }
   // Split-K reduces through DSMEM inside a (1, 1, split_k) cluster when the
   // context can co-schedule such clusters; otherwise (e.g. a green context
   // split without SM co-scheduling) through the global workspace.
