@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
 
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
-    mbar_init(b_full, 3);
+    mbar_init(b_full, WIDE ? 3 : 4);
     for (int i = 0; i < 2; ++i) {
       mbar_init(a_full + i, 3);
       mbar_init(a_empty + i, 1);
@@ -153,19 +153,73 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   // global memory: 16-byte cp.async copies into the (not yet used) im2col tile
   // buffers, repacked into the swizzled B tile below.  In repeated launches of
   // one plan (w_early: weights are layer constants) they go out before the PDL wait.
-  auto issue_weights = [&]() {
+  // im2col path: the raw copy lands in the second tile buffer when it fits and
+  // is repacked by the epilogue warps (idle until the first accumulator), so the
+  // producers start on the patches at once; the ring path repacks in the producers.
+  const bool wraw_b1 = !WIDE && (size_t)BN * a.Kg * 2 <= (size_t)NSUB * A_SUB;
+  uint8_t* wraw = WIDE ? a_s : (a_s + (wraw_b1 ? (size_t)NSUB * A_SUB : 0));
+  const bool w_epi = !WIDE;   // who copies and repacks: warps 4-7 (else 0-2)
+  auto issue_weights = [&](int tid, int nthr) {
     const int nrows = min(BN, a.K - nbase);
     const int64_t wbytes = (int64_t)nrows * a.Kg * 2;
     const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(a.wg) + (int64_t)nbase * a.Kg * 2;
-    for (int64_t c = threadIdx.x; c * 16 < wbytes; c += kProd) {
+    for (int64_t c = tid; c * 16 < wbytes; c += nthr) {
       const int nb = (int)min((int64_t)16, wbytes - c * 16);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(a_s + c * 16)), "l"(wsrc + c * 16),
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(wraw + c * 16)), "l"(wsrc + c * 16),
                    "r"(nb)
                    : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  if (warp < 3 && a.w_early) issue_weights();
+  // Raw weights landed (the caller waited for their cp.async group and synced
+  // the participating warps): row n of B = W[nbase + n] in reduction order k
+  // (zero past K_g / K and in the padding); each participating warp arrives on b_full.
+  auto repack_weights = [&](int tid, int nthr) {
+    const uint16_t* wst = reinterpret_cast<const uint16_t*>(wraw);
+    const int nrows = min(BN, a.K - nbase);
+    for (int idx = tid; idx < BN * CH && !(a.dbg & 2); idx += nthr) {
+      const int n = idx % BN, ch = idx / BN, k0 = ch * 8;
+      uint32_t v[4] = {0u, 0u, 0u, 0u};
+      if constexpr (WIDE) {
+        // k = r K_r + s C_w + c (K_r = S_pad C_w): zero for s >= S, c >= C
+        const int r = k0 / a.kr, s0 = (k0 - r * a.kr) >> (a.wide == 8 ? 3 : (a.wide == 4 ? 2 : 1));
+        if (a.wide == 8) wide_wchunk<8>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
+        else if (a.wide == 4) wide_wchunk<4>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
+        else wide_wchunk<2>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
+        if (a.bias_mma && k0 == 0) {
+          // bias = b1 + b2 + b3 exactly (three bf16 parts of the fp32 value) on
+          // pixel s = 0, channels C..C+2 (C_w = 8: chunk 0 is that pixel)
+          const float bf = (a.has_bias && n < nrows) ? __ldg(a.bias + nbase + n) : 0.0f;
+          const __nv_bfloat16 b1 = __float2bfloat16_rn(bf);
+          const float r1 = bf - __bfloat162float(b1);
+          const __nv_bfloat16 b2 = __float2bfloat16_rn(r1);
+          const __nv_bfloat16 b3 = __float2bfloat16_rn(r1 - __bfloat162float(b2));
+          const uint32_t p1 = __bfloat16_as_ushort(b1), p2 = __bfloat16_as_ushort(b2), p3 = __bfloat16_as_ushort(b3);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int j = c - C;
+            const uint32_t pv = j == 0 ? p1 : (j == 1 ? p2 : p3);
+            if (j >= 0 && j < 3) v[c >> 1] |= pv << ((c & 1) * 16);
+          }
+        }
+      } else {
+        const int lim = n < nrows ? a.Kg - k0 : 0;   // elements j < lim of the chunk are W[n][k0 + j]
+        const uint16_t* src = wst + n * a.Kg + k0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < lim) v[j >> 1] |= (uint32_t)src[j] << ((j & 1) * 16);
+      }
+      const uint32_t off = (uint32_t)n * 128 + ((uint32_t)(((k0 & 63) >> 3) ^ (n & 7)) << 4);
+      *reinterpret_cast<uint4*>(b_s + (size_t)(k0 >> 6) * B_SUB + off) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(b_full);
+  };
+  if (a.w_early) {
+    if (w_epi && warp >= 4) issue_weights((int)threadIdx.x - 128, 128);
+    else if (!w_epi && warp < 3) issue_weights((int)threadIdx.x, kProd);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -178,57 +232,8 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     const int pt = threadIdx.x;
     if (warp == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint16_t* xg = reinterpret_cast<const uint16_t*>(a.xg);
-    if (!a.w_early) issue_weights();
+    if (!w_epi && !a.w_early) issue_weights(pt, kProd);
 
-    // Weights landed (the caller waited for their cp.async group): row n of B =
-    // W[nbase + n] in reduction order k (zero past K_g / K and in the padding).
-    auto repack_weights = [&]() {
-      asm volatile("bar.sync 1, 96;" ::: "memory");
-      if (trace && pt == 0) trace[53] = (unsigned long long)clock64();
-      {
-        const uint16_t* wst = reinterpret_cast<const uint16_t*>(a_s);
-        const int nrows = min(BN, a.K - nbase);
-        for (int idx = pt; idx < BN * CH && !(a.dbg & 2); idx += kProd) {
-          const int n = idx % BN, ch = idx / BN, k0 = ch * 8;
-          uint32_t v[4] = {0u, 0u, 0u, 0u};
-          if constexpr (WIDE) {
-            // k = r K_r + s C_w + c (K_r = S_pad C_w): zero for s >= S, c >= C
-            const int r = k0 / a.kr, s0 = (k0 - r * a.kr) >> (a.wide == 8 ? 3 : (a.wide == 4 ? 2 : 1));
-            if (a.wide == 8) wide_wchunk<8>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
-            else if (a.wide == 4) wide_wchunk<4>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
-            else wide_wchunk<2>(wst + n * a.Kg + r * a.S * C, v, s0, a.S, C, n < nrows && r < a.R);
-            if (a.bias_mma && k0 == 0) {
-              // bias = b1 + b2 + b3 exactly (three bf16 parts of the fp32 value) on
-              // pixel s = 0, channels C..C+2 (C_w = 8: chunk 0 is that pixel)
-              const float bf = (a.has_bias && n < nrows) ? __ldg(a.bias + nbase + n) : 0.0f;
-              const __nv_bfloat16 b1 = __float2bfloat16_rn(bf);
-              const float r1 = bf - __bfloat162float(b1);
-              const __nv_bfloat16 b2 = __float2bfloat16_rn(r1);
-              const __nv_bfloat16 b3 = __float2bfloat16_rn(r1 - __bfloat162float(b2));
-              const uint32_t p1 = __bfloat16_as_ushort(b1), p2 = __bfloat16_as_ushort(b2), p3 = __bfloat16_as_ushort(b3);
-#pragma unroll
-              for (int c = 0; c < 8; ++c) {
-                const int j = c - C;
-                const uint32_t pv = j == 0 ? p1 : (j == 1 ? p2 : p3);
-                if (j >= 0 && j < 3) v[c >> 1] |= pv << ((c & 1) * 16);
-              }
-            }
-          } else {
-            const int lim = n < nrows ? a.Kg - k0 : 0;   // elements j < lim of the chunk are W[n][k0 + j]
-            const uint16_t* src = wst + n * a.Kg + k0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (j < lim) v[j >> 1] |= (uint32_t)src[j] << ((j & 1) * 16);
-          }
-          const uint32_t off = (uint32_t)n * 128 + ((uint32_t)(((k0 & 63) >> 3) ^ (n & 7)) << 4);
-          *reinterpret_cast<uint4*>(b_s + (size_t)(k0 >> 6) * B_SUB + off) = make_uint4(v[0], v[1], v[2], v[3]);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(b_full);
-      if (trace && pt == 0) trace[2] = (unsigned long long)clock64();
-    };
     const int WC = a.W * C;
     const int nw = prow >> 1;   // 4-byte words per patch row
     // Stream tile t's patch into buffer pb: with cp.async (4-byte words, zero
@@ -363,7 +368,8 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       }
       if (trace && pt == 0) trace[52] = (unsigned long long)clock64();
       asm volatile("cp.async.wait_group 2;" ::: "memory");   // the weights (older than the kPDT tiles)
-      repack_weights();
+      asm volatile("bar.sync 1, 96;" ::: "memory");
+      repack_weights(pt, kProd);
       int sl = 0, rbi = 0;             // ring slot / raw buffer of the next row to widen
       uint32_t freeph = 0xFFFFFFFFu;   // bit s: parity that passes slot s's next free wait (first: free)
       const int pw8 = a.pcolsw;
@@ -441,9 +447,6 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       else asm volatile("cp.async.commit_group;" ::: "memory");
     }
     if (trace && pt == 0) trace[52] = (unsigned long long)clock64();
-    if (PD == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-    else asm volatile("cp.async.wait_group 1;" ::: "memory");
-    repack_weights();
     for (int i = 0; i < ntl; ++i) {
       const int b = i & 1;
       const uint16_t* patch = reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(patch0) +
@@ -456,7 +459,10 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       // Tile buffer b is free once the MMAs of tile i-2 are done: warp 0 polls,
       // the named barrier releases the other producer warps (and publishes
       // every thread's landed patch copies).
-      if (warp == 0) mbar_wait(a_empty + b, ((uint32_t)(i >> 1) & 1u) ^ 1u);
+      if (warp == 0) {
+        mbar_wait(a_empty + b, ((uint32_t)(i >> 1) & 1u) ^ 1u);
+        if (i == (wraw_b1 ? 1 : 0)) mbar_wait(b_full, 0);   // the raw weights in this buffer are repacked
+      }
       asm volatile("bar.sync 1, 96;" ::: "memory");
       if (trace && pt == 0 && i < 8) trace[44 + i] = (unsigned long long)clock64();
       uint8_t* at = a_s + (size_t)b * NSUB * A_SUB;
@@ -603,6 +609,13 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     // y_tma: the tile is staged in its own buffer in the swizzled box layout of
     // a 3-D [N P][Q][K] map (q >= Q clipped by the store) and written by one
     // 2-D-per-column-block TMA store; else 16-byte row stores.
+    if (w_epi) {
+      if (!a.w_early) issue_weights((int)threadIdx.x - 128, 128);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      repack_weights((int)threadIdx.x - 128, 128);
+      if (trace && threadIdx.x == 128) trace[2] = (unsigned long long)clock64();
+    }
     const int quad = warp & 3;
     const int row = (BM == 128) ? quad * 32 + lane : quad * 16 + lane;
     const bool row_ok = (BM == 128 || lane < 16);
