@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     // ---------------- producers ----------------
     const int pt = threadIdx.x;
     if (warp == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (trace && pt == 0) trace[54] = (unsigned long long)clock64();
     const uint16_t* xg = reinterpret_cast<const uint16_t*>(a.xg);
     if (!w_epi && !a.w_early) issue_weights(pt, kProd);
 
@@ -442,9 +443,11 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       }
     } else {
     const int PD = a.pdist;
+    if (trace && pt == 0) trace[55] = (unsigned long long)clock64();
     for (int j = 0; j < PD; ++j) {
       if (j < ntl) stage_patch(j);
       else asm volatile("cp.async.commit_group;" ::: "memory");
+      if (trace && pt == 0) trace[56 + j] = (unsigned long long)clock64();
     }
     if (trace && pt == 0) trace[52] = (unsigned long long)clock64();
     for (int i = 0; i < ntl; ++i) {

@@ -27,8 +27,11 @@ print(d["name"], {k: s[k] for k in ("kind", "bm", "bn", "stages", "tiles_per_cta
       "ctas run", len(tr), "threads", m["threads_per_cta"])
 print("median cycles from entry: prologue", int(np.median(rel(1))), "end", int(np.median(rel(3))),
       *(("weights staged", int(np.median(rel(2)))) if (tr[:, 2] > 0).all() else ()),
-      *(("| stem: patches issued", int(np.median(rel(52))), "weights landed", int(np.median(rel(53))))
-        if (tr[:, 53] > 0).all() else ()))
+      *(("| stem: first patches issued", int(np.median(rel(52)))) if (tr[:, 52] > 0).all() else ()),
+      *(("weights landed", int(np.median(rel(53)))) if (tr[:, 53] > 0).all() else ()),
+      *(("| stem: after trigger", int(np.median(rel(54))), "before staging", int(np.median(rel(55))),
+         "patch 0", int(np.median(rel(56))), "patch 1", int(np.median(rel(57))))
+        if (tr[:, 57] > 0).all() else ()))
 for name, base in (("loads issued", 4), ("stem: a free", 44), ("tile built", 36), ("MMAs issued", 12), ("acc ready", 28), ("drained", 20)):
     print(f"  {name:13s}", [int(np.median(rel(base + i))) for i in range(8) if (tr[:, base + i] > 0).all()])
 d_tile = np.diff(np.stack([rel(20 + i) for i in range(8) if (tr[:, 20 + i] > 0).all()], 1), axis=1)
