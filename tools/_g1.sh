@@ -1,2 +1,2 @@
 cd /root/repo
-for i in 344 348; do timeout 120 python tools/mt_trace.py resnet50 r50.conv1 $i 1.0; done > gpurun_out/st_r50.log 2>&1
+timeout 600 python tools/gap_trace.py profiles/r02_bench.json r50.l1.b0.c1,r50.l2.b0.c2,r50.l3.b0.c2,r50.l4.b0.c1 > gpurun_out/gap.log 2>&1

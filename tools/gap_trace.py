@@ -9,6 +9,16 @@ breakdown of the last launch.
   python tools/gap_trace.py profiles/r02_bench_first.json [layer,layer,...] [fraction] [catalog]
 """
 import json
+import sys
+
+
+def _load_json(path):
+    """A JSON file, or the last JSON line of a bench.py stdout capture."""
+    text = open(path).read()
+    try:
+        return json.loads(text)
+    except ValueError:
+        return json.loads([ln for ln in text.splitlines() if ln.strip().startswith('{')][-1])
 import os
 import sys
 
@@ -18,7 +28,7 @@ import numpy as np  # noqa: E402
 from paper_2008_03602_b200 import datagen, tp, workloads as wl  # noqa: E402
 
 tp.init(0)
-src = json.load(open(sys.argv[1]))
+src = _load_json(sys.argv[1])
 rows = src["latency_us"]["per_layer"] if "latency_us" in src else src["layers"]
 best = {r["layer"]: r["space_index"] for r in rows}
 names = sys.argv[2].split(",") if len(sys.argv) > 2 and sys.argv[2] else list(best)

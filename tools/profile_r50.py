@@ -4,9 +4,20 @@ full captures.  usage: profile_r50.py best.json [reps] [layer,layer,...]
 (best.json: {layer name: space_index}, or a bench.py JSON line)."""
 import json
 import sys
+
+
+def _load_json(path):
+    """A JSON file, or the last JSON line of a bench.py stdout capture."""
+    text = open(path).read()
+    try:
+        return json.loads(text)
+    except ValueError:
+        return json.loads([ln for ln in text.splitlines() if ln.strip().startswith('{')][-1])
+
+
 sys.path.insert(0, '.')
 from paper_2008_03602_b200 import datagen, tp, workloads as wl
-src = json.load(open(sys.argv[1]))
+src = _load_json(sys.argv[1])
 if "latency_us" in src:
     src = {r["layer"]: r["space_index"] for r in src["latency_us"]["per_layer"]}
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
