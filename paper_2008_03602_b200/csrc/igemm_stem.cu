@@ -119,9 +119,18 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   // start on a 4-byte word, since q0 s_w C is even).
   const int C = a.C, prow = a.prow, sh1 = a.psh;   // (16-byte mode: a 16-byte boundary, psh = (-p_w C) mod 8)
 
+  // ring path: the raw copy goes to the output staging buffer (unused until
+  // the first drain) when it fits, and the epilogue warps repack it too.
+  const bool wraw_b1 = !WIDE && (size_t)BN * a.Kg * 2 <= (size_t)NSUB * A_SUB;
+  const bool wraw_stg = WIDE && (size_t)BN * a.Kg * 2 <= (size_t)BM * BN * (a.out_f32 ? 4 : 2);
+  uint8_t* wraw = WIDE ? (wraw_stg ? smem_raw + a.recv_off : a_s) : (a_s + (wraw_b1 ? (size_t)NSUB * A_SUB : 0));
+  const bool w_epi = !WIDE || wraw_stg;   // who copies and repacks: warps 4-7, else the producer warp(s)
+  // (one producer warp for the ring path was tried: VGG conv1_1 86.9 -> 105 us,
+  // the per-row copy + widen chain is latency-bound, three warps overlap it)
+  constexpr int kProdR = kProd;
   if (warp == 0 && lane == 0) {
     if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
-    mbar_init(b_full, WIDE ? 3 : 4);
+    mbar_init(b_full, w_epi ? 4 : 3);
     for (int i = 0; i < 2; ++i) {
       mbar_init(a_full + i, 3);
       mbar_init(a_empty + i, 1);
@@ -156,9 +165,6 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   // im2col path: the raw copy lands in the second tile buffer when it fits and
   // is repacked by the epilogue warps (idle until the first accumulator), so the
   // producers start on the patches at once; the ring path repacks in the producers.
-  const bool wraw_b1 = !WIDE && (size_t)BN * a.Kg * 2 <= (size_t)NSUB * A_SUB;
-  uint8_t* wraw = WIDE ? a_s : (a_s + (wraw_b1 ? (size_t)NSUB * A_SUB : 0));
-  const bool w_epi = !WIDE;   // who copies and repacks: warps 4-7 (else 0-2)
   auto issue_weights = [&](int tid, int nthr) {
     const int nrows = min(BN, a.K - nbase);
     const int64_t wbytes = (int64_t)nrows * a.Kg * 2;
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
   };
   if (a.w_early) {
     if (w_epi && warp >= 4) issue_weights((int)threadIdx.x - 128, 128);
-    else if (!w_epi && warp < 3) issue_weights((int)threadIdx.x, kProd);
+    else if (!w_epi && warp < 3) issue_weights((int)threadIdx.x, kProdR);
   }
   tc_fence_before();
   __syncthreads();
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
     if (warp == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (trace && pt == 0) trace[54] = (unsigned long long)clock64();
     const uint16_t* xg = reinterpret_cast<const uint16_t*>(a.xg);
-    if (!w_epi && !a.w_early) issue_weights(pt, kProd);
+    if (!w_epi && !a.w_early) issue_weights(pt, kProdR);
 
     const int WC = a.W * C;
     const int nw = prow >> 1;   // 4-byte words per patch row
@@ -320,7 +326,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
         const uint16_t* xr = xg + ((int64_t)n * a.H + (hv ? h : 0)) * WC;
         uint16_t* pr = reinterpret_cast<uint16_t*>(rawb + (size_t)rb * a.rrow);
         if (a.pc_async == 2) {
-          for (int vi = pt; vi < (prow >> 3); vi += kProd) {
+          for (int vi = pt; vi < (prow >> 3); vi += kProdR) {
             const int g = e0 + 8 * vi;
             const bool ok = hv && g >= 0 && g < WC;
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(pr + 8 * vi)),
@@ -328,7 +334,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
                          : "memory");
           }
         } else if (a.pc_async == 1) {
-          for (int wi = pt; wi < nw; wi += kProd) {
+          for (int wi = pt; wi < nw; wi += kProdR) {
             const int g = e0 + 2 * wi;
             const bool ok = hv && g >= 0 && g < WC;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(pr + 2 * wi)),
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
                          : "memory");
           }
         } else {
-          for (int e = pt; e < prow; e += kProd) {
+          for (int e = pt; e < prow; e += kProdR) {
             const int g = e0 + e;
             pr[e] = (hv && (unsigned)g < (unsigned)WC) ? __ldg(xr + g) : (uint16_t)0;
           }
@@ -368,9 +374,11 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
         else asm volatile("cp.async.commit_group;" ::: "memory");
       }
       if (trace && pt == 0) trace[52] = (unsigned long long)clock64();
-      asm volatile("cp.async.wait_group 2;" ::: "memory");   // the weights (older than the kPDT tiles)
-      asm volatile("bar.sync 1, 96;" ::: "memory");
-      repack_weights(pt, kProd);
+      if (!w_epi) {
+        asm volatile("cp.async.wait_group 2;" ::: "memory");   // the weights (older than the kPDT tiles)
+        asm volatile("bar.sync 1, 96;" ::: "memory");
+        repack_weights(pt, kProdR);
+      }
       int sl = 0, rbi = 0;             // ring slot / raw buffer of the next row to widen
       uint32_t freeph = 0xFFFFFFFFu;   // bit s: parity that passes slot s's next free wait (first: free)
       const int pw8 = a.pcolsw;
@@ -394,7 +402,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
             if (++s2 == NS) s2 = 0;
           }
         }
-        asm volatile("bar.sync 1, 96;" ::: "memory");
+        asm volatile("bar.sync 1, 96;" ::: "memory");   // every thread's row copies landed, the slots are free
         // widen rows k < nnew: pixel u of row k -> slot (sl + k) % NS
         int k = 0, u = pt;
         while (u >= pw8 && k < nnew) { u -= pw8; ++k; }
@@ -418,7 +426,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
           } else {
             widen_px<2, 0, false>(rawr, wr, u, a.pcols, sh1, C);
           }
-          u += kProd;
+          u += kProdR;
           while (u >= pw8 && k < nnew) { u -= pw8; ++k; }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -607,7 +615,7 @@ __global__ void __launch_bounds__(256) igemm_stem_kernel(const __grid_constant__
       tc_commit_p(t_full + b, lead);
       if (trace && lane == 0 && i < 8) trace[12 + i] = (unsigned long long)clock64();
     }
-  } else {
+  } else if (warp >= 4) {
     // ---------------- epilogue (warps 4-7) ----------------
     // y_tma: the tile is staged in its own buffer in the swizzled box layout of
     // a 3-D [N P][Q][K] map (q >= Q clipped by the store) and written by one

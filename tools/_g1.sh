@@ -1,2 +1,4 @@
 cd /root/repo
-timeout 600 python tools/gap_trace.py profiles/r02_bench.json r50.l1.b0.c1,r50.l2.b0.c2,r50.l3.b0.c2,r50.l4.b0.c1 > gpurun_out/gap.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -k "stem" > gpurun_out/st_pytest.log 2>&1
+tail -1 gpurun_out/st_pytest.log
+timeout 300 python tools/stem_probe.py > gpurun_out/st_probe_1.log 2>&1
