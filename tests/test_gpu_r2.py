@@ -135,6 +135,15 @@ def test_vgg_full_size_every_kind_vs_oracle(li):
     win = _vgg_exhaustive_winners().get(d["name"])
     if win is not None and win[0] == tp.space_size(d):
         chosen.append(tp.space_get(d, win[1]))
+    # the round-2 code paths at full size: the resident-weight row kind with two
+    # MMA-issuing warps (N = 64, ring >= 2 tiles of k-blocks) and both stem paths
+    # (ring for >= 4 tiles per CTA, im2col tile below)
+    for kind, pred in ((tp.KIND_IGEMM_TC_ROWW, lambda s: s["bn"] == 64 and s["stages"] >= 6),
+                       (tp.KIND_IGEMM_TC_STEM, lambda s: s["tiles_per_cta"] >= 4),
+                       (tp.KIND_IGEMM_TC_STEM, lambda s: s["tiles_per_cta"] <= 2)):
+        extra = [s for s in kinds_of(d).get(kind, []) if pred(s)]
+        if extra:
+            chosen.append(extra[len(extra) // 2])
     bad = []
     for s in chosen:
         s = dict(s, sm_tuned=part.sm_granted)
