@@ -10,6 +10,7 @@
 //  10 = 3 with the 8 KB written by one bulk copy (cp.async.bulk smem -> global), wait_group.read
 //  11 = 10 with wait_group 0 (writes complete) before the exit
 //  12 = 3 with 2 KB per CTA, 13 = 3 with 32 KB per CTA
+//  P  = 1 with a 1 KB __grid_constant__ parameter block (the conv kernels pass ~0.9 KB)
 // usage: launch_gap [ctas=100] [threads=256]     Build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o launch_gap launch_gap.cu
 #include <cuda_runtime.h>
@@ -86,6 +87,50 @@ __global__ void __launch_bounds__(256) k(const uint4* __restrict__ x, uint4* __r
   }
 }
 
+struct Big { unsigned char b[1024]; };
+
+__global__ void __launch_bounds__(256) kbig(const __grid_constant__ Big p, uint4* __restrict__ y) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.b[threadIdx.x] == 0xAB && threadIdx.x == 1023) y[0] = make_uint4(1, 1, 1, 1);
+}
+
+static float period_big(int ctas, int threads, uint4* y, cudaStream_t st, int n) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  Big p = {};
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  for (int i = 0; i < n; ++i) cudaLaunchKernelEx(&cfg, kbig, p, y);
+  cudaStreamEndCapture(st, &g);
+  cudaGraphInstantiate(&ge, g, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int w = 0; w < 3; ++w) cudaGraphLaunch(ge, st);
+  float best = 1e30f;
+  for (int r = 0; r < 7; ++r) {
+    cudaEventRecord(e0, st);
+    cudaGraphLaunch(ge, st);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  return best * 1000.0f / n;
+}
+
 template <int V>
 static float period(int ctas, int threads, const uint4* x, uint4* y, cudaStream_t st, int n) {
   cudaLaunchAttribute at[1];
@@ -146,6 +191,7 @@ int main(int argc, char** argv) {
   printf("11 = 8 KB bulk, done    %.3f\n", period<11>(ctas, threads, x, y, st, n));
   printf("12 = 2 KB stores        %.3f\n", period<12>(ctas, threads, x, y, st, n));
   printf("13 = 32 KB stores       %.3f\n", period<13>(ctas, threads, x, y, st, n));
+  printf("P = 1 + 1 KB params     %.3f\n", period_big(ctas, threads, y, st, n));
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return 0;
