@@ -24,7 +24,7 @@
  *   - libtp owns green contexts, their streams and events, TMA descriptors and
  *     the kernel instantiation table; tp_shutdown() frees them.
  *   - Host-only functions (tp_space_*, tp_output_shape, tp_select_best,
- *     tp_gate_points, tp_search_next, tp_status_str, tp_last_error) never
+ *     tp_gate_points, tp_search_next, tp_search_should_stop, tp_status_str, tp_last_error) never
  *     touch the GPU and work without one.
  *   - Threading: one tuner thread per partition; calls on *different*
  *     partitions may run concurrently from different host threads (a green
@@ -305,6 +305,25 @@ tp_status tp_tune_guided(const tp_conv_desc* d, tp_partition* part, int32_t tria
                          size_t ws_bytes, const int64_t* check_idx, const double* check_ref, int32_t n_check,
                          double tol, const tp_timing* timing, tp_schedule* best, tp_measurement* best_m,
                          tp_measurement* records, int32_t records_cap, int32_t* n_records);
+
+/* Early stopping ("halts tuning if a newer
+ * configuration generated by the explorer is worse than previously profiled
+ * configurations", "stops tuning, when the new configurations ... do not
+ * show latency improvement"; reading C19: TVM's rule, a patience count).
+ * us[0..n): measured medians in measurement order, < 0 = a candidate that
+ * failed (never an improvement).  Returns 1 when the last `early_stop`
+ * candidates did not lower the best latency measured before them (strictly),
+ * 0 otherwise; early_stop <= 0: never stops.  Host-only. */
+int32_t tp_search_should_stop(const double* us, int32_t n, int32_t early_stop);
+
+/* tp_tune_guided that checks tp_search_should_stop(records so far,
+ * early_stop) after every batch and stops there (early_stop <= 0: exactly
+ * tp_tune_guided). */
+tp_status tp_tune_guided_es(const tp_conv_desc* d, tp_partition* part, int32_t trials, int32_t batch, double explore,
+                            uint64_t seed, int32_t early_stop, const void* x, const void* w, const void* bias, void* y,
+                            void* ws, size_t ws_bytes, const int64_t* check_idx, const double* check_ref,
+                            int32_t n_check, double tol, const tp_timing* timing, tp_schedule* best,
+                            tp_measurement* best_m, tp_measurement* records, int32_t records_cap, int32_t* n_records);
 
 /* Cross-evaluation: run schedule tuned at p (frozen geometry, reading C15)
  * inside partition `part_q` with the timing protocol (a13). */

@@ -1583,6 +1583,15 @@ tp_status tp_tune_guided(const tp_conv_desc* d, tp_partition* part, int32_t tria
                          size_t ws_bytes, const int64_t* check_idx, const double* check_ref, int32_t n_check,
                          double tol, const tp_timing* timing, tp_schedule* best, tp_measurement* best_m,
                          tp_measurement* records, int32_t cap, int32_t* n_records) {
+  return tp_tune_guided_es(d, part, trials, batch, explore, seed, 0, x, w, bias, y, ws, ws_bytes, check_idx,
+                           check_ref, n_check, tol, timing, best, best_m, records, cap, n_records);
+}
+
+tp_status tp_tune_guided_es(const tp_conv_desc* d, tp_partition* part, int32_t trials, int32_t batch, double explore,
+                            uint64_t seed, int32_t early_stop, const void* x, const void* w, const void* bias, void* y,
+                            void* ws, size_t ws_bytes, const int64_t* check_idx, const double* check_ref,
+                            int32_t n_check, double tol, const tp_timing* timing, tp_schedule* best,
+                            tp_measurement* best_m, tp_measurement* records, int32_t cap, int32_t* n_records) {
   Layer L;
   tp_status st = make_layer(d, &L);
   if (st != TP_OK) return st;
@@ -1612,6 +1621,7 @@ tp_status tp_tune_guided(const tp_conv_desc* d, tp_partition* part, int32_t tria
       idx.push_back(brec[i].space_index);
       us.push_back(brec[i].status == TP_OK ? brec[i].median_us : -1.0);
     }
+    if (tp_search_should_stop(us.data(), (int32_t)us.size(), early_stop)) break;   // reading C19
   }
   const int32_t nrec = (int32_t)recs.size();
   if (records) std::memcpy(records, recs.data(), sizeof(tp_measurement) * std::min(cap, nrec));

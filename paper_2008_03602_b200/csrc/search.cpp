@@ -227,3 +227,18 @@ tp_status tp_search_next(const tp_conv_desc* d, int32_t sm_granted, const int64_
 }
 
 }  // extern "C"
+
+// Early stopping (tp.h): the last `early_stop` measured candidates did not
+// strictly lower the best latency measured before them.
+extern "C" int32_t tp_search_should_stop(const double* us, int32_t n, int32_t early_stop) {
+  if (early_stop <= 0 || !us || n < early_stop) return 0;
+  double best = -1.0;   // < 0: nothing valid measured yet
+  int32_t last_improve = -1;
+  for (int32_t i = 0; i < n; ++i) {
+    if (us[i] >= 0.0 && (best < 0.0 || us[i] < best)) {
+      best = us[i];
+      last_improve = i;
+    }
+  }
+  return (n - 1 - last_improve) >= early_stop ? 1 : 0;
+}

@@ -112,6 +112,10 @@ _sig("tp_tune_subset", _P(ConvDesc), _vp, _P(_i64), _i32, _vp, _vp, _vp, _vp, _v
 _sig("tp_search_next", _P(ConvDesc), _i32, _P(_i64), _P(_dbl), _i32, _i32, _dbl, _u64, _P(_i64), _P(_i32))
 _sig("tp_tune_guided", _P(ConvDesc), _vp, _i32, _i32, _dbl, _u64, _vp, _vp, _vp, _vp, _vp, _sz, _P(_i64), _P(_dbl),
      _i32, _dbl, _P(Timing), _P(Schedule), _P(Measurement), _P(Measurement), _i32, _P(_i32))
+_sig("tp_tune_guided_es", _P(ConvDesc), _vp, _i32, _i32, _dbl, _u64, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _P(_i64),
+     _P(_dbl), _i32, _dbl, _P(Timing), _P(Schedule), _P(Measurement), _P(Measurement), _i32, _P(_i32))
+_lib.tp_search_should_stop.argtypes = [_P(_dbl), _i32, _i32]
+_lib.tp_search_should_stop.restype = _i32
 _sig("tp_cross_eval", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(Timing), _P(Measurement))
 _sig("tp_conv2d_trace", _P(ConvDesc), _P(Schedule), _vp, _vp, _vp, _vp, _vp, _vp, _sz, _P(_u64), _i32, _P(_i32))
 _sig("tp_chain_run", _i32, _P(ConvDesc), _P(Schedule), _vp, _P(_vp), _P(_vp), _P(_vp), _P(_vp), _P(_vp), _P(_sz), _i32,
@@ -463,20 +467,29 @@ def tune(buf: LayerBuffers, part: Partition | None, trials: int, seed: int, chec
     return sched_to_dict(best), meas_to_dict(best_m), records
 
 
+def search_should_stop(us, early_stop: int) -> bool:
+    """Early-stopping rule (tp_search_should_stop, reading C19): the last
+    `early_stop` measured candidates did not lower the best latency (us < 0 =
+    failed candidate)."""
+    a = np.ascontiguousarray(us, dtype=np.float64)
+    return bool(_lib.tp_search_should_stop(a.ctypes.data_as(_P(_dbl)), int(a.shape[0]), int(early_stop)))
+
+
 def tune_guided(buf: "LayerBuffers", part: Partition | None, trials: int, batch: int = 16, explore: float = 0.25,
-                seed: int = 42, tol: float = 0.0, timing_cfg: Timing | None = None):
-    """Model-guided tuning (tp_tune_guided): (best schedule, best measurement, records)."""
+                seed: int = 42, tol: float = 0.0, timing_cfg: Timing | None = None, early_stop: int = 0):
+    """Model-guided tuning (tp_tune_guided_es; early_stop = 0: tp_tune_guided):
+    (best schedule, best measurement, records in measurement order)."""
     x, w, b, y, ws, wsb = buf.ptrs()
     cap = max(1, min(trials, space_size(buf.d)))
     recs = (Measurement * cap)()
     nrec = _i32()
     best, best_m = Schedule(), Measurement()
-    st = _lib.tp_tune_guided(ctypes.byref(buf.cd), _h(part), int(trials), int(batch), float(explore),
-                             int(seed) & (2**64 - 1), x, w, b, y, ws, wsb, None, None, 0, float(tol),
-                             ctypes.byref(timing_cfg) if timing_cfg is not None else None, ctypes.byref(best),
-                             ctypes.byref(best_m), recs, cap, ctypes.byref(nrec))
+    st = _lib.tp_tune_guided_es(ctypes.byref(buf.cd), _h(part), int(trials), int(batch), float(explore),
+                                int(seed) & (2**64 - 1), int(early_stop), x, w, b, y, ws, wsb, None, None, 0,
+                                float(tol), ctypes.byref(timing_cfg) if timing_cfg is not None else None,
+                                ctypes.byref(best), ctypes.byref(best_m), recs, cap, ctypes.byref(nrec))
     records = [meas_to_dict(recs[i]) for i in range(nrec.value)]
-    _ck(st, "tp_tune_guided")
+    _ck(st, "tp_tune_guided_es")
     return sched_to_dict(best), meas_to_dict(best_m), records
 
 

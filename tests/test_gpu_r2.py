@@ -570,3 +570,29 @@ def test_stem_both_paths_every_schedule(mode):
                        text=True, timeout=900, env=dict(os.environ, TP_STEM_WIDE=mode))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout
+
+
+def test_tune_guided_early_stop_stops_at_the_first_batch_boundary_where_the_rule_holds():
+    """f1 early stopping (reading C19, P:284 / P:388): tp_tune_guided_es checks
+    tp_search_should_stop after every batch.  The records it returns must end at
+    the first batch boundary where the rule holds (or at the budget), the
+    winner is the fastest gated record, and it matches the oracle."""
+    d = mk(1, 64, 28, 28, 64, 3, 3, 1, 1, out=tp.FP32, epi=3)   # fp32 output: exact on integer data
+    x, w, b = datagen.make_inputs(d, 41, integer=True)
+    ref = oracle_ref(d, x, w, b)
+    buf = tp.LayerBuffers(d, x, w, b)
+    batch, es, trials = 8, 12, 200
+    best, best_m, recs = tp.tune_guided(buf, None, trials, batch=batch, explore=0.25, seed=5, early_stop=es,
+                                        timing_cfg=tp.timing(warmup=1, groups=2, n_min=3, target_group_us=5.0))
+    us = [r["median_us"] if r["status"] == 0 else -1.0 for r in recs]
+    n = len(us)
+    budget = min(trials, tp.space_size(d))
+    assert n <= budget and n > 0
+    for k in range(batch, n, batch):
+        assert not tp.search_should_stop(us[:k], es), k
+    assert n == budget or tp.search_should_stop(us, es)
+    ok = [r for r in recs if r["status"] == 0]
+    assert best_m["median_us"] == min(r["median_us"] for r in ok)
+    tp.conv2d_run(buf, best)
+    torch.cuda.synchronize()
+    assert np.array_equal(buf.output(), ref)

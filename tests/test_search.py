@@ -78,3 +78,21 @@ def test_bad_arguments():
         tp.search_next(D, 148, [10 ** 6], [1.0], 4)
     with pytest.raises(tp.TPError):
         tp.search_next(D, 148, [], [], 0)
+
+
+def test_early_stop_rule_hand_cases():
+    """Reading C19 (TVM stops when new configurations show no
+    latency improvement): stop once the last `early_stop` measured candidates
+    did not strictly lower the best latency measured before them."""
+    f = tp.search_should_stop
+    assert not f([], 3)
+    assert not f([5.0, 4.0, 3.0], 3)                 # every candidate improves
+    assert not f([5.0, 4.0, 6.0, 7.0], 3)            # two after the last improvement
+    assert f([5.0, 4.0, 6.0, 7.0, 4.5], 3)           # three after it
+    assert not f([5.0, 4.0, 6.0, 4.0], 3)            # a tie is no improvement, but only two so far
+    assert f([5.0, 4.0, 6.0, 4.0, 4.0], 3)
+    assert f([5.0, 4.0, 6.0, 4.0, 4.0, 3.9], 3) is False   # the newest one improves
+    assert f([-1.0, -1.0, -1.0], 3)                  # failed candidates never improve
+    assert not f([-1.0, -1.0, 2.0], 3)               # the first valid one is an improvement
+    assert not f([9.0] * 10, 0)                      # early_stop <= 0: never
+    assert f([1.0] + [2.0] * 5, 5) and not f([1.0] + [2.0] * 4, 5)
