@@ -1388,6 +1388,14 @@ static size_t tc_bar_off(int bm, int bn, int bk, int stages, bool cluster_red, b
   return (off + 1023) & ~(size_t)1023;
 }
 
+// L2 promotion of the A (activation) tensor maps (TP_A_PROMO = 0 / 64 / 128 / 256 bytes; default 128)
+static CUtensorMapL2promotion a_promotion() {
+  static const int v = getenv("TP_A_PROMO") ? atoi(getenv("TP_A_PROMO")) : 128;
+  return v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                  : (v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                             : (v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_128B));
+}
+
 static bool ystage2_enabled() {
   static const bool on = !(getenv("TP_YSTAGE2") && atoi(getenv("TP_YSTAGE2")) == 0);
   return on;
@@ -1773,7 +1781,7 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
     cuuint32_t a_box[2] = {(cuuint32_t)sub_k, (cuuint32_t)pb.bm};
     cuuint32_t a_estr[2] = {1, 1};
     r = drv.encodeTiled(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pb.x), a_dims, a_strides,
-                        a_box, a_estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        a_box, a_estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, a_promotion(),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
       set_error("cuTensorMapEncodeTiled (1x1 A) failed (" + std::to_string((int)r) + ")");
@@ -1788,7 +1796,7 @@ tp_status tc_prepare(const TcProblem& pb, TcPlan* plan) {
   cuuint32_t a_estr[4] = {1, (cuuint32_t)pb.sw, (cuuint32_t)pb.sh, 1};
   r = drv.encodeIm2col(&plan->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pb.x), a_dims,
                        a_strides, lower, upper, (cuuint32_t)sub_k, (cuuint32_t)pb.bm, a_estr,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz, a_promotion(),
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")");
